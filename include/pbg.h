@@ -1,0 +1,143 @@
+/*
+ * pbg.h — C-ABI of the B200-native PB-SpGEMM hot path.
+ *
+ * C = A * B with A in CSC and B in CSR, C in CSR: outer-product expand into
+ * row-range bins, per-bin sort + duplicate merge, CSR assembly — the path of
+ * spgemm::pb_multiply (reference: proj/include/spgemm/pb_spgemm.hpp:116,
+ * proj/src/pb_spgemm.cpp:330-361), re-implemented as sm_100a CUDA kernels.
+ *
+ * The reference has no FFI layer: its boundary is the C++ call
+ *     spgemm::PbResult spgemm::pb_multiply(const CscMatrix&, const CsrMatrix&,
+ *                                          const PbConfig& = {});
+ * This header is what that C++ entry point is re-implemented on top of
+ * (include/spgemm_b200/pb_spgemm.hpp, the drop-in); INTEGRATION.md shows the
+ * binding. Plain pointers and sizes only: no torch, no CUDA types.
+ *
+ * No CPU fallback: without a CUDA device every compute entry point returns
+ * PBG_ERR_NODEVICE.
+ */
+#ifndef PBG_H
+#define PBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes. The C++ drop-in maps DIM/NBINS/LBIN/FLOP_OVERFLOW to
+ * spgemm::parameter_error (reference types.hpp:80-83, pb_spgemm.cpp:88-89,
+ * :103-105, :252-253), INTERNAL to spgemm::internal_error (types.hpp:89-91,
+ * pb_spgemm.cpp:241-245, :342-345, :358-359) and the rest to
+ * std::runtime_error. */
+enum {
+    PBG_OK = 0,
+    PBG_ERR_DIM = 1,            /* a.ncols != b.nrows              (types.hpp:97-102)  */
+    PBG_ERR_NBINS = 2,          /* cfg.nbins not a power of two    (pb_spgemm.cpp:88)  */
+    PBG_ERR_LBIN = 3,           /* lbin_bytes not k*16, k>0        (pb_spgemm.cpp:252) */
+    PBG_ERR_FLOP_OVERFLOW = 4,  /* flop does not fit 64 bits       (pb_spgemm.cpp:103) */
+    PBG_ERR_INTERNAL = 5,       /* a conservation self-check failed                    */
+    PBG_ERR_CUDA = 6,
+    PBG_ERR_OOM = 7,
+    PBG_ERR_NCCL = 8,
+    PBG_ERR_ARG = 9,            /* null pointer / malformed view                        */
+    PBG_ERR_UNIMPLEMENTED = 10,
+    PBG_ERR_NODEVICE = 11
+};
+
+/* A borrowed compressed-sparse view. For CSC: nrows x ncols, ptr = colptr
+ * [ncols+1], idx = rowids [nnz]; for CSR: ptr = rowptr [nrows+1], idx = colids.
+ * Field meaning follows spgemm::CscMatrix / CsrMatrix (types.hpp:51-69):
+ * u64 offsets, u32 indices, f64 values. */
+typedef struct pbg_csx_view {
+    uint32_t nrows;
+    uint32_t ncols;
+    uint64_t nnz;
+    const uint64_t* ptr;
+    const uint32_t* idx;
+    const double* val;
+} pbg_csx_view;
+
+/* spgemm::PbConfig (pb_spgemm.hpp:11-17) plus GPU fields. The reference
+ * fields keep their validation contract; on the GPU nbins/l2_bytes/
+ * balanced_bins only shape the REFERENCE-layout symbolic report
+ * (pbg_symbolic_fetch), nthreads and lbin_bytes' staging role have no GPU
+ * meaning. The GPU bins are sized to shared memory. */
+typedef struct pbg_config {
+    uint32_t nbins;        /* 0 = auto (choose_nbins), else a power of two */
+    uint32_t lbin_bytes;   /* must be a positive multiple of 16            */
+    uint64_t l2_bytes;     /* reference L2 sizing input (default 1 MiB)     */
+    int32_t nthreads;      /* ignored on the GPU                           */
+    int32_t balanced_bins; /* reference-layout report only                 */
+    int32_t device;        /* CUDA ordinal, -1 = current device            */
+    uint32_t bin_cap;      /* GPU bin capacity in tuples, 0 = default 4096 */
+    uint64_t reserved[4];
+} pbg_config;
+
+/* spgemm::PhaseReport times (report.hpp:26-33) measured with CUDA events,
+ * plus the acceptance counters (acceptance.cpp:46-58). The fused sort+merge+
+ * CSR kernel is reported in t_sort; t_compress and t_convert are 0. */
+typedef struct pbg_report {
+    double t_symbolic, t_expand, t_sort, t_compress, t_convert, t_total; /* seconds */
+    double t_h2d, t_d2h;  /* host path only                                       */
+    uint64_t flop, nnz_c, nnz_a, nnz_b;
+    uint64_t tuples_into_sort; /* sum of expand fill cursors                      */
+    uint64_t merged_total;     /* sum of per-bin merged counts                    */
+    uint32_t nbins;            /* reference-layout bin count (choose_nbins rule) */
+    uint32_t gpu_bins;         /* shared-memory bins actually used on the GPU     */
+    uint32_t heavy_bins;       /* bins larger than bin_cap (global-memory path)   */
+    uint32_t bin_cap;
+    uint64_t tuple_bytes;      /* bytes of tuple storage (12 B per tuple + pad)   */
+} pbg_report;
+
+typedef struct pbg_handle pbg_handle;
+typedef struct pbg_context pbg_context;
+
+/* Thread-local message for the last non-zero return on this thread. */
+const char* pbg_last_error(void);
+void pbg_default_config(pbg_config* cfg);
+/* 1 when a CUDA device is usable, else 0. */
+int pbg_device_available(void);
+
+/* ---- host-buffer path: the drop-in for pb_multiply ------------------- */
+/* Copies A (CSC) and B (CSR) from host memory, runs the pipeline and keeps C
+ * on the device. *nnz_c receives nnz(C) so the caller can size its arrays. */
+int pbg_multiply_begin(const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
+                       const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_c);
+/* D2H of C into caller-owned rowptr[m+1], colids[nnz], values[nnz]; rep may
+ * be NULL. */
+int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
+                       pbg_report* rep);
+/* The reference SymbolicResult (pb_spgemm.hpp:48-55) on the REFERENCE bin
+ * layout: per_column_flop[a.ncols], per_bin_flop[nbins], bin_row_starts
+ * [nbins+1]; nbins from pbg_report.nbins. Any pointer may be NULL. */
+int pbg_symbolic_fetch(pbg_handle* h, uint64_t* per_column_flop, uint64_t* per_bin_flop,
+                       uint32_t* bin_row_starts);
+void pbg_release(pbg_handle* h);
+
+/* ---- device-resident path: inputs already in HBM --------------------- */
+int pbg_context_create(int device, pbg_context** out);
+void pbg_context_destroy(pbg_context* ctx);
+/* Views hold DEVICE pointers. stream is a cudaStream_t (NULL = legacy default).
+ * Blocks until nnz(C) is known. C stays in the context until the next call. */
+int pbg_multiply_device(pbg_context* ctx, const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
+                        const pbg_config* cfg, void* stream, uint64_t* nnz_c, pbg_report* rep);
+/* Device pointers to the last product's CSR arrays (valid until the next
+ * pbg_multiply_device on this context). */
+int pbg_context_result(pbg_context* ctx, const uint64_t** rowptr, const uint32_t** colids,
+                       const double** values);
+/* Reference-layout symbolic arrays of the last product (host destinations). */
+int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg, uint64_t* per_column_flop,
+                         uint64_t* per_bin_flop, uint32_t* bin_row_starts);
+/* Kernel launches issued by the last pbg_multiply_device call. */
+uint32_t pbg_context_launches(pbg_context* ctx);
+
+/* ---- reference helpers with no device work --------------------------- */
+/* choose_nbins (pb_spgemm.cpp:10-18) */
+uint32_t pbg_choose_nbins(uint64_t flop, uint32_t nrows, uint64_t l2_bytes, uint32_t tuple_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBG_H */

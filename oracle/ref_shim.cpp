@@ -1,0 +1,243 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the UNMODIFIED reference library (compiled from
+// /root/reference/proj/src/*.cpp by oracle/build_ref.sh into oracle/_ref/).
+// It lets the Python tests and bench.py's reference/cpu_baseline arm call the
+// reference's own entry points through ctypes:
+//   spgemm::pb_multiply           proj/include/spgemm/pb_spgemm.hpp:116
+//   spgemm::symbolic/make_bins/expand/sort_bins/compress_bins/convert_csr
+//                                 proj/include/spgemm/pb_spgemm.hpp:59-108
+//   spgemm::gen_er / gen_rmat     proj/include/spgemm/generate.hpp:65-69
+//   spgemm::coo_to_csc/coo_to_csr proj/include/spgemm/convert.hpp:8-9
+//   spgemm::reference_multiply    proj/include/spgemm/reference.hpp:12
+// Exceptions are turned into return codes: 1 parameter_error, 2 internal_error,
+// 3 anything else; the message goes to ref_last_error().
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "spgemm/convert.hpp"
+#include "spgemm/generate.hpp"
+#include "spgemm/pb_spgemm.hpp"
+#include "spgemm/reference.hpp"
+
+using namespace spgemm;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const parameter_error& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const internal_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+CscMatrix make_csc(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint64_t* ptr,
+                   const uint32_t* idx, const double* val) {
+    CscMatrix m;
+    m.dims = {nrows, ncols};
+    m.colptr.assign(ptr, ptr + ncols + 1);
+    m.rowids.assign(idx, idx + nnz);
+    m.values.assign(val, val + nnz);
+    return m;
+}
+
+CsrMatrix make_csr(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint64_t* ptr,
+                   const uint32_t* idx, const double* val) {
+    CsrMatrix m;
+    m.dims = {nrows, ncols};
+    m.rowptr.assign(ptr, ptr + nrows + 1);
+    m.colids.assign(idx, idx + nnz);
+    m.values.assign(val, val + nnz);
+    return m;
+}
+
+PbConfig make_cfg(uint32_t nbins, uint32_t lbin, uint64_t l2, int nthreads, int balanced) {
+    PbConfig c;
+    c.nbins = nbins;
+    c.lbin_bytes = lbin;
+    c.l2_bytes = l2;
+    c.nthreads = nthreads;
+    c.balanced_bins = balanced != 0;
+    return c;
+}
+
+struct RefResult {
+    CsrMatrix c;
+    SymbolicResult sym;
+    PhaseReport phases;
+    uint64_t tuples_into_sort = 0;
+    uint64_t merged_total = 0;
+};
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// ---- generators (values 1.0 as the reference emits them) ----
+int ref_gen(int kind, int scale, uint32_t ef, uint64_t seed, void** out) {
+    return guarded([&] {
+        auto* m = new CooMatrix(kind == 0 ? gen_er(GenSpec::er(scale, ef, seed))
+                                          : gen_rmat(GenSpec::rmat(scale, ef, seed)));
+        *out = m;
+    });
+}
+
+uint64_t ref_coo_nnz(void* h) { return static_cast<CooMatrix*>(h)->nnz(); }
+
+void ref_coo_get(void* h, uint32_t* rows, uint32_t* cols, double* vals) {
+    auto* m = static_cast<CooMatrix*>(h);
+    for (size_t i = 0; i < m->entries.size(); ++i) {
+        rows[i] = m->entries[i].row;
+        cols[i] = m->entries[i].col;
+        vals[i] = m->entries[i].val;
+    }
+}
+
+void ref_coo_free(void* h) { delete static_cast<CooMatrix*>(h); }
+
+// ---- conversion: COO -> CSC (major=col) or CSR (major=row) ----
+// Caller gives ptr of size nmajor+1 and idx/val of size nnz (upper bound);
+// *nnz_out gets the merged count.
+int ref_coo_convert(int to_csr, uint32_t nrows, uint32_t ncols, uint64_t nnz,
+                    const uint32_t* rows, const uint32_t* cols, const double* vals,
+                    uint64_t* ptr, uint32_t* idx, double* val, uint64_t* nnz_out) {
+    return guarded([&] {
+        CooMatrix m;
+        m.dims = {nrows, ncols};
+        m.entries.resize(nnz);
+        for (uint64_t i = 0; i < nnz; ++i) m.entries[i] = {rows[i], cols[i], vals[i]};
+        if (to_csr) {
+            CsrMatrix r = coo_to_csr(m);
+            std::memcpy(ptr, r.rowptr.data(), r.rowptr.size() * 8);
+            std::memcpy(idx, r.colids.data(), r.colids.size() * 4);
+            std::memcpy(val, r.values.data(), r.values.size() * 8);
+            *nnz_out = r.nnz();
+        } else {
+            CscMatrix c = coo_to_csc(m);
+            std::memcpy(ptr, c.colptr.data(), c.colptr.size() * 8);
+            std::memcpy(idx, c.rowids.data(), c.rowids.size() * 4);
+            std::memcpy(val, c.values.data(), c.values.size() * 8);
+            *nnz_out = c.nnz();
+        }
+    });
+}
+
+// ---- the hot path: pb_multiply (stepwise=1 runs the stepwise API to expose
+// the conservation counters, as acceptance.cpp:46-58 does) ----
+int ref_pb_multiply(uint32_t a_nrows, uint32_t a_ncols, uint64_t a_nnz, const uint64_t* a_colptr,
+                    const uint32_t* a_rowids, const double* a_vals, uint32_t b_nrows,
+                    uint32_t b_ncols, uint64_t b_nnz, const uint64_t* b_rowptr,
+                    const uint32_t* b_colids, const double* b_vals, uint32_t nbins,
+                    uint32_t lbin_bytes, uint64_t l2_bytes, int nthreads, int balanced,
+                    int stepwise, void** out) {
+    return guarded([&] {
+        const CscMatrix a = make_csc(a_nrows, a_ncols, a_nnz, a_colptr, a_rowids, a_vals);
+        const CsrMatrix b = make_csr(b_nrows, b_ncols, b_nnz, b_rowptr, b_colids, b_vals);
+        const PbConfig cfg = make_cfg(nbins, lbin_bytes, l2_bytes, nthreads, balanced);
+        auto* r = new RefResult;
+        try {
+            if (stepwise) {
+                r->sym = symbolic(a, b, cfg);
+                BinSet bins = make_bins(r->sym, {a.dims.nrows, b.dims.ncols});
+                expand(a, b, bins, cfg);
+                r->tuples_into_sort = bins.total_filled();
+                sort_bins(bins, cfg);
+                compress_bins(bins, cfg);
+                r->merged_total = bins.total_merged();
+                r->c = convert_csr(bins);
+            } else {
+                PbResult res = pb_multiply(a, b, cfg);
+                r->c = std::move(res.c);
+                r->sym = std::move(res.sym);
+                r->phases = res.phases;
+                r->tuples_into_sort = r->sym.flop;
+                r->merged_total = r->c.nnz();
+            }
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        *out = r;
+    });
+}
+
+uint64_t ref_res_nnz(void* h) { return static_cast<RefResult*>(h)->c.nnz(); }
+uint32_t ref_res_nbins(void* h) { return static_cast<RefResult*>(h)->sym.nbins; }
+
+void ref_res_get(void* h, uint64_t* rowptr, uint32_t* colids, double* vals) {
+    auto* r = static_cast<RefResult*>(h);
+    std::memcpy(rowptr, r->c.rowptr.data(), r->c.rowptr.size() * 8);
+    std::memcpy(colids, r->c.colids.data(), r->c.colids.size() * 4);
+    std::memcpy(vals, r->c.values.data(), r->c.values.size() * 8);
+}
+
+// counters[0..3] = flop, tuples_into_sort, merged_total, uniform_rows_per_bin
+void ref_res_counters(void* h, uint64_t* counters) {
+    auto* r = static_cast<RefResult*>(h);
+    counters[0] = r->sym.flop;
+    counters[1] = r->tuples_into_sort;
+    counters[2] = r->merged_total;
+    counters[3] = r->sym.uniform_rows_per_bin;
+}
+
+// per_column_flop[ncols(A)], per_bin_flop[nbins], bin_row_starts[nbins+1]
+void ref_res_symbolic(void* h, uint64_t* per_column_flop, uint64_t* per_bin_flop,
+                      uint32_t* bin_row_starts) {
+    auto* r = static_cast<RefResult*>(h);
+    std::memcpy(per_column_flop, r->sym.per_column_flop.data(),
+                r->sym.per_column_flop.size() * 8);
+    std::memcpy(per_bin_flop, r->sym.per_bin_flop.data(), r->sym.per_bin_flop.size() * 8);
+    std::memcpy(bin_row_starts, r->sym.bin_row_starts.data(),
+                r->sym.bin_row_starts.size() * 4);
+}
+
+// t_symbolic, t_expand, t_sort, t_compress, t_convert, t_total (seconds)
+void ref_res_times(void* h, double* t) {
+    auto* r = static_cast<RefResult*>(h);
+    t[0] = r->phases.t_symbolic;
+    t[1] = r->phases.t_expand;
+    t[2] = r->phases.t_sort;
+    t[3] = r->phases.t_compress;
+    t[4] = r->phases.t_convert;
+    t[5] = r->phases.t_total;
+}
+
+void ref_res_free(void* h) { delete static_cast<RefResult*>(h); }
+
+// choose_nbins (pb_spgemm.cpp:10-18) for the KATs
+uint32_t ref_choose_nbins(uint64_t flop, uint32_t nrows, uint64_t l2_bytes, uint32_t tuple_bytes) {
+    PbConfig c;
+    c.l2_bytes = l2_bytes;
+    return choose_nbins(flop, nrows, c, tuple_bytes);
+}
+
+// dense oracle (reference.cpp:8-35) on COO input; output COO in a handle
+int ref_dense_multiply(uint32_t m, uint32_t k, uint32_t n, uint64_t annz, const uint32_t* ar,
+                       const uint32_t* ac, const double* av, uint64_t bnnz, const uint32_t* br,
+                       const uint32_t* bc, const double* bv, void** out) {
+    return guarded([&] {
+        CooMatrix a, b;
+        a.dims = {m, k};
+        b.dims = {k, n};
+        for (uint64_t i = 0; i < annz; ++i) a.entries.push_back({ar[i], ac[i], av[i]});
+        for (uint64_t i = 0; i < bnnz; ++i) b.entries.push_back({br[i], bc[i], bv[i]});
+        *out = new CooMatrix(reference_multiply(a, b));
+    });
+}
+
+}  // extern "C"

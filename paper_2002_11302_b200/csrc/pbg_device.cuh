@@ -1,0 +1,150 @@
+// pbg_device.cuh — device building blocks shared by the PB-SpGEMM kernels:
+// warp/block scans, the decoupled look-back used by every single-pass scan
+// and by the sort+merge kernel's output offsets, and small search helpers.
+#pragma once
+
+#include <cstdint>
+
+namespace pbg {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Look-back status word: 2 flag bits + 62-bit value.
+constexpr uint64_t ST_AGG = 1ull << 62;
+constexpr uint64_t ST_INC = 2ull << 62;
+constexpr uint64_t ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint64_t ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ void st_volatile(unsigned long long* p, uint64_t v) {
+    *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    return x;
+}
+
+// Block-wide exclusive scan of one value per thread. s_warp needs NT/32+1
+// slots. Returns the exclusive prefix and the block total. Ends with a
+// __syncthreads so s_warp can be reused immediately.
+template <int NT, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* s_warp, T& total) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T x = warp_inclusive_scan(v);
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        T t = lane < NW ? s_warp[lane] : T(0);
+        T inc = warp_inclusive_scan(t);
+        if (lane < NW) s_warp[lane] = inc - t;
+        if (lane == NW - 1) s_warp[NW] = inc;
+    }
+    __syncthreads();
+    T excl = s_warp[w] + x - v;
+    total = s_warp[NW];
+    __syncthreads();
+    return excl;
+}
+
+// Decoupled look-back (single-pass chained scan). Called by one full warp of
+// the CTA owning `tile`; publishes `aggregate`, walks predecessors 32 at a
+// time, publishes the inclusive prefix and returns the exclusive prefix
+// (same value in every lane). Predecessors always hold an earlier ticket, so
+// they are resident or finished: no deadlock.
+__device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, uint64_t tile,
+                                                  uint64_t aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) {
+            __threadfence();
+            st_volatile(&status[0], ST_INC | (aggregate & ST_VAL));
+        }
+        return 0;
+    }
+    if (lane == 0) {
+        __threadfence();
+        st_volatile(&status[tile], ST_AGG | (aggregate & ST_VAL));
+    }
+    uint64_t prefix = 0;
+    int64_t idx = static_cast<int64_t>(tile) - 1;
+    while (true) {
+        const int64_t j = idx - lane;
+        uint64_t s = j >= 0 ? ld_volatile(&status[j]) : ST_INC;
+        while (__any_sync(FULL, (s >> 62) == 0)) {
+            if ((s >> 62) == 0) s = ld_volatile(&status[j]);
+        }
+        const uint32_t inc = __ballot_sync(FULL, (s >> 62) == 2);
+        if (inc) {
+            const int first = __ffs(inc) - 1;
+            uint64_t v = lane <= first ? (s & ST_VAL) : 0;
+            prefix += warp_sum(v);
+            break;
+        }
+        prefix += warp_sum(s & ST_VAL);
+        idx -= 32;
+    }
+    if (lane == 0) {
+        __threadfence();
+        st_volatile(&status[tile], ST_INC | ((prefix + aggregate) & ST_VAL));
+    }
+    return prefix;
+}
+
+// Largest i in [lo, hi) with a[i] <= x, assuming a[lo] <= x and a nondecreasing.
+__device__ __forceinline__ uint64_t last_le(const uint64_t* __restrict__ a, uint64_t lo,
+                                            uint64_t hi, uint64_t x) {
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (a[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Warp-cooperative version of last_le: 32 probes per round. Every lane gets
+// the same answer.
+__device__ __forceinline__ uint64_t warp_last_le(const uint64_t* __restrict__ a, uint64_t lo,
+                                                 uint64_t hi, uint64_t x) {
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 1) {
+        const uint64_t span = hi - lo;
+        const uint64_t step = (span + 31) / 32;
+        const uint64_t probe = lo + static_cast<uint64_t>(lane) * step;
+        const bool ok = probe < hi && a[probe] <= x;
+        const uint32_t m = __ballot_sync(FULL, ok);
+        // m is a prefix of lanes (a is sorted); at least lane 0 holds.
+        const int cnt = __popc(m);
+        const uint64_t nlo = lo + static_cast<uint64_t>(cnt - 1) * step;
+        uint64_t nhi = nlo + step;
+        if (nhi > hi) nhi = hi;
+        lo = nlo;
+        hi = nhi;
+        if (step == 1) break;
+    }
+    return lo;
+}
+
+}  // namespace pbg

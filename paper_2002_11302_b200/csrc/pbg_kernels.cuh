@@ -1,0 +1,600 @@
+// pbg_kernels.cuh — the sm_100a kernels of the PB-SpGEMM hot path.
+//
+//   symbolic  : k_colflop_total, k_scan<ColFlop>, k_rowflop, k_scan<RowFlop>,
+//               k_binflags, k_scan<Flags>, k_binrows, k_binsizes, k_scan<Pad>
+//               (reference symbolic + make_bins, pb_spgemm.cpp:86-176)
+//   expand    : k_chunks, k_expand           (expand_impl, pb_spgemm.cpp:180-246)
+//   sort/merge: k_sortmerge — per-bin smem radix sort, duplicate merge, CSR
+//               rows written at look-back offsets (sort_bins + compress_bins +
+//               convert_csr, pb_spgemm.cpp:260-328, pb_spgemm.hpp:118-216)
+//
+// Tuple layout (the reference BinSet's keys32 + values SoA, pb_spgemm.hpp:
+// 84-86): key = (row - bin_row_start) << col_bits | col as u32, value f64.
+// GPU bins are contiguous row ranges sized to one CTA's shared memory.
+#pragma once
+
+#include <cstdint>
+
+#include "pbg_device.cuh"
+
+namespace pbg {
+
+// ---------------------------------------------------------------- scans --
+constexpr int SCAN_NT = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_ITEMS;
+
+// Exclusive scan out[0..n) of in(i), out[n] = total, single pass with
+// decoupled look-back. n may live in device memory (n_dev) when the host does
+// not know it; tiles at or beyond n exit. Optional max of the inputs.
+template <class In>
+__global__ void __launch_bounds__(SCAN_NT)
+k_scan(In in, uint64_t* out, uint64_t n_host, const uint64_t* n_dev, unsigned long long* status,
+       unsigned int* ticket, unsigned long long* total_out, unsigned long long* max_out) {
+    __shared__ uint64_t s_items[SCAN_TILE];
+    __shared__ uint64_t s_warp[SCAN_NT / 32 + 1];
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_prefix;
+    const int tid = threadIdx.x;
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * SCAN_TILE;
+    if (base >= n && !(base == 0)) return;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const uint64_t i = base + j * SCAN_NT + tid;
+        s_items[j * SCAN_NT + tid] = i < n ? in(i) : 0;
+    }
+    __syncthreads();
+    uint64_t loc[SCAN_ITEMS];
+    uint64_t sum = 0, mx = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        loc[j] = s_items[tid * SCAN_ITEMS + j];
+        sum += loc[j];
+        mx = loc[j] > mx ? loc[j] : mx;
+    }
+    uint64_t total;
+    const uint64_t excl = block_exclusive_scan<SCAN_NT>(sum, s_warp, total);
+    if (tid < 32) {
+        const uint64_t p = lookback_warp(status, tile, total);
+        if (tid == 0) s_prefix = p;
+    }
+    if (max_out) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(FULL, mx, o);
+            mx = y > mx ? y : mx;
+        }
+        if ((tid & 31) == 0) atomicMax(max_out, static_cast<unsigned long long>(mx));
+    }
+    __syncthreads();
+    uint64_t run = s_prefix + excl;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        s_items[tid * SCAN_ITEMS + j] = run;
+        run += loc[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        const uint64_t i = base + j * SCAN_NT + tid;
+        if (i < n) out[i] = s_items[j * SCAN_NT + tid];
+    }
+    if (base + SCAN_TILE >= n && tid == 0) {
+        out[n] = s_prefix + total;
+        if (total_out) *total_out = s_prefix + total;
+    }
+}
+
+// per_column_flop[i] = nnz(A(:,i)) * nnz(B(i,:))   (pb_spgemm.cpp:98-101)
+struct ColFlopIn {
+    const uint64_t* a_colptr;
+    const uint64_t* b_rowptr;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        return (a_colptr[i + 1] - a_colptr[i]) * (b_rowptr[i + 1] - b_rowptr[i]);
+    }
+};
+
+struct ArrayIn {
+    const uint64_t* a;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
+};
+
+// 128-bit accumulation of the per-column flop so an overflow of the 64-bit
+// total is detected exactly (pb_spgemm.cpp:103-105). also rejects totals the
+// 62-bit look-back cannot carry.
+__global__ void k_colflop_total(const uint64_t* __restrict__ a_colptr,
+                                const uint64_t* __restrict__ b_rowptr, uint64_t k,
+                                unsigned long long* lo_out, unsigned long long* hi_out) {
+    uint64_t lo = 0, hi = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t la = a_colptr[i + 1] - a_colptr[i];
+        const uint64_t lb = b_rowptr[i + 1] - b_rowptr[i];
+        const uint64_t f = la * lb;
+        hi += __umul64hi(la, lb);
+        const uint64_t s = lo + f;
+        hi += s < lo;
+        lo = s;
+    }
+    // warp reduce lo with carries
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t olo = __shfl_xor_sync(FULL, lo, o);
+        const uint64_t ohi = __shfl_xor_sync(FULL, hi, o);
+        const uint64_t s = lo + olo;
+        hi += ohi + (s < lo);
+        lo = s;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        const unsigned long long old = atomicAdd(lo_out, static_cast<unsigned long long>(lo));
+        if (old + lo < old) hi += 1;
+        if (hi) atomicAdd(hi_out, static_cast<unsigned long long>(hi));
+    }
+}
+
+// row_flop[r] += nnz(B(k,:)) for every A(r,k)  (bin_flop / balanced_starts,
+// pb_spgemm.cpp:36-82, at row granularity). Thread per column; long columns
+// are walked by the whole warp.
+__global__ void k_rowflop(const uint64_t* __restrict__ a_colptr,
+                          const uint32_t* __restrict__ a_rowids,
+                          const uint64_t* __restrict__ b_rowptr, uint64_t k,
+                          unsigned long long* row_flop) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t p0 = 0, p1 = 0, lb = 0;
+    if (i < k) {
+        lb = b_rowptr[i + 1] - b_rowptr[i];
+        if (lb) {
+            p0 = a_colptr[i];
+            p1 = a_colptr[i + 1];
+        }
+    }
+    const bool longcol = (p1 - p0) > 64;
+    if (!longcol)
+        for (uint64_t p = p0; p < p1; ++p) atomicAdd(&row_flop[a_rowids[p]], (unsigned long long)lb);
+    uint32_t lm = __ballot_sync(FULL, longcol);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint64_t q0 = __shfl_sync(FULL, p0, src), q1 = __shfl_sync(FULL, p1, src);
+        const uint64_t qb = __shfl_sync(FULL, lb, src);
+        for (uint64_t p = q0 + lane; p < q1; p += 32)
+            atomicAdd(&row_flop[a_rowids[p]], (unsigned long long)qb);
+    }
+}
+
+// Bin boundaries (GPU bin layout). A row starts a bin when its
+// flop prefix enters a new window of T tuples, at every MAXR-aligned row,
+// and around every row heavier than H (those become single-row bins). All
+// non-heavy bins then hold < T + H = cap tuples and <= MAXR rows.
+struct BinParams {
+    uint64_t cap;   // tuples per bin (smem capacity)
+    uint32_t maxr;  // rows per bin (2^(32-col_bits), <= 1024)
+};
+
+__global__ void k_binflags(const uint64_t* __restrict__ row_flop,
+                           const uint64_t* __restrict__ row_off, uint64_t m, BinParams bp,
+                           const unsigned long long* max_row_flop, uint64_t* flags) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint64_t mx = *max_row_flop;
+    const uint64_t h = mx < bp.cap / 4 ? mx : bp.cap / 4;
+    const uint64_t t = bp.cap - h;
+    uint64_t f;
+    if (r == 0 || (r % bp.maxr) == 0) {
+        f = 1;
+    } else {
+        const bool heavy = row_flop[r] > h, heavy_prev = row_flop[r - 1] > h;
+        f = heavy || heavy_prev || (row_off[r] / t != row_off[r - 1] / t);
+    }
+    flags[r] = f;
+}
+
+// row -> bin id, bin -> first row.
+__global__ void k_binrows(const uint64_t* __restrict__ flag_excl, uint64_t m, uint32_t* row_bin,
+                          uint32_t* bin_rs) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint64_t e = flag_excl[r], e1 = flag_excl[r + 1];
+    const uint32_t b = static_cast<uint32_t>(e1 - 1);  // inclusive - 1
+    row_bin[r] = b;
+    if (e1 != e) bin_rs[b] = static_cast<uint32_t>(r);
+    if (r == m - 1) bin_rs[e1] = static_cast<uint32_t>(m);
+}
+
+// Per-bin tuple count, 4-tuple padded capacity (16-B aligned key runs),
+// cursor/status reset, heavy-bin count.
+__global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
+                           const uint64_t* __restrict__ row_off, const uint64_t* nb_dev,
+                           uint64_t cap, uint64_t* bin_cnt, uint64_t* bin_pad,
+                           unsigned long long* cursor, unsigned long long* status,
+                           unsigned long long* heavy, unsigned long long* maxbin) {
+    const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (b >= *nb_dev) return;
+    const uint64_t c = row_off[bin_rs[b + 1]] - row_off[bin_rs[b]];
+    bin_cnt[b] = c;
+    bin_pad[b] = (c + 3) & ~3ull;
+    cursor[b] = 0;
+    status[b] = 0;
+    if (c > cap) atomicAdd(heavy, 1ull);
+    atomicMax(maxbin, static_cast<unsigned long long>(c));
+}
+
+// ---------------------------------------------------------------- expand --
+// Chunk c owns the runs (A entries) whose tuple range starts in
+// [c*CH, (c+1)*CH); chunk_p0[c] is its first A entry.
+__global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
+                         const uint64_t* __restrict__ a_colptr,
+                         const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t nnz_a,
+                         uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0) {
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (c > nchunks) return;
+    if (c == nchunks) {
+        chunk_p0[c] = nnz_a;
+        return;
+    }
+    const uint64_t t0 = c * ch;
+    const uint64_t col = last_le(colflop_off, 0, k, t0);  // off[col] <= t0 < off[col+1]
+    const uint64_t lb = b_rowptr[col + 1] - b_rowptr[col];
+    const uint64_t rel = t0 - colflop_off[col];
+    const uint64_t i = (rel + lb - 1) / lb;
+    chunk_p0[c] = a_colptr[col] + i;
+}
+
+struct ExpandArgs {
+    const uint64_t* a_colptr;
+    const uint32_t* a_rowids;
+    const double* a_vals;
+    const uint64_t* b_rowptr;
+    const uint32_t* b_colids;
+    const double* b_vals;
+    uint64_t a_ncols;
+    const uint64_t* chunk_p0;
+    uint64_t nchunks;
+    const uint32_t* row_bin;
+    const uint32_t* bin_rs;
+    const uint64_t* bin_off;
+    unsigned long long* cursor;
+    uint32_t* keys;
+    double* vals;
+    int col_bits;
+};
+
+constexpr int EXP_NT = 256;
+constexpr int EXP_NW = EXP_NT / 32;
+
+// Outer-product expansion (expand_impl, pb_spgemm.cpp:180-246). One warp per
+// chunk. Runs are processed 32 at a time, one per lane: the lane resolves the
+// run's column k (shuffle search over 32 colptr boundaries), its bin, and
+// reserves nnz(B(k,:)) slots in the bin with one atomicAdd on the bin cursor
+// (the GPU version of the reference's `omp atomic capture` range
+// reservation). The batch's tuples are then streamed flat, 32 per step, each
+// lane finding its run with a redux.or over run-start bits, so stores of a
+// run are coalesced and no lane idles on short runs. The 126 MB L2 plays the
+// role of the reference's thread-private local bins: each bin's write
+// frontier stays resident until its lines are full.
+__global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
+    __shared__ uint64_t s_dst[EXP_NW][32];
+    __shared__ uint64_t s_bst[EXP_NW][32];
+    __shared__ double s_av[EXP_NW][32];
+    __shared__ uint64_t s_st[EXP_NW][32];
+    __shared__ uint32_t s_rp[EXP_NW][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lt = lanemask_lt();
+    const int cb = a.col_bits;
+
+    for (uint64_t c = gw; c < a.nchunks; c += nw) {
+        uint64_t p = a.chunk_p0[c];
+        const uint64_t pend = a.chunk_p0[c + 1];
+        if (p >= pend) continue;
+        uint64_t kcur = warp_last_le(a.a_colptr, 0, a.a_ncols, p);
+        while (p < pend) {
+            const uint64_t pl = p + lane;
+            const bool valid = pl < pend;
+            // column of run pl: kcur + #{j : colptr[kcur+1+j] <= pl}
+            const uint64_t bi = kcur + 1 + lane;
+            const uint64_t bnd = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
+            int cnt = 0;
+#pragma unroll
+            for (int s = 16; s >= 1; s >>= 1) {
+                const uint64_t v = __shfl_sync(FULL, bnd, cnt + s - 1);
+                if (v <= pl) cnt += s;
+            }
+            {
+                const uint64_t v = __shfl_sync(FULL, bnd, cnt & 31);
+                if (cnt == 31 && v <= pl) cnt = 32;
+            }
+            uint64_t kl = kcur + cnt;
+            if (valid && cnt == 32) kl = last_le(a.a_colptr, kcur, a.a_ncols, pl);
+            uint64_t lb = 0, bst = 0, dst = 0;
+            uint32_t rp = 0;
+            double av = 0.0;
+            if (valid) {
+                bst = a.b_rowptr[kl];
+                lb = a.b_rowptr[kl + 1] - bst;
+                if (lb) {
+                    const uint32_t r = a.a_rowids[pl];
+                    av = a.a_vals[pl];
+                    const uint32_t bin = a.row_bin[r];
+                    const uint32_t rs = a.bin_rs[bin];
+                    const uint64_t pos = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
+                    dst = a.bin_off[bin] + pos;
+                    rp = static_cast<uint32_t>((static_cast<uint64_t>(r - rs)) << cb);
+                }
+            }
+            const bool ne = lb != 0;
+            const uint32_t nemask = __ballot_sync(FULL, ne);
+            const int rank = __popc(nemask & lt);
+            uint64_t incl = warp_inclusive_scan(lb);
+            const uint64_t start = incl - lb;
+            const uint64_t total = __shfl_sync(FULL, incl, 31);
+            if (ne) {
+                s_dst[w][rank] = dst;
+                s_bst[w][rank] = bst;
+                s_av[w][rank] = av;
+                s_st[w][rank] = start;
+                s_rp[w][rank] = rp;
+            }
+            __syncwarp();
+            uint32_t before = 0;
+            for (uint64_t s = 0; s < total; s += 32) {
+                const uint32_t bit =
+                    (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
+                const uint32_t mk = __reduce_or_sync(FULL, bit);
+                const uint64_t t = s + lane;
+                if (t < total) {
+                    const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+                    const int ri = before + __popc(mk & upto) - 1;
+                    const uint64_t q = t - s_st[w][ri];
+                    const uint64_t src = s_bst[w][ri] + q;
+                    const uint32_t key = s_rp[w][ri] | a.b_colids[src];
+                    const double v = s_av[w][ri] * a.b_vals[src];
+                    const uint64_t d = s_dst[w][ri] + q;
+                    a.keys[d] = key;
+                    a.vals[d] = v;
+                }
+                before += __popc(mk);
+            }
+            __syncwarp();
+            const int last = (pend - p) < 32 ? static_cast<int>(pend - p) - 1 : 31;
+            kcur = __shfl_sync(FULL, kl, last);
+            p += 32;
+        }
+    }
+}
+
+// ----------------------------------------------------------- sort+merge --
+constexpr int SM_NT = 512;
+constexpr int SM_NW = SM_NT / 32;
+constexpr int SM_CAP = 4096;                 // max tuples per smem bin
+constexpr int SM_PER_WARP = SM_CAP / SM_NW;  // 256
+constexpr int SM_ITEMS = SM_PER_WARP / 32;   // 8
+
+struct SortArgs {
+    const uint32_t* bin_rs;
+    const uint64_t* bin_cnt;
+    const uint64_t* bin_off;
+    const unsigned long long* cursor;
+    const uint64_t* nb_dev;
+    unsigned long long* status;
+    unsigned int* ticket;
+    uint32_t* keys;  // tuple keys in, C colids out (in place)
+    double* vals;    // tuple values in, C values out (in place)
+    uint64_t* rowptr;
+    uint64_t m;
+    int col_bits;
+    unsigned long long* tuples_total;
+    unsigned long long* merged_total;
+    unsigned int* err;  // bit0 conservation, bit1 heavy bin reached the smem path
+};
+
+struct SortSmem {
+    uint32_t k[2][SM_CAP];
+    double v[2][SM_CAP];
+    uint16_t cnt[256 * SM_NW];
+    uint32_t s_warp32[SM_NW + 1];
+    uint64_t s_bin;
+    uint64_t s_prefix;
+};
+
+// Per-bin sort + merge + CSR rows (sort_bins/compress_bins/convert_csr,
+// pb_spgemm.cpp:260-328). Persistent CTAs take bins in ticket order, so the
+// output offset of bin b is the look-back prefix of the merged counts of
+// bins < b, and C is written straight to its final place. C overlays the
+// tuple arrays: bin b writes [P_b, P_b+U_b) with P_b+U_b <= off_{b+1}, and
+// every bin < b has finished reading before it published its count.
+// Sort: stable LSD radix on 8-bit digits over only the key bits the bin uses
+// (row bits of its span + col bits — the reference skips constant bytes,
+// pb_spgemm.hpp:188-195, to the same effect); ranks from match.any per warp,
+// per-(digit, warp) counters scanned digit-major.
+__global__ void __launch_bounds__(SM_NT, 2) k_sortmerge(SortArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    const uint64_t nb = *a.nb_dev;
+    const int cb = a.col_bits;
+    const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
+
+    while (true) {
+        if (tid == 0) sm.s_bin = atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const uint64_t b = sm.s_bin;
+        if (b >= nb) break;
+        const uint32_t rs = a.bin_rs[b], re = a.bin_rs[b + 1];
+        const uint64_t n = a.bin_cnt[b];
+        const uint64_t off = a.bin_off[b];
+        if (tid == 0) {
+            const uint64_t cur = a.cursor[b];
+            if (cur != n) atomicOr(a.err, 1u);
+            atomicAdd(a.tuples_total, (unsigned long long)cur);
+        }
+        int cbuf = 0;
+        uint32_t U = 0;
+        if (n > SM_CAP) {
+            if (tid == 0) atomicOr(a.err, 2u);
+        } else if (n > 0) {
+            // ---- stage the bin in shared memory (16-B vector loads) ----
+            const uint4* k4 = reinterpret_cast<const uint4*>(a.keys + off);
+            const double2* v2 = reinterpret_cast<const double2*>(a.vals + off);
+            const uint32_t n4 = static_cast<uint32_t>((n + 3) / 4);
+            for (uint32_t i = tid; i < n4; i += SM_NT) {
+                const uint4 kk = __ldcs(k4 + i);
+                *reinterpret_cast<uint4*>(&sm.k[0][4 * i]) = kk;
+            }
+            const uint32_t n2 = static_cast<uint32_t>((n + 1) / 2);
+            for (uint32_t i = tid; i < n2; i += SM_NT) {
+                const double2 vv = __ldcs(v2 + i);
+                *reinterpret_cast<double2*>(&sm.v[0][2 * i]) = vv;
+            }
+            __syncthreads();
+            // ---- LSD radix sort over the used key bits ----
+            const uint32_t span = re - rs;
+            const int rbits = span > 1 ? 32 - __clz(span - 1) : 0;
+            const int bits = rbits + cb;
+            uint32_t kr[SM_ITEMS];
+#pragma unroll
+            for (int it = 0; it < SM_ITEMS; ++it) {
+                const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+                kr[it] = idx < n ? sm.k[0][idx] : 0u;
+            }
+            if (n > 1) {
+                for (int shift = 0; shift < bits; shift += 8) {
+                    for (int i = tid; i < 256 * SM_NW / 2; i += SM_NT)
+                        reinterpret_cast<uint32_t*>(sm.cnt)[i] = 0u;
+                    __syncthreads();
+                    uint16_t rank[SM_ITEMS];
+                    uint32_t dig[SM_ITEMS];
+#pragma unroll
+                    for (int it = 0; it < SM_ITEMS; ++it) {
+                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+                        const bool valid = idx < n;
+                        const uint32_t d = valid ? ((kr[it] >> shift) & 0xffu) : 0x100u;
+                        const uint32_t peers = __match_any_sync(FULL, d);
+                        const uint16_t old = valid ? sm.cnt[d * SM_NW + w] : 0;
+                        rank[it] = old + __popc(peers & lt);
+                        dig[it] = d;
+                        __syncwarp();
+                        if (valid && (peers & lt) == 0) sm.cnt[d * SM_NW + w] = old + __popc(peers);
+                        __syncwarp();
+                    }
+                    __syncthreads();
+                    // exclusive scan of the 4096 counters, digit-major
+                    {
+                        uint32_t c8[8];
+                        uint32_t s8 = 0;
+                        const uint4 raw = reinterpret_cast<const uint4*>(sm.cnt)[tid];
+                        const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            c8[2 * j] = rw[j] & 0xffffu;
+                            c8[2 * j + 1] = rw[j] >> 16;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) s8 += c8[j];
+                        uint32_t tot;
+                        uint32_t run = block_exclusive_scan<SM_NT>(s8, sm.s_warp32, tot);
+                        uint32_t ow[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t lo = run;
+                            run += c8[2 * j];
+                            const uint32_t hi = run;
+                            run += c8[2 * j + 1];
+                            ow[j] = lo | (hi << 16);
+                        }
+                        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int it = 0; it < SM_ITEMS; ++it) {
+                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+                        if (idx < n) {
+                            const uint32_t pos = sm.cnt[dig[it] * SM_NW + w] + rank[it];
+                            sm.k[cbuf ^ 1][pos] = kr[it];
+                            sm.v[cbuf ^ 1][pos] = sm.v[cbuf][idx];
+                        }
+                    }
+                    __syncthreads();
+                    cbuf ^= 1;
+#pragma unroll
+                    for (int it = 0; it < SM_ITEMS; ++it) {
+                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+                        if (idx < n) kr[it] = sm.k[cbuf][idx];
+                    }
+                }
+            }
+            // ---- merge equal keys (compress_bin_records, pb_spgemm.hpp:202-216) ----
+            {
+                const uint32_t* K = sm.k[cbuf];
+                const double* V = sm.v[cbuf];
+                uint32_t* KO = sm.k[cbuf ^ 1];
+                double* VO = sm.v[cbuf ^ 1];
+                const uint32_t i0 = tid * 8;
+                uint32_t heads = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t i = i0 + j;
+                    if (i < n && (i == 0 || K[i] != K[i - 1])) ++heads;
+                }
+                uint32_t tot;
+                uint32_t u = block_exclusive_scan<SM_NT>(heads, sm.s_warp32, tot);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t i = i0 + j;
+                    if (i < n && (i == 0 || K[i] != K[i - 1])) {
+                        const uint32_t key = K[i];
+                        double s = V[i];
+                        for (uint32_t e = i + 1; e < n && K[e] == key; ++e) s += V[e];
+                        KO[u] = key;
+                        VO[u] = s;
+                        ++u;
+                    }
+                }
+                U = tot;
+                cbuf ^= 1;
+            }
+        }
+        // ---- output offset by look-back over merged counts ----
+        if (tid < 32) {
+            const uint64_t pfx = lookback_warp(a.status, b, U);
+            if (tid == 0) sm.s_prefix = pfx;
+        }
+        __syncthreads();
+        const uint64_t P = sm.s_prefix;
+        const uint32_t* K = sm.k[cbuf];
+        const double* V = sm.v[cbuf];
+        for (uint32_t u = tid; u < U; u += SM_NT) {
+            const uint32_t key = K[u];
+            __stcs(a.keys + P + u, key & colmask);
+            __stcs(a.vals + P + u, V[u]);
+            const uint32_t row = static_cast<uint32_t>(static_cast<uint64_t>(key) >> cb);
+            const int64_t prow = u == 0 ? -1 : static_cast<int64_t>(static_cast<uint64_t>(K[u - 1]) >> cb);
+            for (int64_t r = prow + 1; r <= row; ++r) a.rowptr[rs + r] = P + u;
+        }
+        {
+            const int64_t lastrow = U == 0 ? -1 : static_cast<int64_t>(static_cast<uint64_t>(K[U - 1]) >> cb);
+            for (int64_t r = lastrow + 1 + tid; r < static_cast<int64_t>(re - rs); r += SM_NT)
+                a.rowptr[rs + r] = P + U;
+        }
+        if (tid == 0) {
+            if (b == nb - 1) a.rowptr[a.m] = P + U;
+            atomicAdd(a.merged_total, (unsigned long long)U);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_zero_u64(uint64_t* p, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = 0;
+}
+
+}  // namespace pbg
