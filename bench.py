@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""PB-SpGEMM benchmark (BASELINE.json metric: SpGEMM mults/sec + HBM GB/s as
+a fraction of the memory roofline).
+
+A *step* is one full C = A·A multiplication (symbolic + expand + sort/merge/
+CSR) of the workload on device-resident inputs. Default workload: C2 (ER
+n=2^20, d=16), the config BASELINE.json quotes its multiply count on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
+    python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
+
+N>1 (torchrun): output rows are cut into N flop-balanced bands; rank r
+multiplies its CSC row-slab of A by all of B (broadcast once over NCCL at
+setup) with no collective in the timed region ("scaling": "strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from paper_2002_11302_b200 import matrices as M  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def model_bytes(nnz_a, nnz_b, flop, nnz_c, b=16.0):
+    """The reference's traffic model (roofline.hpp:56-63, report.hpp:42-51), b=16."""
+    expand = b * (nnz_a + nnz_b + flop)
+    sort = b * (flop + nnz_c)
+    return expand, sort, expand + sort
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_inputs(cfg_name: str):
+    t = time.time()
+    a_csc, a_csr = M.make_config(cfg_name)
+    log(f"[bench] {cfg_name}: n={a_csr.nrows} nnz={a_csr.nnz} inputs built in {time.time() - t:.1f}s")
+    return a_csc, a_csr
+
+
+def cpu_reference_run(a_csc, b_csr, steps: int, warmup: int, budget_s: float, nthreads: int):
+    """Times the reference's own pb_multiply (oracle/_ref, OpenMP, all host
+    threads) on a flop-balanced leading row band of A sized to the budget."""
+    import oracle
+    impl = "reference" if oracle.ref_available() else "port"
+    kind = "reference" if impl == "reference" else "port"
+    if impl == "port":
+        nthreads = 1
+    rf = M.row_flop(a_csc, b_csr)
+    total = int(rf.sum())
+    # probe: 1/32 of the flop
+    cuts = M.band_cuts(rf, 32)
+    probe = M.row_band(a_csc, 0, int(cuts[1]))
+    t = time.perf_counter()
+    oracle.multiply(probe, b_csr, impl=impl, nthreads=nthreads)
+    rate = max(1.0, float(rf[:int(cuts[1])].sum())) / max(time.perf_counter() - t, 1e-6)
+    per_step = budget_s / max(1, steps + warmup)
+    frac = min(1.0, rate * per_step / max(total, 1))
+    g = max(1, int(round(1.0 / frac))) if frac < 1.0 else 1
+    r1 = int(M.band_cuts(rf, g)[1]) if g > 1 else a_csc.nrows
+    band = a_csc if r1 == a_csc.nrows else M.row_band(a_csc, 0, r1)
+    band_flop = int(rf[:r1].sum())
+    for _ in range(warmup):
+        oracle.multiply(band, b_csr, impl=impl, nthreads=nthreads)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        oracle.multiply(band, b_csr, impl=impl, nthreads=nthreads, stepwise=False)
+        times.append(time.perf_counter() - t)
+    med = statistics.median(times)
+    sample = (f"rows [0,{r1}) of {a_csc.nrows} ({band_flop} of {total} mults, "
+              f"{100.0 * band_flop / max(total, 1):.1f}%), median of {steps} after {warmup} warm-up")
+    return {"value": band_flop / med, "unit": "mult/s", "cores": nthreads, "kind": kind,
+            "sample": sample, "seconds_per_step": med, "times": times}
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    a_csc, a_csr = build_inputs(args.config)
+    nthreads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    res = cpu_reference_run(a_csc, a_csr, args.steps, args.warmup, args.ref_budget, nthreads)
+    line = {
+        "metric": "SpGEMM mults/sec", "value": res["value"], "unit": "mult/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY.md §8d generators)",
+        "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}"},
+        "impl": "reference",
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "mult/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_11302_b200 import api
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    a_csc, a_csr = build_inputs(args.config)
+    n = a_csr.nrows
+    nnz_a = a_csc.nnz
+    # row bands (flop-balanced), rank r owns rows [cuts[r], cuts[r+1])
+    if ws > 1:
+        cuts = M.band_cuts(M.row_flop(a_csc, a_csr), ws)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+        a_band = M.row_band(a_csc, r0, r1)
+    else:
+        r0, r1 = 0, n
+        a_band = a_csc
+
+    def to_dev(x, dt):
+        return torch.from_numpy(x.view(dt)).to(dev)
+
+    A = (to_dev(a_band.colptr, np.int64), to_dev(a_band.rowids, np.int32),
+         to_dev(a_band.values, np.float64))
+    if ws > 1:  # B broadcast once from rank 0 over NCCL (setup, untimed)
+        if rank == 0:
+            Bt = [to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
+                  to_dev(a_csr.values, np.float64)]
+        else:
+            Bt = [torch.empty(n + 1, dtype=torch.int64, device=dev),
+                  torch.empty(a_csr.nnz, dtype=torch.int32, device=dev),
+                  torch.empty(a_csr.nnz, dtype=torch.float64, device=dev)]
+        for t in Bt:
+            dist.broadcast(t, 0)
+        B = tuple(Bt)
+    else:
+        B = (to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
+             to_dev(a_csr.values, np.float64))
+    torch.cuda.synchronize()
+
+    ctx = api.DeviceContext(local)
+    va = api.DeviceContext.view(a_band.nrows, a_band.ncols, *A)
+    vb = api.DeviceContext.view(a_csr.nrows, a_csr.ncols, *B)
+    cfg = api.PbConfig(device=local)
+    stream = torch.cuda.current_stream(dev)
+
+    reps = []
+    for _ in range(args.warmup):
+        reps.append(ctx.multiply(va, vb, cfg, stream.cuda_stream)[1])
+    flop_local = reps[-1]["flop"] if reps else 0
+    nnz_local = reps[-1]["nnz_c"] if reps else 0
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    launches = 0
+    step_reps = []
+    for _ in range(args.steps):
+        _, rep = ctx.multiply(va, vb, cfg, stream.cuda_stream)
+        launches += ctx.launches()
+        step_reps.append(rep)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    t_local = ev0.elapsed_time(ev1) * 1e-3 / max(args.steps, 1)
+
+    flop_local = step_reps[-1]["flop"]
+    nnz_local = step_reps[-1]["nnz_c"]
+    t_sort = statistics.mean(r["t_sort"] for r in step_reps)
+    t_exp = statistics.mean(r["t_expand"] for r in step_reps)
+    t_sym = statistics.mean(r["t_symbolic"] for r in step_reps)
+    stats = torch.tensor([t_local, t_sort, t_exp, t_sym], dtype=torch.float64, device=dev)
+    sums = torch.tensor([flop_local, nnz_local, a_band.nnz], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    t_step, t_sort_max, t_exp_max, t_sym_max = stats.tolist()
+    flop, nnz_c, _ = (int(x) for x in sums.tolist())
+
+    # e2e through the public API with host buffers (pinned), N>1: each rank its band
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda x: torch.from_numpy(x).pin_memory().numpy()  # noqa: E731
+        ah = M.CscMatrix(a_band.nrows, a_band.ncols, pin(a_band.colptr), pin(a_band.rowids),
+                         pin(a_band.values))
+        bh = M.CsrMatrix(a_csr.nrows, a_csr.ncols, pin(a_csr.rowptr), pin(a_csr.colids),
+                         pin(a_csr.values))
+        out = (torch.empty(a_band.nrows + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+               torch.empty(max(nnz_local, 1), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+               torch.empty(max(nnz_local, 1), dtype=torch.float64).pin_memory().numpy())
+        hcfg = api.PbConfig(device=local)
+        api.pb_multiply(ah, bh, hcfg, symbolic=False, out=out)  # warm
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            res = api.pb_multiply(ah, bh, hcfg, symbolic=False, out=out)
+        te = (time.perf_counter() - t0) / args.e2e_steps
+        h2d = (a_band.colptr.nbytes + a_band.rowids.nbytes + a_band.values.nbytes +
+               a_csr.rowptr.nbytes + a_csr.colids.nbytes + a_csr.values.nbytes)
+        d2h = (a_band.nrows + 1) * 8 + res.c.nnz * 12
+        st = torch.tensor([te, h2d, d2h], dtype=torch.float64, device=dev)
+        if ws > 1:
+            t_max = st[:1].clone()
+            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+            dist.all_reduce(st, op=dist.ReduceOp.SUM)
+            st[0] = t_max[0]
+        te, h2d, d2h = st.tolist()
+        e2e = {"value": flop / te, "unit": "mult/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = peak_hbm()
+    b_exp, b_sort, b_tot = model_bytes(nnz_a, a_csr.nnz, flop, nnz_c)
+    # dominant kernel = the longer of expand and sort/merge (rank 0's own band)
+    my_b_exp, my_b_sort, _ = model_bytes(a_band.nnz, a_csr.nnz, flop_local, nnz_local)
+    kern = ("k_sortmerge", my_b_sort, t_sort) if t_sort >= t_exp else ("k_expand", my_b_exp, t_exp)
+    achieved = kern[1] / kern[2] / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"traffic_{args.config}.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(kern[0])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": kern[0], "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": kern[1],
+                "avg_launch_s": kern[2],
+                "per_phase": {
+                    "expand": {"model_bytes": my_b_exp, "s": t_exp,
+                               "GBps": my_b_exp / t_exp / 1e9 if t_exp else None,
+                               "frac": my_b_exp / t_exp / 1e9 / peak if t_exp else None},
+                    "sort_merge": {"model_bytes": my_b_sort, "s": t_sort,
+                                   "GBps": my_b_sort / t_sort / 1e9 if t_sort else None,
+                                   "frac": my_b_sort / t_sort / 1e9 / peak if t_sort else None},
+                    "symbolic_s": t_sym}}
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            res = cpu_reference_run(a_csc, a_csr, 3, 1, args.cpu_budget, os.cpu_count() or 1)
+            cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, not required
+            cpu = {"value": None, "unit": "mult/s", "cores": 0, "kind": "reference",
+                   "sample": f"failed: {e}"}
+    line = {
+        "metric": "SpGEMM mults/sec", "value": flop / t_step, "unit": "mult/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators of SURVEY.md §8d; no dataset)",
+        "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}",
+                   "n": n, "nnz_a": nnz_a, "flop": flop, "nnz_c": nnz_c,
+                   "model_bytes": b_tot, "model_GBps": b_tot / t_step / 1e9,
+                   "model_frac_of_peak_per_gpu": b_tot / t_step / 1e9 / (peak * ws),
+                   "l2": "inputs+tuples larger than L2 (tuples alone are 12 B x flop)",
+                   "partition": f"{ws} flop-balanced row bands" if ws > 1 else "single GPU"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "phases_ms": {"symbolic": t_sym_max * 1e3, "expand": t_exp_max * 1e3,
+                      "sort_merge": t_sort_max * 1e3},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(M.CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=120.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

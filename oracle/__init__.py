@@ -1,0 +1,248 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU oracle of the PB-SpGEMM hot path.
+
+Two checkers, both CPU, both outside the product:
+
+* ``port``      — oracle/pb_oracle.c, a single-threaded C restatement of the
+  reference algorithm (liborc.so);
+* ``reference`` — the reference library itself, compiled unmodified from
+  /root/reference/proj/src by oracle/build_ref.sh into oracle/_ref/.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package. Parity of the port is
+pinned against the reference (tests/test_oracle.py) and against the golden
+fixtures in tests/golden/ generated from the reference
+(tests/golden/make_golden.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORC = HERE / "_build" / "liborc.so"
+REF = HERE / "_ref" / "libspgemm_ref.so"
+
+vp, u32, u64, f64 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_double
+
+
+def build(ref: bool = True) -> None:
+    """Compile the port (always) and the reference (when /root/reference exists)."""
+    subprocess.run(["make", "-C", str(HERE), "_build/liborc.so"], check=True,
+                   stdout=subprocess.DEVNULL)
+    if ref:
+        subprocess.run([str(HERE / "build_ref.sh")], check=True, stdout=subprocess.DEVNULL)
+
+
+_libs = {}
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else C.c_void_p(0)
+
+
+def port_lib():
+    if "orc" not in _libs:
+        if not ORC.exists():
+            build(ref=False)
+        lib = C.CDLL(str(ORC))
+        lib.orc_pb_multiply.restype = C.c_int
+        lib.orc_pb_multiply.argtypes = [u32, u32, u64, vp, vp, vp, u32, u32, u64, vp, vp, vp,
+                                        u32, u32, u64, C.c_int, C.POINTER(vp)]
+        lib.orc_res_nnz.restype = u64
+        lib.orc_res_nnz.argtypes = [vp]
+        lib.orc_res_nbins.restype = u32
+        lib.orc_res_nbins.argtypes = [vp]
+        lib.orc_res_get.argtypes = [vp, vp, vp, vp]
+        lib.orc_res_counters.argtypes = [vp, vp]
+        lib.orc_res_symbolic.argtypes = [vp, vp, u32, vp, vp]
+        lib.orc_free.argtypes = [vp]
+        lib.orc_choose_nbins.restype = u32
+        lib.orc_choose_nbins.argtypes = [u64, u32, u64, u32]
+        lib.orc_value.restype = f64
+        lib.orc_value.argtypes = [u64, u32, u32]
+        lib.orc_split_seed.restype = u64
+        lib.orc_split_seed.argtypes = [u64, u64]
+        lib.orc_gen_er.argtypes = [C.c_int, u32, u64, vp, vp]
+        lib.orc_gen_rmat_draws.argtypes = [C.c_int, u32, u64, f64, f64, f64, vp, vp]
+        _libs["orc"] = lib
+    return _libs["orc"]
+
+
+def ref_available() -> bool:
+    return REF.exists()
+
+
+def ref_lib():
+    if "ref" not in _libs:
+        if not REF.exists():
+            raise RuntimeError(f"{REF} not built (oracle/build_ref.sh needs /root/reference)")
+        lib = C.CDLL(str(REF))
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_gen.argtypes = [C.c_int, C.c_int, u32, u64, C.POINTER(vp)]
+        lib.ref_coo_nnz.restype = u64
+        lib.ref_coo_nnz.argtypes = [vp]
+        lib.ref_coo_get.argtypes = [vp, vp, vp, vp]
+        lib.ref_coo_free.argtypes = [vp]
+        lib.ref_coo_convert.argtypes = [C.c_int, u32, u32, u64, vp, vp, vp, vp, vp, vp,
+                                        C.POINTER(u64)]
+        lib.ref_pb_multiply.argtypes = [u32, u32, u64, vp, vp, vp, u32, u32, u64, vp, vp, vp,
+                                        u32, u32, u64, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+        lib.ref_res_nnz.restype = u64
+        lib.ref_res_nnz.argtypes = [vp]
+        lib.ref_res_nbins.restype = u32
+        lib.ref_res_nbins.argtypes = [vp]
+        lib.ref_res_get.argtypes = [vp, vp, vp, vp]
+        lib.ref_res_counters.argtypes = [vp, vp]
+        lib.ref_res_symbolic.argtypes = [vp, vp, vp, vp]
+        lib.ref_res_times.argtypes = [vp, vp]
+        lib.ref_res_free.argtypes = [vp]
+        lib.ref_choose_nbins.restype = u32
+        lib.ref_choose_nbins.argtypes = [u64, u32, u64, u32]
+        lib.ref_dense_multiply.argtypes = [u32, u32, u32, u64, vp, vp, vp, u64, vp, vp, vp,
+                                           C.POINTER(vp)]
+        _libs["ref"] = lib
+    return _libs["ref"]
+
+
+class OracleError(Exception):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"oracle error {code}: {msg}")
+        self.code = code  # 1 parameter_error, 2 internal_error, 3 other
+
+
+@dataclass
+class OracleResult:
+    rowptr: np.ndarray
+    colids: np.ndarray
+    values: np.ndarray
+    flop: int
+    tuples_into_sort: int
+    merged_total: int
+    nbins: int
+    per_column_flop: np.ndarray
+    per_bin_flop: np.ndarray
+    bin_row_starts: np.ndarray
+    times: np.ndarray | None = None
+
+
+def _arrays(a, b):
+    ap = np.ascontiguousarray(a.colptr, np.uint64)
+    ai = np.ascontiguousarray(a.rowids, np.uint32)
+    av = np.ascontiguousarray(a.values, np.float64)
+    bp = np.ascontiguousarray(b.rowptr, np.uint64)
+    bi = np.ascontiguousarray(b.colids, np.uint32)
+    bv = np.ascontiguousarray(b.values, np.float64)
+    return ap, ai, av, bp, bi, bv
+
+
+def multiply(a, b, nbins=0, lbin_bytes=512, l2_bytes=1 << 20, balanced=False,
+             impl="port", nthreads=1, stepwise=True) -> OracleResult:
+    """C = A·B on the CPU. impl='port' (C restatement) or 'reference'."""
+    ap, ai, av, bp, bi, bv = _arrays(a, b)
+    h = vp()
+    if impl == "port":
+        lib = port_lib()
+        rc = lib.orc_pb_multiply(a.nrows, a.ncols, ai.size, _ptr(ap), _ptr(ai), _ptr(av),
+                                 b.nrows, b.ncols, bi.size, _ptr(bp), _ptr(bi), _ptr(bv),
+                                 nbins, lbin_bytes, l2_bytes, int(balanced), C.byref(h))
+        if rc:
+            raise OracleError(rc)
+        nnz, nb = lib.orc_res_nnz(h), lib.orc_res_nbins(h)
+        get, counters, free = lib.orc_res_get, lib.orc_res_counters, lib.orc_free
+    else:
+        lib = ref_lib()
+        rc = lib.ref_pb_multiply(a.nrows, a.ncols, ai.size, _ptr(ap), _ptr(ai), _ptr(av),
+                                 b.nrows, b.ncols, bi.size, _ptr(bp), _ptr(bi), _ptr(bv),
+                                 nbins, lbin_bytes, l2_bytes, nthreads, int(balanced),
+                                 int(stepwise), C.byref(h))
+        if rc:
+            raise OracleError(rc, lib.ref_last_error().decode())
+        nnz, nb = lib.ref_res_nnz(h), lib.ref_res_nbins(h)
+        get, counters, free = lib.ref_res_get, lib.ref_res_counters, lib.ref_res_free
+    rowptr = np.empty(a.nrows + 1, np.uint64)
+    colids = np.empty(max(nnz, 1), np.uint32)
+    values = np.empty(max(nnz, 1), np.float64)
+    get(h, _ptr(rowptr), _ptr(colids), _ptr(values))
+    cnt = np.zeros(4, np.uint64)
+    counters(h, _ptr(cnt))
+    pcf = np.zeros(max(a.ncols, 1), np.uint64)
+    pbf = np.zeros(max(nb, 1), np.uint64)
+    brs = np.zeros(nb + 1, np.uint32)
+    times = None
+    if impl == "port":
+        lib.orc_res_symbolic(h, _ptr(pcf), a.ncols, _ptr(pbf), _ptr(brs))
+    else:
+        lib.ref_res_symbolic(h, _ptr(pcf), _ptr(pbf), _ptr(brs))
+        times = np.zeros(6)
+        lib.ref_res_times(h, _ptr(times))
+    free(h)
+    return OracleResult(rowptr, colids[:nnz], values[:nnz], int(cnt[0]), int(cnt[1]),
+                        int(cnt[2]), nb, pcf[:a.ncols], pbf[:nb], brs, times)
+
+
+def ref_generate(kind: str, scale: int, ef: int, seed: int):
+    """The reference generator's COO (values 1.0) as (rows, cols)."""
+    lib = ref_lib()
+    h = vp()
+    rc = lib.ref_gen(0 if kind == "er" else 1, scale, ef, seed, C.byref(h))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    n = lib.ref_coo_nnz(h)
+    r = np.empty(n, np.uint32)
+    c = np.empty(n, np.uint32)
+    v = np.empty(n, np.float64)
+    lib.ref_coo_get(h, _ptr(r), _ptr(c), _ptr(v))
+    lib.ref_coo_free(h)
+    return r, c, v
+
+
+def ref_convert(to_csr: bool, nrows: int, ncols: int, rows, cols, vals):
+    """The reference's coo_to_csr / coo_to_csc (convert.cpp:82-98)."""
+    lib = ref_lib()
+    rows = np.ascontiguousarray(rows, np.uint32)
+    cols = np.ascontiguousarray(cols, np.uint32)
+    vals = np.ascontiguousarray(vals, np.float64)
+    nmaj = nrows if to_csr else ncols
+    ptr = np.zeros(nmaj + 1, np.uint64)
+    idx = np.empty(max(rows.size, 1), np.uint32)
+    val = np.empty(max(rows.size, 1), np.float64)
+    out = u64(0)
+    rc = lib.ref_coo_convert(int(to_csr), nrows, ncols, rows.size, _ptr(rows), _ptr(cols),
+                             _ptr(vals), _ptr(ptr), _ptr(idx), _ptr(val), C.byref(out))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    k = out.value
+    return ptr, idx[:k].copy(), val[:k].copy()
+
+
+def value(vseed: int, r: int, c: int) -> float:
+    return port_lib().orc_value(vseed, r, c)
+
+
+def choose_nbins(flop, nrows, l2_bytes=1 << 20, tuple_bytes=12, impl="port") -> int:
+    if impl == "port":
+        return port_lib().orc_choose_nbins(flop, nrows, l2_bytes, tuple_bytes)
+    return ref_lib().ref_choose_nbins(flop, nrows, l2_bytes, tuple_bytes)
+
+
+def dense_multiply(m, k, n, a_coo, b_coo):
+    """The reference dense oracle (reference.cpp:8-35): exact zeros dropped."""
+    lib = ref_lib()
+    ar, ac, av = (np.ascontiguousarray(x, t) for x, t in zip(a_coo, (np.uint32, np.uint32, np.float64)))
+    br, bc, bv = (np.ascontiguousarray(x, t) for x, t in zip(b_coo, (np.uint32, np.uint32, np.float64)))
+    h = vp()
+    rc = lib.ref_dense_multiply(m, k, n, ar.size, _ptr(ar), _ptr(ac), _ptr(av), br.size,
+                                _ptr(br), _ptr(bc), _ptr(bv), C.byref(h))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    nnz = lib.ref_coo_nnz(h)
+    r = np.empty(nnz, np.uint32)
+    c = np.empty(nnz, np.uint32)
+    v = np.empty(nnz, np.float64)
+    lib.ref_coo_get(h, _ptr(r), _ptr(c), _ptr(v))
+    lib.ref_coo_free(h)
+    return r, c, v

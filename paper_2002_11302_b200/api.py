@@ -1,0 +1,213 @@
+"""Python mirror of the reference's PB-SpGEMM entry point.
+
+``pb_multiply(a_csc, b_csr, cfg)`` has the meaning, arguments and error
+behaviour of ``spgemm::pb_multiply`` (proj/include/spgemm/pb_spgemm.hpp:116,
+proj/src/pb_spgemm.cpp:330-361), computed on the B200 through the C-ABI
+(include/pbg.h). ``ParameterError`` / ``InternalError`` stand for the
+reference's ``parameter_error`` / ``internal_error`` (types.hpp:80-91).
+
+``DeviceContext`` is the device-resident path the benchmark times: inputs
+already in HBM (torch tensors as plumbing), one multiply per call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .matrices import CscMatrix, CsrMatrix
+
+
+class ParameterError(ValueError):
+    """spgemm::parameter_error (types.hpp:80-83)."""
+
+
+class InternalError(RuntimeError):
+    """spgemm::internal_error (types.hpp:89-91)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no device (the GPU path has no CPU fallback)."""
+
+
+def _raise(rc: int):
+    msg = _native.last_error()
+    if rc in (_native.PBG_ERR_DIM, _native.PBG_ERR_NBINS, _native.PBG_ERR_LBIN,
+              _native.PBG_ERR_FLOP_OVERFLOW):
+        raise ParameterError(msg)
+    if rc == _native.PBG_ERR_INTERNAL:
+        raise InternalError(msg)
+    if rc == _native.PBG_ERR_UNIMPLEMENTED:
+        raise NotImplementedError(msg)
+    raise DeviceError(f"[pbg {rc}] {msg}")
+
+
+@dataclass
+class PbConfig:
+    """spgemm::PbConfig (pb_spgemm.hpp:11-17) + GPU fields."""
+    nbins: int = 0
+    lbin_bytes: int = 512
+    l2_bytes: int = 1 << 20
+    nthreads: int = 0
+    balanced_bins: bool = False
+    device: int = -1
+    bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
+
+    def to_c(self) -> _native.Config:
+        c = _native.Config()
+        _native.pbg().pbg_default_config(C.byref(c))
+        c.nbins, c.lbin_bytes, c.l2_bytes = self.nbins, self.lbin_bytes, self.l2_bytes
+        c.nthreads, c.balanced_bins = self.nthreads, int(self.balanced_bins)
+        c.device, c.bin_cap = self.device, self.bin_cap
+        return c
+
+
+@dataclass
+class SymbolicResult:
+    """spgemm::SymbolicResult (pb_spgemm.hpp:48-55) on the reference bin layout."""
+    flop: int = 0
+    per_column_flop: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    nbins: int = 1
+    per_bin_flop: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint64))
+    bin_row_starts: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
+
+
+@dataclass
+class PbResult:
+    c: CsrMatrix
+    sym: SymbolicResult
+    phases: dict
+    tuples_into_sort: int
+    merged_total: int
+    report: dict
+
+
+def _view(nrows, ncols, ptr, idx, val) -> _native.CsxView:
+    v = _native.CsxView()
+    v.nrows, v.ncols, v.nnz = nrows, ncols, int(idx.size)
+    v.ptr = ptr.ctypes.data
+    v.idx = idx.ctypes.data if idx.size else None
+    v.val = val.ctypes.data if val.size else None
+    return v
+
+
+def _host_arrays(m):
+    if isinstance(m, CscMatrix):
+        return m.colptr, m.rowids, m.values
+    return m.rowptr, m.colids, m.values
+
+
+def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
+                symbolic: bool = True, out=None) -> PbResult:
+    """C = A·B on the GPU, A in CSC, B in CSR, C in CSR (host buffers in/out).
+
+    ``out`` = (rowptr, colids, values) caller-owned host arrays (e.g. pinned)
+    large enough for C; the returned CsrMatrix views them."""
+    cfg = cfg or PbConfig()
+    lib = _native.pbg()
+    ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))
+    bp, bi, bv = (np.ascontiguousarray(x) for x in _host_arrays(b))
+    if ap.dtype != np.uint64 or bp.dtype != np.uint64 or ai.dtype != np.uint32 \
+            or bi.dtype != np.uint32 or av.dtype != np.float64 or bv.dtype != np.float64:
+        raise TypeError("expected u64 pointers, u32 indices, f64 values")
+    va = _view(a.nrows, a.ncols, ap, ai, av)
+    vb = _view(b.nrows, b.ncols, bp, bi, bv)
+    c_cfg = cfg.to_c()
+    h = C.c_void_p()
+    nnz = C.c_uint64(0)
+    rc = lib.pbg_multiply_begin(C.byref(va), C.byref(vb), C.byref(c_cfg), C.byref(h), C.byref(nnz))
+    if rc:
+        _raise(rc)
+    try:
+        k = nnz.value
+        if out is not None and out[1].size >= k and out[0].size >= a.nrows + 1:
+            rowptr, colids, values = out
+        else:
+            rowptr = np.empty(a.nrows + 1, np.uint64)
+            colids = np.empty(max(k, 1), np.uint32)
+            values = np.empty(max(k, 1), np.float64)
+        rep = _native.Report()
+        rc = lib.pbg_multiply_fetch(h, rowptr.ctypes.data, colids.ctypes.data,
+                                    values.ctypes.data, C.byref(rep))
+        if rc:
+            _raise(rc)
+        sym = SymbolicResult(flop=rep.flop, nbins=rep.nbins)
+        if symbolic:
+            sym.per_column_flop = np.zeros(max(a.ncols, 1), np.uint64)
+            sym.per_bin_flop = np.zeros(max(rep.nbins, 1), np.uint64)
+            sym.bin_row_starts = np.zeros(rep.nbins + 1, np.uint32)
+            rc = lib.pbg_symbolic_fetch(h, sym.per_column_flop.ctypes.data,
+                                        sym.per_bin_flop.ctypes.data,
+                                        sym.bin_row_starts.ctypes.data)
+            if rc:
+                _raise(rc)
+            sym.per_column_flop = sym.per_column_flop[:a.ncols]
+            sym.per_bin_flop = sym.per_bin_flop[:rep.nbins]
+    finally:
+        lib.pbg_release(h)
+    r = rep.as_dict()
+    phases = {key: r[key] for key in ("t_symbolic", "t_expand", "t_sort", "t_compress",
+                                      "t_convert", "t_total", "t_h2d", "t_d2h")}
+    c = CsrMatrix(a.nrows, b.ncols, rowptr[:a.nrows + 1], colids[:k], values[:k])
+    if c.nnz != rep.merged_total:
+        raise InternalError("compressed counts disagree with output nnz")
+    return PbResult(c, sym, phases, rep.tuples_into_sort, rep.merged_total, r)
+
+
+class DeviceContext:
+    """Device-resident multiply: views over CUDA memory (e.g. torch tensors)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _native.pbg()
+        self._ctx = C.c_void_p()
+        rc = self._lib.pbg_context_create(device, C.byref(self._ctx))
+        if rc:
+            _raise(rc)
+        self.device = device
+
+    def close(self):
+        if self._ctx:
+            self._lib.pbg_context_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def view(nrows: int, ncols: int, ptr, idx, val) -> _native.CsxView:
+        """View over torch CUDA tensors (u64-as-int64 ptr, u32-as-int32 idx, f64 val)."""
+        v = _native.CsxView()
+        v.nrows, v.ncols, v.nnz = nrows, ncols, int(idx.numel())
+        v.ptr, v.idx, v.val = ptr.data_ptr(), idx.data_ptr() or None, val.data_ptr() or None
+        return v
+
+    def multiply(self, a_view, b_view, cfg: PbConfig | None = None, stream: int = 0):
+        cfg = cfg or PbConfig()
+        c_cfg = cfg.to_c()
+        nnz = C.c_uint64(0)
+        rep = _native.Report()
+        rc = self._lib.pbg_multiply_device(self._ctx, C.byref(a_view), C.byref(b_view),
+                                           C.byref(c_cfg), C.c_void_p(stream or None),
+                                           C.byref(nnz), C.byref(rep))
+        if rc:
+            _raise(rc)
+        return nnz.value, rep.as_dict()
+
+    def result_pointers(self):
+        rp, ci, va = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        rc = self._lib.pbg_context_result(self._ctx, C.byref(rp), C.byref(ci), C.byref(va))
+        if rc:
+            _raise(rc)
+        return rp.value, ci.value, va.value
+
+    def launches(self) -> int:
+        return int(self._lib.pbg_context_launches(self._ctx))
+
+
+def device_available() -> bool:
+    return bool(_native.pbg().pbg_device_available())

@@ -1,0 +1,99 @@
+// pb_spgemm_shim.cpp — spgemm::pb_multiply re-implemented over the C-ABI
+// (include/pbg.h). The drop-in for reference proj/src/pb_spgemm.cpp:330-361:
+// same signature, same exception classes, GPU underneath, no CPU fallback.
+#include <stdexcept>
+
+#include "pbg.h"
+#include "spgemm_b200/pb_spgemm.hpp"
+
+namespace spgemm {
+
+std::uint32_t choose_nbins(std::uint64_t flop, index_t nrows, const PbConfig& cfg,
+                           std::uint32_t tuple_bytes) {
+    return pbg_choose_nbins(flop, nrows, cfg.l2_bytes, tuple_bytes);
+}
+
+namespace {
+
+[[noreturn]] void throw_for(int rc) {
+    const std::string msg = pbg_last_error();
+    switch (rc) {
+        case PBG_ERR_DIM:
+        case PBG_ERR_NBINS:
+        case PBG_ERR_LBIN:
+        case PBG_ERR_FLOP_OVERFLOW:
+            throw parameter_error(msg);
+        case PBG_ERR_INTERNAL:
+            throw internal_error(msg);
+        default:
+            throw std::runtime_error("pb_multiply (GPU): " + msg);
+    }
+}
+
+pbg_config to_c(const PbConfig& c) {
+    pbg_config o;
+    pbg_default_config(&o);
+    o.nbins = c.nbins;
+    o.lbin_bytes = c.lbin_bytes;
+    o.l2_bytes = c.l2_bytes;
+    o.nthreads = c.nthreads;
+    o.balanced_bins = c.balanced_bins ? 1 : 0;
+    return o;
+}
+
+struct Handle {
+    pbg_handle* h = nullptr;
+    ~Handle() { pbg_release(h); }
+};
+
+}  // namespace
+
+PbResult pb_multiply(const CscMatrix& a, const CsrMatrix& b, const PbConfig& cfg) {
+    require_multipliable(a.dims, b.dims);
+    const pbg_config c = to_c(cfg);
+    const pbg_csx_view av{a.dims.nrows, a.dims.ncols, a.nnz(), a.colptr.data(), a.rowids.data(),
+                          a.values.data()};
+    const pbg_csx_view bv{b.dims.nrows, b.dims.ncols, b.nnz(), b.rowptr.data(), b.colids.data(),
+                          b.values.data()};
+    Handle h;
+    std::uint64_t nnz = 0;
+    int rc = pbg_multiply_begin(&av, &bv, &c, &h.h, &nnz);
+    if (rc) throw_for(rc);
+    PbResult res;
+    res.c.dims = {a.dims.nrows, b.dims.ncols};
+    res.c.rowptr.resize(static_cast<std::size_t>(a.dims.nrows) + 1);
+    res.c.colids.resize(nnz);
+    res.c.values.resize(nnz);
+    pbg_report rep;
+    rc = pbg_multiply_fetch(h.h, res.c.rowptr.data(), res.c.colids.data(), res.c.values.data(),
+                            &rep);
+    if (rc) throw_for(rc);
+    res.sym.flop = rep.flop;
+    res.sym.nbins = rep.nbins;
+    res.sym.per_column_flop.resize(a.dims.ncols);
+    res.sym.per_bin_flop.resize(rep.nbins);
+    res.sym.bin_row_starts.resize(static_cast<std::size_t>(rep.nbins) + 1);
+    rc = pbg_symbolic_fetch(h.h, res.sym.per_column_flop.data(), res.sym.per_bin_flop.data(),
+                            res.sym.bin_row_starts.data());
+    if (rc) throw_for(rc);
+    const index_t m = a.dims.nrows;
+    const std::uint64_t rpb = rep.nbins ? (static_cast<std::uint64_t>(m) + rep.nbins - 1) / rep.nbins : 0;
+    bool uniform = true;
+    for (std::uint32_t i = 0; i <= rep.nbins; ++i)
+        if (res.sym.bin_row_starts[i] != std::min<std::uint64_t>(i * rpb, m)) uniform = false;
+    res.sym.uniform_rows_per_bin = uniform ? static_cast<index_t>(rpb) : 0;
+    res.phases.t_symbolic = rep.t_symbolic;
+    res.phases.t_expand = rep.t_expand;
+    res.phases.t_sort = rep.t_sort;
+    res.phases.t_compress = rep.t_compress;
+    res.phases.t_convert = rep.t_convert;
+    res.phases.t_total = rep.t_total;
+    res.tuples_into_sort = rep.tuples_into_sort;
+    res.merged_total = rep.merged_total;
+    res.gpu_bins = rep.gpu_bins;
+    if (res.c.nnz() != res.merged_total)
+        throw internal_error("compressed counts disagree with output nnz");
+    return res;
+}
+
+}  // namespace spgemm

@@ -1,0 +1,661 @@
+// pbg.cu — host orchestration and the C-ABI (include/pbg.h) of the
+// B200-native PB-SpGEMM path. Replaces spgemm::pb_multiply
+// (reference proj/src/pb_spgemm.cpp:330-361): symbolic, expand, sort+merge+
+// convert, all on one CUDA stream, timed with CUDA events.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pbg.h"
+#include "pbg_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            const int code_ = e_ == cudaErrorMemoryAllocation ? PBG_ERR_OOM : PBG_ERR_CUDA; \
+            return fail(code_, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+        }                                                                               \
+    } while (0)
+
+int ceil_log2_u64(uint64_t x) {  // pb_spgemm.hpp:20
+    if (x <= 1) return 0;
+    return 64 - __builtin_clzll(x - 1);
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+int grow(DevBuf& b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return PBG_OK;
+    b.release();
+    const size_t want = bytes + bytes / 8;  // grow-only with headroom
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        e = cudaMalloc(&b.p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            b.p = nullptr;
+            return fail(PBG_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+        }
+        b.cap = bytes;
+        return PBG_OK;
+    }
+    b.cap = want;
+    return PBG_OK;
+}
+
+// Scalars the kernels report back (one D2H each sync point).
+enum Scalar : int {
+    S_FLOP = 0,        // scan total of per-column flop
+    S_FLOP_LO,         // 128-bit total (overflow check)
+    S_FLOP_HI,
+    S_MAXROW,          // max per-row flop
+    S_NBINS,           // GPU bin count
+    S_TUPLE_CAP,       // padded tuple capacity
+    S_HEAVY,           // bins above cap
+    S_MAXBIN,
+    S_TUPLES_TOTAL,    // sum of cursors (tuples into sort)
+    S_MERGED_TOTAL,    // sum of merged counts
+    S_ERR,             // error bits (u32 in low word)
+    S_COUNT
+};
+constexpr int kTickets = 8;
+constexpr int kScans = 4;
+
+}  // namespace
+
+struct pbg_context {
+    int device = 0;
+    int num_sms = 148;
+    DevBuf colflop_off, row_flop, row_off, flags, row_bin, bin_rs, bin_cnt, bin_off, cursor,
+        status, chunk_p0, keys, vals, rowptr, zero_block, in_a_ptr, in_a_idx, in_a_val,
+        in_b_ptr, in_b_idx, in_b_val;
+    size_t zero_bytes = 0;
+    cudaEvent_t ev[6] = {};
+    bool ev_ok = false;
+    // last product
+    uint64_t m = 0, k = 0, n = 0, nnz_c = 0, flop = 0;
+    int col_bits = 0;
+    pbg_report rep{};
+    uint32_t launches = 0;
+    bool have_result = false;
+    ~pbg_context() {
+        for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
+                          &bin_off, &cursor, &status, &chunk_p0, &keys, &vals, &rowptr,
+                          &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr, &in_b_idx,
+                          &in_b_val})
+            b->release();
+        if (ev_ok)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+
+struct pbg_handle {
+    pbg_context* ctx = nullptr;
+    pbg_config cfg{};
+    double t_h2d = 0.0;
+};
+
+namespace {
+
+int set_device(int dev) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(PBG_ERR_NODEVICE, "no CUDA device available (the PB-SpGEMM GPU path has no CPU fallback)");
+    }
+    if (dev >= 0) CUDA_TRY(cudaSetDevice(dev));
+    return PBG_OK;
+}
+
+int validate_view(const pbg_csx_view* v, const char* what) {
+    if (!v) return fail(PBG_ERR_ARG, std::string(what) + " view is null");
+    if (!v->ptr) return fail(PBG_ERR_ARG, std::string(what) + " ptr is null");
+    if (v->nnz && (!v->idx || !v->val)) return fail(PBG_ERR_ARG, std::string(what) + " idx/val null");
+    return PBG_OK;
+}
+
+int validate_cfg(const pbg_config& c) {
+    if (c.nbins != 0 && (c.nbins & (c.nbins - 1)) != 0)
+        return fail(PBG_ERR_NBINS, "nbins must be a power of two");
+    if (c.lbin_bytes == 0 || c.lbin_bytes % 16 != 0)
+        return fail(PBG_ERR_LBIN, "lbin_bytes must be a positive multiple of 16");
+    if (c.bin_cap > static_cast<uint32_t>(pbg::SM_CAP))
+        return fail(PBG_ERR_ARG, "bin_cap above the shared-memory bin capacity " + std::to_string(pbg::SM_CAP));
+    if (c.bin_cap != 0 && c.bin_cap < 16) return fail(PBG_ERR_ARG, "bin_cap must be >= 16");
+    return PBG_OK;
+}
+
+template <class In>
+void launch_scan(In in, uint64_t* out, uint64_t n_host, const uint64_t* n_dev, uint64_t n_max,
+                 unsigned long long* status, unsigned int* ticket, unsigned long long* total_out,
+                 unsigned long long* max_out, cudaStream_t st) {
+    const uint64_t tiles = std::max<uint64_t>(1, (n_max + pbg::SCAN_TILE - 1) / pbg::SCAN_TILE);
+    pbg::k_scan<In><<<static_cast<unsigned>(tiles), pbg::SCAN_NT, 0, st>>>(
+        in, out, n_host, n_dev, status, ticket, total_out, max_out);
+}
+
+unsigned blocks_for(uint64_t n, unsigned nt) {
+    uint64_t b = (n + nt - 1) / nt;
+    return static_cast<unsigned>(std::max<uint64_t>(1, b));
+}
+
+// The pipeline on device-resident views.
+int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
+                 const pbg_config& cfg, cudaStream_t st) {
+    using namespace pbg;
+    const uint64_t m = A.nrows, k = A.ncols, n = B.ncols;
+    const uint64_t nnz_a = A.nnz;
+    const uint64_t cap = cfg.bin_cap ? cfg.bin_cap : SM_CAP;
+    const int cb = ceil_log2_u64(n);
+    uint32_t maxr = cb >= 32 ? 1u : (cb >= 22 ? (1u << (32 - cb)) : 1024u);
+    ctx->m = m;
+    ctx->k = k;
+    ctx->n = n;
+    ctx->col_bits = cb;
+    ctx->have_result = false;
+    ctx->launches = 0;
+    ctx->rep = pbg_report{};
+
+    int rc;
+    // ---- workspace ----
+    const uint64_t tiles_k = (k + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    const uint64_t tiles_m = (m + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    const uint64_t status_words = tiles_k + 3 * tiles_m;
+    const size_t zero_bytes = (S_COUNT + kTickets) * 8 + status_words * 8;
+    if ((rc = grow(ctx->zero_block, zero_bytes))) return rc;
+    if ((rc = grow(ctx->colflop_off, (k + 1) * 8))) return rc;
+    if ((rc = grow(ctx->row_flop, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->row_off, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->flags, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->row_bin, (m + 1) * 4))) return rc;
+    if ((rc = grow(ctx->bin_rs, (m + 2) * 4))) return rc;
+    if ((rc = grow(ctx->bin_cnt, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->bin_off, (m + 2) * 8))) return rc;
+    if ((rc = grow(ctx->cursor, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->status, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->rowptr, (m + 1) * 8))) return rc;
+    if (!ctx->ev_ok) {
+        for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+        ctx->ev_ok = true;
+    }
+
+    auto* zb = static_cast<unsigned long long*>(ctx->zero_block.p);
+    unsigned long long* sc = zb;                                           // scalars
+    unsigned int* tickets = reinterpret_cast<unsigned int*>(zb + S_COUNT);  // 2 per u64
+    unsigned long long* sstat = zb + S_COUNT + kTickets;
+    unsigned long long* stat_k = sstat;
+    unsigned long long* stat_m1 = stat_k + tiles_k;
+    unsigned long long* stat_m2 = stat_m1 + tiles_m;
+    unsigned long long* stat_m3 = stat_m2 + tiles_m;
+
+    auto* colflop_off = static_cast<uint64_t*>(ctx->colflop_off.p);
+    auto* row_flop = static_cast<unsigned long long*>(ctx->row_flop.p);
+    auto* row_off = static_cast<uint64_t*>(ctx->row_off.p);
+    auto* flags = static_cast<uint64_t*>(ctx->flags.p);
+    auto* row_bin = static_cast<uint32_t*>(ctx->row_bin.p);
+    auto* bin_rs = static_cast<uint32_t*>(ctx->bin_rs.p);
+    auto* bin_cnt = static_cast<uint64_t*>(ctx->bin_cnt.p);
+    auto* bin_off = static_cast<uint64_t*>(ctx->bin_off.p);
+    auto* cursor = static_cast<unsigned long long*>(ctx->cursor.p);
+    auto* status = static_cast<unsigned long long*>(ctx->status.p);
+    auto* rowptr = static_cast<uint64_t*>(ctx->rowptr.p);
+
+    CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+    CUDA_TRY(cudaMemsetAsync(zb, 0, zero_bytes, st));
+    uint32_t L = 0;
+
+    // ---- symbolic (pb_spgemm.cpp:86-139) + bin layout (make_bins :141-176) ----
+    launch_scan(ColFlopIn{A.ptr, B.ptr}, colflop_off, k, nullptr, k, stat_k, tickets + 0,
+                sc + S_FLOP, nullptr, st);
+    ++L;
+    k_colflop_total<<<std::min<unsigned>(blocks_for(k, 256), 4 * ctx->num_sms), 256, 0, st>>>(
+        A.ptr, B.ptr, k, sc + S_FLOP_LO, sc + S_FLOP_HI);
+    ++L;
+    if (m > 0) {
+        CUDA_TRY(cudaMemsetAsync(row_flop, 0, m * 8, st));
+        if (k > 0) {
+            k_rowflop<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, B.ptr, k, row_flop);
+            ++L;
+        }
+        launch_scan(ArrayIn{reinterpret_cast<const uint64_t*>(row_flop)}, row_off, m, nullptr, m,
+                    stat_m1, tickets + 1, nullptr, sc + S_MAXROW, st);
+        ++L;
+        k_binflags<<<blocks_for(m, 256), 256, 0, st>>>(reinterpret_cast<const uint64_t*>(row_flop),
+                                                       row_off, m, BinParams{cap, maxr},
+                                                       sc + S_MAXROW, flags);
+        ++L;
+        launch_scan(ArrayIn{flags}, flags, m, nullptr, m, stat_m2, tickets + 2, sc + S_NBINS,
+                    nullptr, st);
+        ++L;
+        k_binrows<<<blocks_for(m, 256), 256, 0, st>>>(flags, m, row_bin, bin_rs);
+        ++L;
+        k_binsizes<<<blocks_for(m, 256), 256, 0, st>>>(
+            bin_rs, row_off, reinterpret_cast<const uint64_t*>(sc + S_NBINS), cap, bin_cnt,
+            bin_off, cursor, status, sc + S_HEAVY, sc + S_MAXBIN);
+        ++L;
+        launch_scan(ArrayIn{bin_off}, bin_off, 0, reinterpret_cast<const uint64_t*>(sc + S_NBINS),
+                    m, stat_m3, tickets + 3, sc + S_TUPLE_CAP, nullptr, st);
+        ++L;
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    unsigned long long hs[S_COUNT];
+    CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+
+    if (hs[S_FLOP_HI] != 0 || hs[S_FLOP_LO] > ST_VAL)
+        return fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits");
+    const uint64_t flop = hs[S_FLOP];
+    ctx->flop = flop;
+    ctx->rep.flop = flop;
+    ctx->rep.nnz_a = A.nnz;
+    ctx->rep.nnz_b = B.nnz;
+    ctx->rep.gpu_bins = static_cast<uint32_t>(hs[S_NBINS]);
+    ctx->rep.heavy_bins = static_cast<uint32_t>(hs[S_HEAVY]);
+    ctx->rep.bin_cap = static_cast<uint32_t>(cap);
+    if (flop != hs[S_FLOP_LO]) return fail(PBG_ERR_INTERNAL, "flop scan and reduction disagree");
+    if (hs[S_HEAVY] != 0)
+        return fail(PBG_ERR_UNIMPLEMENTED,
+                    "a single output row generates " + std::to_string(hs[S_MAXBIN]) +
+                        " tuples, above the shared-memory bin capacity " + std::to_string(cap) +
+                        " (heavy-row path not built yet)");
+    const uint64_t nb = hs[S_NBINS];
+    const uint64_t tcap = hs[S_TUPLE_CAP];
+    ctx->rep.tuple_bytes = tcap * 12;
+
+    if (flop == 0 || m == 0) {
+        if (m > 0) {
+            k_zero_u64<<<blocks_for(m + 1, 256), 256, 0, st>>>(rowptr, m + 1);
+            ++L;
+        } else {
+            CUDA_TRY(cudaMemsetAsync(rowptr, 0, 8, st));
+        }
+        CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+        CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
+        ctx->rep.nbins = 0;
+        ctx->nnz_c = 0;
+    } else {
+        if ((rc = grow(ctx->keys, tcap * 4))) return rc;
+        if ((rc = grow(ctx->vals, tcap * 8))) return rc;
+        CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
+        auto* keys = static_cast<uint32_t*>(ctx->keys.p);
+        auto* vals = static_cast<double*>(ctx->vals.p);
+
+        // ---- expand (pb_spgemm.cpp:180-258) ----
+        const unsigned exp_blocks = 8u * ctx->num_sms;
+        const uint64_t warps = static_cast<uint64_t>(exp_blocks) * EXP_NW;
+        uint64_t ch = 256;
+        while (ch < 16384 && flop / ch > warps * 4) ch <<= 1;
+        const uint64_t nchunks = (flop + ch - 1) / ch;
+        if ((rc = grow(ctx->chunk_p0, (nchunks + 1) * 8))) return rc;
+        auto* chunk_p0 = static_cast<uint64_t*>(ctx->chunk_p0.p);
+        k_chunks<<<blocks_for(nchunks + 1, 256), 256, 0, st>>>(colflop_off, A.ptr, B.ptr, k,
+                                                              nnz_a, ch, nchunks, chunk_p0);
+        ++L;
+        ExpandArgs ea{A.ptr, A.idx,  A.val,   B.ptr,   B.idx, B.val, k,   chunk_p0, nchunks,
+                      row_bin, bin_rs, bin_off, cursor, keys, vals, cb};
+        k_expand<<<exp_blocks, EXP_NT, 0, st>>>(ea);
+        ++L;
+        CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+
+        // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
+        static bool attr_set[64] = {};
+        if (!attr_set[ctx->device & 63]) {
+            CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sizeof(SortSmem))));
+            attr_set[ctx->device & 63] = true;
+        }
+        SortArgs sa{bin_rs,
+                    bin_cnt,
+                    bin_off,
+                    cursor,
+                    reinterpret_cast<const uint64_t*>(sc + S_NBINS),
+                    status,
+                    tickets + 4,
+                    keys,
+                    vals,
+                    rowptr,
+                    m,
+                    cb,
+                    sc + S_TUPLES_TOTAL,
+                    sc + S_MERGED_TOTAL,
+                    reinterpret_cast<unsigned int*>(sc + S_ERR)};
+        const unsigned sm_blocks =
+            static_cast<unsigned>(std::min<uint64_t>(nb, 2ull * ctx->num_sms));
+        k_sortmerge<<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
+        ++L;
+        CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
+        CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+        uint64_t nnz = 0;
+        CUDA_TRY(cudaMemcpyAsync(&nnz, rowptr + m, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaGetLastError());
+        ctx->nnz_c = nnz;
+        ctx->rep.tuples_into_sort = hs[S_TUPLES_TOTAL];
+        ctx->rep.merged_total = hs[S_MERGED_TOTAL];
+        const unsigned err = static_cast<unsigned>(hs[S_ERR]);
+        if (err & 2u) return fail(PBG_ERR_UNIMPLEMENTED, "bin above shared-memory capacity");
+        if (err & 1u || hs[S_TUPLES_TOTAL] != flop)
+            return fail(PBG_ERR_INTERNAL, "tuple conservation broken: expanded " +
+                                              std::to_string(hs[S_TUPLES_TOTAL]) + " of " +
+                                              std::to_string(flop));
+        if (hs[S_MERGED_TOTAL] != nnz)
+            return fail(PBG_ERR_INTERNAL, "compressed counts disagree with output nnz");
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
+    CUDA_TRY(cudaEventSynchronize(ctx->ev[4]));
+    float t_sym = 0, t_exp = 0, t_sort = 0, t_tot = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t_sym, ctx->ev[0], ctx->ev[1]));
+    CUDA_TRY(cudaEventElapsedTime(&t_exp, ctx->ev[flop == 0 || m == 0 ? 1 : 5], ctx->ev[2]));
+    CUDA_TRY(cudaEventElapsedTime(&t_sort, ctx->ev[2], ctx->ev[3]));
+    CUDA_TRY(cudaEventElapsedTime(&t_tot, ctx->ev[0], ctx->ev[4]));
+    ctx->rep.t_symbolic = t_sym * 1e-3;
+    ctx->rep.t_expand = t_exp * 1e-3;
+    ctx->rep.t_sort = t_sort * 1e-3;
+    ctx->rep.t_total = t_tot * 1e-3;
+    ctx->rep.nnz_c = ctx->nnz_c;
+    // reference-layout bin count (choose_nbins, pb_spgemm.cpp:109-114)
+    {
+        uint32_t nbr = cfg.nbins ? cfg.nbins : pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 12);
+        if (m > 0) {
+            uint64_t rpb = (m + nbr - 1) / nbr;
+            if (cfg.nbins == 0 && ceil_log2_u64(rpb) + cb > 32)
+                nbr = pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 16);
+        }
+        ctx->rep.nbins = nbr;
+    }
+    ctx->launches = L;
+    ctx->have_result = true;
+    return PBG_OK;
+}
+
+std::mutex g_pool_mu;
+std::vector<pbg_context*> g_pool;
+
+pbg_context* pool_get(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i)
+        if (g_pool[i]->device == dev) {
+            pbg_context* c = g_pool[i];
+            g_pool.erase(g_pool.begin() + i);
+            return c;
+        }
+    return nullptr;
+}
+
+void pool_put(pbg_context* c) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(c);
+}
+
+int make_context(int device, pbg_context** out) {
+    int rc = set_device(device);
+    if (rc) return rc;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    auto* c = new pbg_context;
+    c->device = dev;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+        c->num_sms = sms;
+    *out = c;
+    return PBG_OK;
+}
+
+int copy_in(DevBuf& b, const void* src, size_t bytes, cudaStream_t st) {
+    int rc = grow(b, bytes);
+    if (rc) return rc;
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st));
+    return PBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pbg_last_error(void) { return g_err.c_str(); }
+
+void pbg_default_config(pbg_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof *c);
+    c->nbins = 0;
+    c->lbin_bytes = 512;
+    c->l2_bytes = 1ull << 20;
+    c->nthreads = 0;
+    c->balanced_bins = 0;
+    c->device = -1;
+    c->bin_cap = 0;
+}
+
+int pbg_device_available(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count > 0;
+}
+
+uint32_t pbg_choose_nbins(uint64_t flop, uint32_t nrows, uint64_t l2_bytes, uint32_t tuple_bytes) {
+    const uint64_t budget = std::max<uint64_t>(1, l2_bytes / 2);
+    const uint64_t raw = (flop * tuple_bytes + budget - 1) / budget;
+    uint64_t nb = 1;
+    while (nb < std::max<uint64_t>(raw, 1)) nb <<= 1;
+    nb = std::clamp<uint64_t>(nb, 64, 8192);
+    while (nb > nrows) nb >>= 1;
+    return static_cast<uint32_t>(std::max<uint64_t>(nb, 1));
+}
+
+int pbg_context_create(int device, pbg_context** out) {
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    return make_context(device, out);
+}
+
+void pbg_context_destroy(pbg_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    delete ctx;
+}
+
+int pbg_multiply_device(pbg_context* ctx, const pbg_csx_view* a, const pbg_csx_view* b,
+                        const pbg_config* cfg_in, void* stream, uint64_t* nnz_c, pbg_report* rep) {
+    if (!ctx) return fail(PBG_ERR_ARG, "context is null");
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    if (a->ncols != b->nrows)
+        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
+                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
+                                     "x" + std::to_string(b->ncols));
+    if ((rc = validate_cfg(cfg))) return rc;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    rc = run_pipeline(ctx, *a, *b, cfg, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    if (nnz_c) *nnz_c = ctx->nnz_c;
+    if (rep) *rep = ctx->rep;
+    return PBG_OK;
+}
+
+int pbg_context_result(pbg_context* ctx, const uint64_t** rowptr, const uint32_t** colids,
+                       const double** values) {
+    if (!ctx || !ctx->have_result) return fail(PBG_ERR_ARG, "no product in this context");
+    if (rowptr) *rowptr = static_cast<const uint64_t*>(ctx->rowptr.p);
+    if (colids) *colids = static_cast<const uint32_t*>(ctx->keys.p);
+    if (values) *values = static_cast<const double*>(ctx->vals.p);
+    return PBG_OK;
+}
+
+uint32_t pbg_context_launches(pbg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg_in, uint64_t* per_column_flop,
+                         uint64_t* per_bin_flop, uint32_t* bin_row_starts) {
+    if (!ctx || !ctx->have_result) return fail(PBG_ERR_ARG, "no product in this context");
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    const uint64_t m = ctx->m, k = ctx->k;
+    if (per_column_flop && k) {
+        std::vector<uint64_t> off(k + 1);
+        CUDA_TRY(cudaMemcpy(off.data(), ctx->colflop_off.p, (k + 1) * 8, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < k; ++i) per_column_flop[i] = off[i + 1] - off[i];
+    }
+    if (!per_bin_flop && !bin_row_starts) return PBG_OK;
+    // The reference bin layout (pb_spgemm.cpp:107-137) from the device's
+    // per-row flop.
+    std::vector<uint64_t> rf(m);
+    if (m && ctx->flop) CUDA_TRY(cudaMemcpy(rf.data(), ctx->row_flop.p, m * 8, cudaMemcpyDeviceToHost));
+    const uint32_t nb = ctx->rep.nbins ? ctx->rep.nbins : 1;
+    const uint64_t rpb = m ? (m + nb - 1) / nb : 0;
+    std::vector<uint32_t> starts(nb + 1);
+    for (uint32_t b = 0; b <= nb; ++b) starts[b] = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(b) * rpb, m));
+    std::vector<uint64_t> pbf(nb, 0);
+    for (uint64_t r = 0; r < m; ++r) pbf[rpb ? r / rpb : 0] += rf[r];
+    if (cfg.balanced_bins) {
+        const uint32_t tb = ceil_log2_u64(rpb) + ctx->col_bits <= 32 ? 12 : 16;
+        const uint64_t maxb = pbf.empty() ? 0 : *std::max_element(pbf.begin(), pbf.end());
+        if (maxb * tb > cfg.l2_bytes) {  // balanced_starts, pb_spgemm.cpp:58-82
+            std::fill(starts.begin(), starts.end(), static_cast<uint32_t>(m));
+            starts[0] = 0;
+            const double target = static_cast<double>(ctx->flop) / nb;
+            uint64_t acc = 0;
+            uint32_t bin = 1;
+            for (uint64_t r = 0; r < m && bin < nb; ++r) {
+                acc += rf[r];
+                if (static_cast<double>(acc) >= target * bin) starts[bin++] = static_cast<uint32_t>(r + 1);
+            }
+            std::fill(pbf.begin(), pbf.end(), 0);
+            for (uint32_t b = 0; b < nb; ++b)
+                for (uint64_t r = starts[b]; r < starts[b + 1]; ++r) pbf[b] += rf[r];
+        }
+    }
+    if (per_bin_flop) std::memcpy(per_bin_flop, pbf.data(), nb * 8);
+    if (bin_row_starts) std::memcpy(bin_row_starts, starts.data(), (nb + 1) * 4);
+    return PBG_OK;
+}
+
+int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
+                       pbg_handle** out, uint64_t* nnz_c) {
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    *out = nullptr;
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    if (a->ncols != b->nrows)
+        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
+                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
+                                     "x" + std::to_string(b->ncols));
+    if ((rc = validate_cfg(cfg))) return rc;
+    if ((rc = set_device(cfg.device))) return rc;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    pbg_context* ctx = pool_get(dev);
+    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
+    auto* h = new pbg_handle;
+    h->ctx = ctx;
+    h->cfg = cfg;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
+    cudaEventRecord(e1, st);
+    if (!rc) {
+        pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                        static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                        static_cast<const double*>(ctx->in_a_val.p)};
+        pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                        static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                        static_cast<const double*>(ctx->in_b_val.p)};
+        rc = run_pipeline(ctx, da, db, cfg, st);
+    }
+    float ms = 0;
+    if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
+        h->t_h2d = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) {
+        pbg_release(h);
+        return rc;
+    }
+    if (nnz_c) *nnz_c = ctx->nnz_c;
+    *out = h;
+    return PBG_OK;
+}
+
+int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
+                       pbg_report* rep) {
+    if (!h || !h->ctx || !h->ctx->have_result) return fail(PBG_ERR_ARG, "invalid handle");
+    pbg_context* ctx = h->ctx;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    cudaEventRecord(e0, nullptr);
+    if (rowptr) CUDA_TRY(cudaMemcpyAsync(rowptr, ctx->rowptr.p, (ctx->m + 1) * 8, cudaMemcpyDeviceToHost, nullptr));
+    if (colids && ctx->nnz_c)
+        CUDA_TRY(cudaMemcpyAsync(colids, ctx->keys.p, ctx->nnz_c * 4, cudaMemcpyDeviceToHost, nullptr));
+    if (values && ctx->nnz_c)
+        CUDA_TRY(cudaMemcpyAsync(values, ctx->vals.p, ctx->nnz_c * 8, cudaMemcpyDeviceToHost, nullptr));
+    cudaEventRecord(e1, nullptr);
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rep) {
+        *rep = ctx->rep;
+        rep->t_h2d = h->t_h2d;
+        rep->t_d2h = ms * 1e-3;
+    }
+    return PBG_OK;
+}
+
+int pbg_symbolic_fetch(pbg_handle* h, uint64_t* per_column_flop, uint64_t* per_bin_flop,
+                       uint32_t* bin_row_starts) {
+    if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");
+    return pbg_context_symbolic(h->ctx, &h->cfg, per_column_flop, per_bin_flop, bin_row_starts);
+}
+
+void pbg_release(pbg_handle* h) {
+    if (!h) return;
+    if (h->ctx) pool_put(h->ctx);
+    delete h;
+}
+
+}  // extern "C"
