@@ -262,15 +262,16 @@ def run_gpu_arm(args):
 
     flop_local = step_reps[-1]["flop"]
     nnz_local = step_reps[-1]["nnz_c"]
-    t_sort = statistics.mean(r["t_sort"] for r in step_reps)
+    t_sort = statistics.mean(r["t_sortmerge_kernel"] for r in step_reps)
+    t_count = statistics.mean(r["t_count"] for r in step_reps)
     t_exp = statistics.mean(r["t_expand"] for r in step_reps)
     t_sym = statistics.mean(r["t_symbolic"] for r in step_reps)
-    stats = torch.tensor([t_local, t_sort, t_exp, t_sym], dtype=torch.float64, device=dev)
+    stats = torch.tensor([t_local, t_sort, t_exp, t_sym, t_count], dtype=torch.float64, device=dev)
     sums = torch.tensor([flop_local, nnz_local, a_band.nnz], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-    t_step, t_sort_max, t_exp_max, t_sym_max = stats.tolist()
+    t_step, t_sort_max, t_exp_max, t_sym_max, t_count_max = stats.tolist()
     flop, nnz_c, _ = (int(x) for x in sums.tolist())
 
     # e2e through the public API with host buffers (pinned), N>1: each rank its band
@@ -335,7 +336,7 @@ def run_gpu_arm(args):
                     "sort_merge": {"model_bytes": my_b_sort, "s": t_sort,
                                    "GBps": my_b_sort / t_sort / 1e9 if t_sort else None,
                                    "frac": my_b_sort / t_sort / 1e9 / peak if t_sort else None},
-                    "symbolic_s": t_sym}}
+                    "symbolic_s": t_sym, "bin_count_s": t_count}}
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
@@ -362,7 +363,7 @@ def run_gpu_arm(args):
         "gpu_launches": launches,
         "clocks": clocks,
         "phases_ms": {"symbolic": t_sym_max * 1e3, "expand": t_exp_max * 1e3,
-                      "sort_merge": t_sort_max * 1e3},
+                      "bin_count": t_count_max * 1e3, "sort_merge": t_sort_max * 1e3},
     }
     print(json.dumps(line), flush=True)
     if ws > 1:

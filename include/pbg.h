@@ -76,8 +76,9 @@ typedef struct pbg_config {
 } pbg_config;
 
 /* spgemm::PhaseReport times (report.hpp:26-33) measured with CUDA events,
- * plus the acceptance counters (acceptance.cpp:46-58). The fused sort+merge+
- * CSR kernel is reported in t_sort; t_compress and t_convert are 0. */
+ * plus the acceptance counters (acceptance.cpp:46-58). t_sort covers the
+ * per-bin distinct count, the offset scan and the fused sort+merge+CSR
+ * kernel; t_compress and t_convert are 0 (fused). */
 typedef struct pbg_report {
     double t_symbolic, t_expand, t_sort, t_compress, t_convert, t_total; /* seconds */
     double t_h2d, t_d2h;  /* host path only                                       */
@@ -89,6 +90,9 @@ typedef struct pbg_report {
     uint32_t heavy_bins;       /* bins larger than bin_cap (global-memory path)   */
     uint32_t bin_cap;
     uint64_t tuple_bytes;      /* bytes of tuple storage (12 B per tuple + pad)   */
+    uint64_t sort_fallbacks;   /* bins sorted by the LSD fallback (clustered keys) */
+    double t_count;            /* per-bin distinct-key count + offset scan (in t_sort) */
+    double t_sortmerge_kernel; /* the sort+merge+CSR kernel alone (in t_sort)     */
 } pbg_report;
 
 typedef struct pbg_handle pbg_handle;

@@ -48,7 +48,8 @@ class Report(C.Structure):
                 ("flop", u64), ("nnz_c", u64), ("nnz_a", u64), ("nnz_b", u64),
                 ("tuples_into_sort", u64), ("merged_total", u64),
                 ("nbins", u32), ("gpu_bins", u32), ("heavy_bins", u32), ("bin_cap", u32),
-                ("tuple_bytes", u64)]
+                ("tuple_bytes", u64), ("sort_fallbacks", u64),
+                ("t_count", f64), ("t_sortmerge_kernel", f64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -105,8 +106,10 @@ def _load(name: str, exports: dict):
 
 
 def pbg():
-    """libpbg.so: the sm_100a PB-SpGEMM kernels behind the C-ABI."""
-    return _load("libpbg.so", PBG_EXPORTS)
+    """libpbg.so: the sm_100a PB-SpGEMM kernels behind the C-ABI
+    (PBG_LIB=<name> selects an in-tree variant build, e.g. for A/B tuning)."""
+    import os
+    return _load(os.environ.get("PBG_LIB", "libpbg.so"), PBG_EXPORTS)
 
 
 def host():

@@ -13,6 +13,7 @@
 
 #include "pbg.h"
 #include "pbg_kernels.cuh"
+#include "pbg_sort.cuh"
 
 namespace {
 
@@ -81,10 +82,11 @@ enum Scalar : int {
     S_TUPLES_TOTAL,    // sum of cursors (tuples into sort)
     S_MERGED_TOTAL,    // sum of merged counts
     S_ERR,             // error bits (u32 in low word)
+    S_FALLBACKS,       // bins sorted by the LSD fallback
+    S_NNZ,             // nnz(C) from the distinct-count scan
     S_COUNT
 };
 constexpr int kTickets = 8;
-constexpr int kScans = 4;
 
 }  // namespace
 
@@ -92,10 +94,10 @@ struct pbg_context {
     int device = 0;
     int num_sms = 148;
     DevBuf colflop_off, row_flop, row_off, flags, row_bin, bin_rs, bin_cnt, bin_off, cursor,
-        status, chunk_p0, keys, vals, rowptr, zero_block, in_a_ptr, in_a_idx, in_a_val,
-        in_b_ptr, in_b_idx, in_b_val;
+        bin_out, chunk_p0, keys, vals, ccol, cval, rowptr, zero_block, in_a_ptr, in_a_idx,
+        in_a_val, in_b_ptr, in_b_idx, in_b_val;
     size_t zero_bytes = 0;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[8] = {};
     bool ev_ok = false;
     // last product
     uint64_t m = 0, k = 0, n = 0, nnz_c = 0, flop = 0;
@@ -105,9 +107,9 @@ struct pbg_context {
     bool have_result = false;
     ~pbg_context() {
         for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
-                          &bin_off, &cursor, &status, &chunk_p0, &keys, &vals, &rowptr,
-                          &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr, &in_b_idx,
-                          &in_b_val})
+                          &bin_off, &cursor, &bin_out, &chunk_p0, &keys, &vals, &ccol, &cval,
+                          &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
+                          &in_b_idx, &in_b_val})
             b->release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
@@ -172,7 +174,9 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     const uint64_t nnz_a = A.nnz;
     const uint64_t cap = cfg.bin_cap ? cfg.bin_cap : SM_CAP;
     const int cb = ceil_log2_u64(n);
-    uint32_t maxr = cb >= 32 ? 1u : (cb >= 22 ? (1u << (32 - cb)) : 1024u);
+    // rows per bin: local_row << col_bits | col must stay below 2^31 so keys
+    // never collide with the hash-set sentinel 0xffffffff
+    const uint32_t maxr = cb >= 31 ? 1u : (cb >= 21 ? (1u << (31 - cb)) : 1024u);
     ctx->m = m;
     ctx->k = k;
     ctx->n = n;
@@ -185,7 +189,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     // ---- workspace ----
     const uint64_t tiles_k = (k + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
     const uint64_t tiles_m = (m + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-    const uint64_t status_words = tiles_k + 3 * tiles_m;
+    const uint64_t status_words = tiles_k + 4 * tiles_m;
     const size_t zero_bytes = (S_COUNT + kTickets) * 8 + status_words * 8;
     if ((rc = grow(ctx->zero_block, zero_bytes))) return rc;
     if ((rc = grow(ctx->colflop_off, (k + 1) * 8))) return rc;
@@ -197,7 +201,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     if ((rc = grow(ctx->bin_cnt, (m + 1) * 8))) return rc;
     if ((rc = grow(ctx->bin_off, (m + 2) * 8))) return rc;
     if ((rc = grow(ctx->cursor, (m + 1) * 8))) return rc;
-    if ((rc = grow(ctx->status, (m + 1) * 8))) return rc;
+    if ((rc = grow(ctx->bin_out, (m + 2) * 8))) return rc;
     if ((rc = grow(ctx->rowptr, (m + 1) * 8))) return rc;
     if (!ctx->ev_ok) {
         for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
@@ -212,6 +216,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     unsigned long long* stat_m1 = stat_k + tiles_k;
     unsigned long long* stat_m2 = stat_m1 + tiles_m;
     unsigned long long* stat_m3 = stat_m2 + tiles_m;
+    unsigned long long* stat_m4 = stat_m3 + tiles_m;
 
     auto* colflop_off = static_cast<uint64_t*>(ctx->colflop_off.p);
     auto* row_flop = static_cast<unsigned long long*>(ctx->row_flop.p);
@@ -222,7 +227,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     auto* bin_cnt = static_cast<uint64_t*>(ctx->bin_cnt.p);
     auto* bin_off = static_cast<uint64_t*>(ctx->bin_off.p);
     auto* cursor = static_cast<unsigned long long*>(ctx->cursor.p);
-    auto* status = static_cast<unsigned long long*>(ctx->status.p);
+    auto* bin_out = static_cast<uint64_t*>(ctx->bin_out.p);
     auto* rowptr = static_cast<uint64_t*>(ctx->rowptr.p);
 
     CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
@@ -256,7 +261,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         k_binsizes<<<blocks_for(m, 256), 256, 0, st>>>(
             bin_rs, row_off, reinterpret_cast<const uint64_t*>(sc + S_NBINS), cap, bin_cnt,
-            bin_off, cursor, status, sc + S_HEAVY, sc + S_MAXBIN);
+            bin_off, cursor, sc + S_HEAVY, sc + S_MAXBIN);
         ++L;
         launch_scan(ArrayIn{bin_off}, bin_off, 0, reinterpret_cast<const uint64_t*>(sc + S_NBINS),
                     m, stat_m3, tickets + 3, sc + S_TUPLE_CAP, nullptr, st);
@@ -302,6 +307,10 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     } else {
         if ((rc = grow(ctx->keys, tcap * 4))) return rc;
         if ((rc = grow(ctx->vals, tcap * 8))) return rc;
+        // C arrays sized to the flop upper bound (nnz(C) <= flop): no sync
+        // for nnz(C) before the sort kernel
+        if ((rc = grow(ctx->ccol, flop * 4))) return rc;
+        if ((rc = grow(ctx->cval, flop * 8))) return rc;
         CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
         auto* keys = static_cast<uint32_t*>(ctx->keys.p);
         auto* vals = static_cast<double*>(ctx->vals.p);
@@ -323,30 +332,61 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
+        // ---- distinct keys per bin -> output offset of every bin ----
+        uint64_t* bin_nnz = flags;  // free after k_binrows
+        const uint64_t* nb_dev = reinterpret_cast<const uint64_t*>(sc + S_NBINS);
+        static bool cnt_attr[64] = {};
+        const size_t cnt_smem = CNT_SLOTS * 4;
+        if (!cnt_attr[ctx->device & 63]) {
+            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(cnt_smem)));
+            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          100));
+            cnt_attr[ctx->device & 63] = true;
+        }
+        int cnt_per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cnt_per_sm, k_bincount, CNT_NT, cnt_smem);
+        k_bincount<<<static_cast<unsigned>(std::min<uint64_t>(
+                         nb, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
+                     CNT_NT, cnt_smem, st>>>(keys, bin_off, bin_cnt, nb_dev, cap, bin_nnz);
+        ++L;
+        launch_scan(ArrayIn{bin_nnz}, bin_out, 0, nb_dev, m, stat_m4, tickets + 5,
+                    sc + S_NNZ, nullptr, st);
+        ++L;
+        CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
         static bool attr_set[64] = {};
         if (!attr_set[ctx->device & 63]) {
             CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(sizeof(SortSmem))));
+            CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          100));
             attr_set[ctx->device & 63] = true;
         }
-        SortArgs sa{bin_rs,
-                    bin_cnt,
-                    bin_off,
-                    cursor,
-                    reinterpret_cast<const uint64_t*>(sc + S_NBINS),
-                    status,
-                    tickets + 4,
-                    keys,
-                    vals,
-                    rowptr,
-                    m,
-                    cb,
-                    sc + S_TUPLES_TOTAL,
-                    sc + S_MERGED_TOTAL,
-                    reinterpret_cast<unsigned int*>(sc + S_ERR)};
-        const unsigned sm_blocks =
-            static_cast<unsigned>(std::min<uint64_t>(nb, 2ull * ctx->num_sms));
+        SortArgs sa{};
+        sa.bin_rs = bin_rs;
+        sa.bin_cnt = bin_cnt;
+        sa.bin_off = bin_off;
+        sa.cursor = cursor;
+        sa.nb_dev = nb_dev;
+        sa.bin_out = bin_out;
+        sa.bin_nnz = bin_nnz;
+        sa.ticket = tickets + 4;
+        sa.keys = keys;
+        sa.vals = vals;
+        sa.ccol = static_cast<uint32_t*>(ctx->ccol.p);
+        sa.cval = static_cast<double*>(ctx->cval.p);
+        sa.rowptr = rowptr;
+        sa.m = m;
+        sa.col_bits = cb;
+        sa.tuples_total = sc + S_TUPLES_TOTAL;
+        sa.merged_total = sc + S_MERGED_TOTAL;
+        sa.err = reinterpret_cast<unsigned int*>(sc + S_ERR);
+        sa.fallbacks = sc + S_FALLBACKS;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge, SM_NT, sizeof(SortSmem));
+        const unsigned sm_blocks = static_cast<unsigned>(
+            std::min<uint64_t>(nb, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
         k_sortmerge<<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
@@ -358,8 +398,11 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ctx->nnz_c = nnz;
         ctx->rep.tuples_into_sort = hs[S_TUPLES_TOTAL];
         ctx->rep.merged_total = hs[S_MERGED_TOTAL];
+        ctx->rep.sort_fallbacks = hs[S_FALLBACKS];
         const unsigned err = static_cast<unsigned>(hs[S_ERR]);
         if (err & 2u) return fail(PBG_ERR_UNIMPLEMENTED, "bin above shared-memory capacity");
+        if (err & 4u || hs[S_NNZ] != nnz)
+            return fail(PBG_ERR_INTERNAL, "merged counts disagree with the distinct-key counts");
         if (err & 1u || hs[S_TUPLES_TOTAL] != flop)
             return fail(PBG_ERR_INTERNAL, "tuple conservation broken: expanded " +
                                               std::to_string(hs[S_TUPLES_TOTAL]) + " of " +
@@ -373,6 +416,13 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     CUDA_TRY(cudaEventElapsedTime(&t_sym, ctx->ev[0], ctx->ev[1]));
     CUDA_TRY(cudaEventElapsedTime(&t_exp, ctx->ev[flop == 0 || m == 0 ? 1 : 5], ctx->ev[2]));
     CUDA_TRY(cudaEventElapsedTime(&t_sort, ctx->ev[2], ctx->ev[3]));
+    float t_cnt = 0, t_sm = 0;
+    if (flop != 0 && m != 0) {
+        CUDA_TRY(cudaEventElapsedTime(&t_cnt, ctx->ev[2], ctx->ev[6]));
+        CUDA_TRY(cudaEventElapsedTime(&t_sm, ctx->ev[6], ctx->ev[3]));
+    }
+    ctx->rep.t_count = t_cnt * 1e-3;
+    ctx->rep.t_sortmerge_kernel = t_sm * 1e-3;
     CUDA_TRY(cudaEventElapsedTime(&t_tot, ctx->ev[0], ctx->ev[4]));
     ctx->rep.t_symbolic = t_sym * 1e-3;
     ctx->rep.t_expand = t_exp * 1e-3;
@@ -507,8 +557,8 @@ int pbg_context_result(pbg_context* ctx, const uint64_t** rowptr, const uint32_t
                        const double** values) {
     if (!ctx || !ctx->have_result) return fail(PBG_ERR_ARG, "no product in this context");
     if (rowptr) *rowptr = static_cast<const uint64_t*>(ctx->rowptr.p);
-    if (colids) *colids = static_cast<const uint32_t*>(ctx->keys.p);
-    if (values) *values = static_cast<const double*>(ctx->vals.p);
+    if (colids) *colids = static_cast<const uint32_t*>(ctx->ccol.p);
+    if (values) *values = static_cast<const double*>(ctx->cval.p);
     return PBG_OK;
 }
 
@@ -629,9 +679,9 @@ int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double
     cudaEventRecord(e0, nullptr);
     if (rowptr) CUDA_TRY(cudaMemcpyAsync(rowptr, ctx->rowptr.p, (ctx->m + 1) * 8, cudaMemcpyDeviceToHost, nullptr));
     if (colids && ctx->nnz_c)
-        CUDA_TRY(cudaMemcpyAsync(colids, ctx->keys.p, ctx->nnz_c * 4, cudaMemcpyDeviceToHost, nullptr));
+        CUDA_TRY(cudaMemcpyAsync(colids, ctx->ccol.p, ctx->nnz_c * 4, cudaMemcpyDeviceToHost, nullptr));
     if (values && ctx->nnz_c)
-        CUDA_TRY(cudaMemcpyAsync(values, ctx->vals.p, ctx->nnz_c * 8, cudaMemcpyDeviceToHost, nullptr));
+        CUDA_TRY(cudaMemcpyAsync(values, ctx->cval.p, ctx->nnz_c * 8, cudaMemcpyDeviceToHost, nullptr));
     cudaEventRecord(e1, nullptr);
     CUDA_TRY(cudaEventSynchronize(e1));
     float ms = 0;

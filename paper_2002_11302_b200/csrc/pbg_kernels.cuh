@@ -207,19 +207,18 @@ __global__ void k_binrows(const uint64_t* __restrict__ flag_excl, uint64_t m, ui
 }
 
 // Per-bin tuple count, 4-tuple padded capacity (16-B aligned key runs),
-// cursor/status reset, heavy-bin count.
+// cursor reset, heavy-bin count.
 __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
                            const uint64_t* __restrict__ row_off, const uint64_t* nb_dev,
                            uint64_t cap, uint64_t* bin_cnt, uint64_t* bin_pad,
-                           unsigned long long* cursor, unsigned long long* status,
-                           unsigned long long* heavy, unsigned long long* maxbin) {
+                           unsigned long long* cursor, unsigned long long* heavy,
+                           unsigned long long* maxbin) {
     const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (b >= *nb_dev) return;
     const uint64_t c = row_off[bin_rs[b + 1]] - row_off[bin_rs[b]];
     bin_cnt[b] = c;
     bin_pad[b] = (c + 3) & ~3ull;
     cursor[b] = 0;
-    status[b] = 0;
     if (c > cap) atomicAdd(heavy, 1ull);
     atomicMax(maxbin, static_cast<unsigned long long>(c));
 }
@@ -369,224 +368,77 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
     }
 }
 
-// ----------------------------------------------------------- sort+merge --
-constexpr int SM_NT = 512;
-constexpr int SM_NW = SM_NT / 32;
-constexpr int SM_CAP = 4096;                 // max tuples per smem bin
-constexpr int SM_PER_WARP = SM_CAP / SM_NW;  // 256
-constexpr int SM_ITEMS = SM_PER_WARP / 32;   // 8
+// ------------------------------------------------------- bin nnz count --
+// Distinct keys per bin = the bin's merged count (its share of nnz(C)),
+// counted from the keys alone with a shared-memory hash set (load <= 1/8 for
+// a full bin, so probe chains stay short and warps rarely diverge). A scan of
+// these counts gives every bin its output offset before the sort+merge
+// kernel runs. Bins above `cap` are skipped (heavy-row path).
+constexpr int CNT_NT = 512;
+constexpr int CNT_SLOTS_LOG = 14;
+constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
+constexpr uint32_t CNT_EMPTY = 0xffffffffu;
+constexpr int CNT_PER = 8;  // keys per thread for a bin of CNT_NT*CNT_PER tuples
 
-struct SortArgs {
-    const uint32_t* bin_rs;
-    const uint64_t* bin_cnt;
-    const uint64_t* bin_off;
-    const unsigned long long* cursor;
-    const uint64_t* nb_dev;
-    unsigned long long* status;
-    unsigned int* ticket;
-    uint32_t* keys;  // tuple keys in, C colids out (in place)
-    double* vals;    // tuple values in, C values out (in place)
-    uint64_t* rowptr;
-    uint64_t m;
-    int col_bits;
-    unsigned long long* tuples_total;
-    unsigned long long* merged_total;
-    unsigned int* err;  // bit0 conservation, bit1 heavy bin reached the smem path
-};
-
-struct SortSmem {
-    uint32_t k[2][SM_CAP];
-    double v[2][SM_CAP];
-    uint16_t cnt[256 * SM_NW];
-    uint32_t s_warp32[SM_NW + 1];
-    uint64_t s_bin;
-    uint64_t s_prefix;
-};
-
-// Per-bin sort + merge + CSR rows (sort_bins/compress_bins/convert_csr,
-// pb_spgemm.cpp:260-328). Persistent CTAs take bins in ticket order, so the
-// output offset of bin b is the look-back prefix of the merged counts of
-// bins < b, and C is written straight to its final place. C overlays the
-// tuple arrays: bin b writes [P_b, P_b+U_b) with P_b+U_b <= off_{b+1}, and
-// every bin < b has finished reading before it published its count.
-// Sort: stable LSD radix on 8-bit digits over only the key bits the bin uses
-// (row bits of its span + col bits — the reference skips constant bytes,
-// pb_spgemm.hpp:188-195, to the same effect); ranks from match.any per warp,
-// per-(digit, warp) counters scanned digit-major.
-__global__ void __launch_bounds__(SM_NT, 2) k_sortmerge(SortArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+__global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict__ keys,
+                                                   const uint64_t* __restrict__ bin_off,
+                                                   const uint64_t* __restrict__ bin_cnt,
+                                                   const uint64_t* nb_dev, uint64_t cap,
+                                                   uint64_t* bin_nnz) {
+    extern __shared__ __align__(16) uint32_t table[];  // CNT_SLOTS
+    __shared__ uint32_t s_red[2][CNT_NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const uint32_t lt = lanemask_lt();
-    const uint64_t nb = *a.nb_dev;
-    const int cb = a.col_bits;
-    const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
-
-    while (true) {
-        if (tid == 0) sm.s_bin = atomicAdd(a.ticket, 1u);
+    const uint64_t nb = *nb_dev;
+    for (int i = tid; i < CNT_SLOTS / 4; i += CNT_NT)
+        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
+    __syncthreads();
+    int par = 0;
+    for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const uint64_t n = bin_cnt[b];
+        if (n > cap || n > static_cast<uint64_t>(CNT_NT) * CNT_PER) {
+            if (tid == 0) bin_nnz[b] = 0;
+            continue;
+        }
+        const uint32_t* kb = keys + bin_off[b];
+        uint32_t slot[CNT_PER], kk[CNT_PER];
+        uint32_t fresh = 0;
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j) {  // all loads in flight first
+            const uint32_t i = tid + j * CNT_NT;
+            kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
+        }
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j) {
+            slot[j] = CNT_SLOTS;  // none
+            const uint32_t key = kk[j];
+            if (tid + j * CNT_NT < n) {
+                uint32_t h = (key * 0x9E3779B1u) >> (32 - CNT_SLOTS_LOG);
+                while (true) {
+                    const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
+                    if (old == CNT_EMPTY) {
+                        ++fresh;
+                        slot[j] = h;
+                        break;
+                    }
+                    if (old == key) break;
+                    h = (h + 1) & (CNT_SLOTS - 1);
+                }
+            }
+        }
+        fresh = warp_sum(fresh);
+        if (lane == 0) s_red[par][w] = fresh;
         __syncthreads();
-        const uint64_t b = sm.s_bin;
-        if (b >= nb) break;
-        const uint32_t rs = a.bin_rs[b], re = a.bin_rs[b + 1];
-        const uint64_t n = a.bin_cnt[b];
-        const uint64_t off = a.bin_off[b];
+        // reset only the slots this thread claimed: the table is clean for the
+        // next bin without a full clear
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j)
+            if (slot[j] < CNT_SLOTS) table[slot[j]] = CNT_EMPTY;
         if (tid == 0) {
-            const uint64_t cur = a.cursor[b];
-            if (cur != n) atomicOr(a.err, 1u);
-            atomicAdd(a.tuples_total, (unsigned long long)cur);
+            uint32_t t = 0;
+            for (int i = 0; i < CNT_NT / 32; ++i) t += s_red[par][i];
+            bin_nnz[b] = t;
         }
-        int cbuf = 0;
-        uint32_t U = 0;
-        if (n > SM_CAP) {
-            if (tid == 0) atomicOr(a.err, 2u);
-        } else if (n > 0) {
-            // ---- stage the bin in shared memory (16-B vector loads) ----
-            const uint4* k4 = reinterpret_cast<const uint4*>(a.keys + off);
-            const double2* v2 = reinterpret_cast<const double2*>(a.vals + off);
-            const uint32_t n4 = static_cast<uint32_t>((n + 3) / 4);
-            for (uint32_t i = tid; i < n4; i += SM_NT) {
-                const uint4 kk = __ldcs(k4 + i);
-                *reinterpret_cast<uint4*>(&sm.k[0][4 * i]) = kk;
-            }
-            const uint32_t n2 = static_cast<uint32_t>((n + 1) / 2);
-            for (uint32_t i = tid; i < n2; i += SM_NT) {
-                const double2 vv = __ldcs(v2 + i);
-                *reinterpret_cast<double2*>(&sm.v[0][2 * i]) = vv;
-            }
-            __syncthreads();
-            // ---- LSD radix sort over the used key bits ----
-            const uint32_t span = re - rs;
-            const int rbits = span > 1 ? 32 - __clz(span - 1) : 0;
-            const int bits = rbits + cb;
-            uint32_t kr[SM_ITEMS];
-#pragma unroll
-            for (int it = 0; it < SM_ITEMS; ++it) {
-                const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
-                kr[it] = idx < n ? sm.k[0][idx] : 0u;
-            }
-            if (n > 1) {
-                for (int shift = 0; shift < bits; shift += 8) {
-                    for (int i = tid; i < 256 * SM_NW / 2; i += SM_NT)
-                        reinterpret_cast<uint32_t*>(sm.cnt)[i] = 0u;
-                    __syncthreads();
-                    uint16_t rank[SM_ITEMS];
-                    uint32_t dig[SM_ITEMS];
-#pragma unroll
-                    for (int it = 0; it < SM_ITEMS; ++it) {
-                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
-                        const bool valid = idx < n;
-                        const uint32_t d = valid ? ((kr[it] >> shift) & 0xffu) : 0x100u;
-                        const uint32_t peers = __match_any_sync(FULL, d);
-                        const uint16_t old = valid ? sm.cnt[d * SM_NW + w] : 0;
-                        rank[it] = old + __popc(peers & lt);
-                        dig[it] = d;
-                        __syncwarp();
-                        if (valid && (peers & lt) == 0) sm.cnt[d * SM_NW + w] = old + __popc(peers);
-                        __syncwarp();
-                    }
-                    __syncthreads();
-                    // exclusive scan of the 4096 counters, digit-major
-                    {
-                        uint32_t c8[8];
-                        uint32_t s8 = 0;
-                        const uint4 raw = reinterpret_cast<const uint4*>(sm.cnt)[tid];
-                        const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            c8[2 * j] = rw[j] & 0xffffu;
-                            c8[2 * j + 1] = rw[j] >> 16;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) s8 += c8[j];
-                        uint32_t tot;
-                        uint32_t run = block_exclusive_scan<SM_NT>(s8, sm.s_warp32, tot);
-                        uint32_t ow[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint32_t lo = run;
-                            run += c8[2 * j];
-                            const uint32_t hi = run;
-                            run += c8[2 * j + 1];
-                            ow[j] = lo | (hi << 16);
-                        }
-                        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int it = 0; it < SM_ITEMS; ++it) {
-                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
-                        if (idx < n) {
-                            const uint32_t pos = sm.cnt[dig[it] * SM_NW + w] + rank[it];
-                            sm.k[cbuf ^ 1][pos] = kr[it];
-                            sm.v[cbuf ^ 1][pos] = sm.v[cbuf][idx];
-                        }
-                    }
-                    __syncthreads();
-                    cbuf ^= 1;
-#pragma unroll
-                    for (int it = 0; it < SM_ITEMS; ++it) {
-                        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
-                        if (idx < n) kr[it] = sm.k[cbuf][idx];
-                    }
-                }
-            }
-            // ---- merge equal keys (compress_bin_records, pb_spgemm.hpp:202-216) ----
-            {
-                const uint32_t* K = sm.k[cbuf];
-                const double* V = sm.v[cbuf];
-                uint32_t* KO = sm.k[cbuf ^ 1];
-                double* VO = sm.v[cbuf ^ 1];
-                const uint32_t i0 = tid * 8;
-                uint32_t heads = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t i = i0 + j;
-                    if (i < n && (i == 0 || K[i] != K[i - 1])) ++heads;
-                }
-                uint32_t tot;
-                uint32_t u = block_exclusive_scan<SM_NT>(heads, sm.s_warp32, tot);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t i = i0 + j;
-                    if (i < n && (i == 0 || K[i] != K[i - 1])) {
-                        const uint32_t key = K[i];
-                        double s = V[i];
-                        for (uint32_t e = i + 1; e < n && K[e] == key; ++e) s += V[e];
-                        KO[u] = key;
-                        VO[u] = s;
-                        ++u;
-                    }
-                }
-                U = tot;
-                cbuf ^= 1;
-            }
-        }
-        // ---- output offset by look-back over merged counts ----
-        if (tid < 32) {
-            const uint64_t pfx = lookback_warp(a.status, b, U);
-            if (tid == 0) sm.s_prefix = pfx;
-        }
-        __syncthreads();
-        const uint64_t P = sm.s_prefix;
-        const uint32_t* K = sm.k[cbuf];
-        const double* V = sm.v[cbuf];
-        for (uint32_t u = tid; u < U; u += SM_NT) {
-            const uint32_t key = K[u];
-            __stcs(a.keys + P + u, key & colmask);
-            __stcs(a.vals + P + u, V[u]);
-            const uint32_t row = static_cast<uint32_t>(static_cast<uint64_t>(key) >> cb);
-            const int64_t prow = u == 0 ? -1 : static_cast<int64_t>(static_cast<uint64_t>(K[u - 1]) >> cb);
-            for (int64_t r = prow + 1; r <= row; ++r) a.rowptr[rs + r] = P + u;
-        }
-        {
-            const int64_t lastrow = U == 0 ? -1 : static_cast<int64_t>(static_cast<uint64_t>(K[U - 1]) >> cb);
-            for (int64_t r = lastrow + 1 + tid; r < static_cast<int64_t>(re - rs); r += SM_NT)
-                a.rowptr[rs + r] = P + U;
-        }
-        if (tid == 0) {
-            if (b == nb - 1) a.rowptr[a.m] = P + U;
-            atomicAdd(a.merged_total, (unsigned long long)U);
-        }
+        par ^= 1;
         __syncthreads();
     }
 }

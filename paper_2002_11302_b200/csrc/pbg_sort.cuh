@@ -1,0 +1,426 @@
+// pbg_sort.cuh — per-bin sort + duplicate merge + CSR assembly (one kernel).
+//
+// Replaces sort_bins -> sort_bin_records (American-flag MSD radix with an
+// insertion-sort cutoff, pb_spgemm.hpp:118-197), compress_bins ->
+// compress_bin_records (two-pointer merge, pb_spgemm.hpp:202-216) and
+// convert_csr (pb_spgemm.cpp:288-328).
+//
+// Persistent CTAs take bins in ticket order. A bin holds <= SM_CAP tuples
+// (u32 key = local_row << col_bits | col, f64 value). Per bin:
+//   0. the bin arrives in shared memory by two TMA bulk copies
+//      (cp.async.bulk, mbarrier completion) issued while the CTA was still
+//      busy with the previous bin;
+//   1. MSD bucket pass: SM_CAP buckets on the top used key bits (smem
+//      histogram -> scan -> scatter) — the reference's first radix level,
+//      wide enough that buckets hold ~1 tuple;
+//   2. rank inside the bucket (smaller keys, ties by position): every tuple
+//      lands at its sorted position. A bucket above SM_BMAX (clustered or
+//      duplicate-heavy keys) switches the bin to a stable LSD radix sort;
+//   3. duplicate keys are summed (two-pointer merge semantics: exact zeros
+//      are kept) and compacted;
+//   4. colids / values / rowptr are written at the bin's output offset P_b,
+//      known before the kernel starts (k_bincount counts each bin's
+//      distinct keys, a scan turns them into offsets), so bins are fully
+//      independent: no look-back chain, no waiting on slower neighbours.
+//      (A single-pass decoupled look-back over U_b was measured 2-3x slower:
+//      per-bin work is long and uneven, so every CTA ended up waiting on the
+//      slowest in-flight predecessor.)
+#pragma once
+
+#include <cstdint>
+
+#include "pbg_device.cuh"
+
+namespace pbg {
+
+#ifndef PBG_SM_CAP
+#define PBG_SM_CAP 2048
+#endif
+#ifndef PBG_SM_NT
+#define PBG_SM_NT 256
+#endif
+
+constexpr int SM_NT = PBG_SM_NT;
+constexpr int SM_NW = SM_NT / 32;
+constexpr int SM_CAP = PBG_SM_CAP;            // max tuples per smem bin
+constexpr int SM_NB = SM_CAP;                 // buckets of the MSD pass
+constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
+constexpr int SM_BMAX = 32;                   // largest bucket ranked in place
+constexpr int SM_ITEMS = SM_CAP / SM_NT;      // 8
+constexpr int SM_PER_WARP = SM_CAP / SM_NW;
+constexpr int SM_NBUF = 2;                    // ping, pong
+static_assert(SM_ITEMS == 8, "one uint4 of u16 counters per thread");
+static_assert(SM_NB * 2 / 16 == SM_NT, "counter scan layout");
+
+struct SortArgs {
+    const uint32_t* bin_rs;
+    const uint64_t* bin_cnt;
+    const uint64_t* bin_off;
+    const unsigned long long* cursor;
+    const uint64_t* nb_dev;
+    const uint64_t* bin_out;  // output offset of every bin (scan of k_bincount)
+    const uint64_t* bin_nnz;  // distinct keys per bin (k_bincount), cross-checked
+    unsigned int* ticket;
+    const uint32_t* keys;  // tuples
+    const double* vals;
+    uint32_t* ccol;        // C colids
+    double* cval;          // C values
+    uint64_t* rowptr;
+    uint64_t m;
+    int col_bits;
+    unsigned long long* tuples_total;
+    unsigned long long* merged_total;
+    unsigned int* err;  // bit0 conservation, bit1 heavy bin reached the smem path,
+                        // bit2 merged count != k_bincount's distinct count
+    unsigned long long* fallbacks;
+};
+
+struct SortSmem {
+    uint32_t k[SM_NBUF][SM_CAP];
+    double v[SM_NBUF][SM_CAP];
+    uint16_t cnt[SM_NB];  // bucket histogram -> bucket ends; LSD per-warp counters
+    uint32_t s_warp32[SM_NW + 1];
+    unsigned long long mbar;
+    uint64_t s_next;
+    uint32_t s_loaded;
+};
+
+// ---- TMA bulk copy (global -> shared) with mbarrier completion ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Thread 0: take the next ticket and, for a bin that fits, start its copy
+// into buffer `buf` (generic-proxy accesses to it are finished: caller syncs).
+__device__ __forceinline__ void prefetch_next(const SortArgs& a, SortSmem& sm, int buf,
+                                              uint64_t nb) {
+    const uint64_t b = atomicAdd(a.ticket, 1u);
+    sm.s_next = b;
+    sm.s_loaded = 0;
+    if (b < nb) {
+        const uint64_t n = a.bin_cnt[b];
+        if (n > 0 && n <= SM_CAP) {
+            const uint64_t off = a.bin_off[b];
+            const uint32_t kb = static_cast<uint32_t>((n * 4 + 15) & ~15ull);
+            const uint32_t vb = static_cast<uint32_t>((n * 8 + 15) & ~15ull);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.mbar, kb + vb);
+            bulk_g2s(sm.k[buf], a.keys + off, kb, &sm.mbar);
+            bulk_g2s(sm.v[buf], a.vals + off, vb, &sm.mbar);
+            sm.s_loaded = 1;
+        }
+    }
+}
+
+// Exclusive scan of the SM_NB u16 counters in index order (8 per thread).
+__device__ __forceinline__ void scan_cnt(SortSmem& sm) {
+    const int tid = threadIdx.x;
+    const uint4 raw = reinterpret_cast<const uint4*>(sm.cnt)[tid];
+    const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
+    uint32_t c8[8];
+    uint32_t s8 = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        c8[2 * j] = rw[j] & 0xffffu;
+        c8[2 * j + 1] = rw[j] >> 16;
+        s8 += c8[2 * j] + c8[2 * j + 1];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<SM_NT>(s8, sm.s_warp32, tot);
+    uint32_t ow[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t lo = run;
+        run += c8[2 * j];
+        const uint32_t hi = run;
+        run += c8[2 * j + 1];
+        ow[j] = lo | (hi << 16);
+    }
+    reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+}
+
+// Stable LSD radix sort of buffer `x` (n <= SM_CAP) over `bits` key bits,
+// 8-bit digits, ping-ponging with buffer `y`. Ranks from match.any per warp in
+// element order, per-(warp, digit) counters cnt[w*256+d] scanned digit-major.
+// Returns the buffer holding the result.
+__device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits) {
+    static_assert(SM_NW * 256 <= SM_NB, "LSD counters fit the bucket counters");
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    int cur = x, nxt = y;
+    uint32_t kr[SM_ITEMS];
+#pragma unroll
+    for (int it = 0; it < SM_ITEMS; ++it) {
+        const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+        kr[it] = idx < n ? sm.k[cur][idx] : 0u;
+    }
+    for (int shift = 0; shift < bits; shift += 8) {
+        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        uint16_t rank[SM_ITEMS];
+        uint32_t dig[SM_ITEMS];
+        uint16_t* wc = sm.cnt + w * 256;
+#pragma unroll
+        for (int it = 0; it < SM_ITEMS; ++it) {
+            const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+            const bool valid = idx < n;
+            const uint32_t d = valid ? ((kr[it] >> shift) & 0xffu) : 0x100u;
+            const uint32_t peers = __match_any_sync(FULL, d);
+            const uint16_t old = valid ? wc[d] : 0;
+            rank[it] = old + __popc(peers & lt);
+            dig[it] = d;
+            __syncwarp();
+            if (valid && (peers & lt) == 0) wc[d] = old + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        {  // digit-major exclusive scan over (digit, warp)
+            constexpr int PER = SM_NW * 256 / SM_NT;  // counters per thread
+            constexpr int TPD = SM_NW / PER;          // threads per digit
+            const int d = tid / TPD, w0 = (tid % TPD) * PER;
+            uint32_t c[PER], s = 0;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                c[j] = sm.cnt[(w0 + j) * 256 + d];
+                s += c[j];
+            }
+            uint32_t tot;
+            uint32_t run = block_exclusive_scan<SM_NT>(s, sm.s_warp32, tot);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                sm.cnt[(w0 + j) * 256 + d] = static_cast<uint16_t>(run);
+                run += c[j];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < SM_ITEMS; ++it) {
+            const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+            if (idx < n) {
+                const uint32_t pos = wc[dig[it]] + rank[it];
+                sm.k[nxt][pos] = kr[it];
+                sm.v[nxt][pos] = sm.v[cur][idx];
+            }
+        }
+        __syncthreads();
+        const int t = cur;
+        cur = nxt;
+        nxt = t;
+#pragma unroll
+        for (int it = 0; it < SM_ITEMS; ++it) {
+            const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
+            if (idx < n) kr[it] = sm.k[cur][idx];
+        }
+    }
+    return cur;
+}
+
+// Sum equal-key runs of sorted buffer `x` into buffer `y`, compacted.
+// Warp w owns elements [w*PER_WARP, +PER_WARP), lane-striped.
+__device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint32_t n) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t* K = sm.k[x];
+    const double* V = sm.v[x];
+    uint32_t* KO = sm.k[y];
+    double* VO = sm.v[y];
+    uint32_t masks[SM_ITEMS];
+    uint32_t heads = 0;
+#pragma unroll
+    for (int it = 0; it < SM_ITEMS; ++it) {
+        const uint32_t i = w * SM_PER_WARP + it * 32 + lane;
+        const bool h = i < n && (i == 0 || K[i] != K[i - 1]);
+        masks[it] = __ballot_sync(FULL, h);
+        heads += __popc(masks[it]);
+    }
+    uint32_t tot;
+    uint32_t base = block_exclusive_scan<SM_NT>(lane == 0 ? heads : 0u, sm.s_warp32, tot);
+    base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+    for (int it = 0; it < SM_ITEMS; ++it) {
+        const uint32_t i = w * SM_PER_WARP + it * 32 + lane;
+        if ((masks[it] >> lane) & 1u) {
+            const uint32_t u = base + __popc(masks[it] & lt);
+            const uint32_t key = K[i];
+            double s = V[i];
+            for (uint32_t e = i + 1; e < n && K[e] == key; ++e) s += V[e];
+            KO[u] = key;
+            VO[u] = s;
+        }
+        base += __popc(masks[it]);
+    }
+    return tot;
+}
+
+// Sort + merge the bin in buffer `in` using scratch buffer `scr`. Returns the
+// merged count; *res gets the buffer holding the merged output.
+__device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
+                                   int bits, int* res) {
+    const int tid = threadIdx.x;
+    uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);
+    const int sh = bits > SM_NB_BITS ? bits - SM_NB_BITS : 0;
+    // ---- 1. bucket histogram / scan / scatter in -> scr ----
+    for (uint32_t i = tid; i < n; i += SM_NT) {
+        const uint32_t d = sm.k[in][i] >> sh;
+        atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
+    }
+    __syncthreads();
+    scan_cnt(sm);
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += SM_NT) {
+        const uint32_t key = sm.k[in][i];
+        const uint32_t d = key >> sh;
+        const uint32_t old = atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
+        const uint32_t pos = (old >> ((d & 1) * 16)) & 0xffffu;
+        sm.k[scr][pos] = key;
+        sm.v[scr][pos] = sm.v[in][i];
+    }
+    __syncthreads();
+    // ---- 2. rank inside buckets scr -> in (cnt[d] = end of bucket d) ----
+    bool big = false;
+    for (uint32_t i = tid; i < n; i += SM_NT) {
+        const uint32_t key = sm.k[scr][i];
+        const uint32_t d = key >> sh;
+        const uint32_t lo = d ? sm.cnt[d - 1] : 0u, hi = sm.cnt[d];
+        if (hi - lo > SM_BMAX) {
+            big = true;
+            continue;
+        }
+        uint32_t r = 0;
+#pragma unroll 1
+        for (uint32_t j = lo; j < hi; ++j) {
+            const uint32_t kj = sm.k[scr][j];
+            r += (kj < key) | ((kj == key) & (j < i));
+        }
+        sm.k[in][lo + r] = key;
+        sm.v[in][lo + r] = sm.v[scr][i];
+    }
+    const bool any_big = __syncthreads_or(big);
+    int sorted, other;
+    if (any_big) {
+        // clustered keys: stable LSD radix on scr (a permutation of the bin)
+        sorted = lsd_sort(sm, scr, in, n, bits);
+        other = sorted == scr ? in : scr;
+        if (tid == 0) atomicAdd(a.fallbacks, 1ull);
+    } else {
+        sorted = in;
+        other = scr;
+    }
+    bool dup = false;
+    for (uint32_t i = tid + 1; i < n; i += SM_NT) dup |= sm.k[sorted][i] == sm.k[sorted][i - 1];
+    // ---- 3. merge duplicates ----
+    if (__syncthreads_or(dup)) {
+        *res = other;
+        return merge_dups(sm, sorted, other, n);
+    }
+    *res = sorted;
+    return n;
+}
+
+// Write a resolved bin: colids / values at P, rowptr of its rows.
+__device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm, int buf,
+                                          uint64_t b, uint64_t nb, uint32_t rs, uint32_t re,
+                                          uint32_t U, uint64_t P) {
+    const int tid = threadIdx.x;
+    const int cb = a.col_bits;
+    const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
+    const uint32_t* K = sm.k[buf];
+    const double* V = sm.v[buf];
+    uint32_t* okeys = a.ccol + P;
+    double* ovals = a.cval + P;
+    for (uint32_t u = tid; u < U; u += SM_NT) {
+        __stcs(okeys + u, K[u] & colmask);
+        __stcs(ovals + u, V[u]);
+    }
+    // rowptr[rs + r] = P + first merged entry of local row r (binary search)
+    const uint32_t span = re - rs;
+    for (uint32_t r = tid; r < span; r += SM_NT) {
+        const uint64_t target = static_cast<uint64_t>(r) << cb;
+        uint32_t lo = 0, hi = U;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (static_cast<uint64_t>(K[mid]) < target) lo = mid + 1;
+            else hi = mid;
+        }
+        a.rowptr[rs + r] = P + lo;
+    }
+    if (tid == 0 && b == nb - 1) a.rowptr[a.m] = P + U;
+}
+
+__global__ void __launch_bounds__(SM_NT, 4) k_sortmerge(SortArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const uint64_t nb = *a.nb_dev;
+
+    if (tid == 0) {
+        mbar_init(&sm.mbar, 1);
+        prefetch_next(a, sm, 0, nb);
+    }
+    __syncthreads();
+    uint32_t parity = 0;
+    int inb = 0;  // buffer the current bin was copied into
+
+    while (true) {
+        const uint64_t b = sm.s_next;
+        if (b >= nb) break;
+        const bool loaded = sm.s_loaded != 0;
+        const uint32_t rs = a.bin_rs[b], re = a.bin_rs[b + 1];
+        const uint64_t n64 = a.bin_cnt[b];
+        if (tid == 0) {
+            const uint64_t cur = a.cursor[b];
+            if (cur != n64) atomicOr(a.err, 1u);
+            atomicAdd(a.tuples_total, (unsigned long long)cur);
+            if (n64 > SM_CAP) atomicOr(a.err, 2u);
+        }
+        int res = inb;
+        uint32_t U = 0;
+        if (loaded) {
+            reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+            const uint32_t span = re - rs;
+            const int bits = (span > 1 ? 32 - __clz(span - 1) : 0) + a.col_bits;
+            mbar_wait(&sm.mbar, parity);
+            parity ^= 1;
+            __syncthreads();
+            U = sort_merge_bin(a, sm, inb, inb ^ 1, static_cast<uint32_t>(n64), bits, &res);
+        }
+        __syncthreads();
+        // next bin's copy into the free buffer overlaps this bin's output
+        if (tid == 0) {
+            prefetch_next(a, sm, res ^ 1, nb);
+            if (loaded && U != a.bin_nnz[b]) atomicOr(a.err, 4u);
+            atomicAdd(a.merged_total, (unsigned long long)U);
+        }
+        write_bin(a, sm, res, b, nb, rs, re, U, a.bin_out[b]);
+        inb = res ^ 1;
+        __syncthreads();
+    }
+}
+
+}  // namespace pbg

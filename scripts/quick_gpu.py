@@ -13,7 +13,7 @@ def check(name, a, b, cfg=None, impl="port"):
     ok_ci = np.array_equal(res.c.colids, ref.colids)
     ok_v = ok_ci and np.all(np.abs(res.c.values - ref.values) <= 1e-12 * np.maximum(np.maximum(abs(res.c.values), abs(ref.values)), 1e-300))
     print(f"{name}: flop={ref.flop} nnz={ref.colids.size} rowptr={ok_rp} colids={ok_ci} vals={ok_v} "
-          f"gpu_wall={tg:.3f}s cpu={tc:.3f}s phases={ {k: round(v*1e3,3) for k,v in res.phases.items()} } bins={res.report['gpu_bins']}", flush=True)
+          f"gpu_wall={tg:.3f}s cpu={tc:.3f}s phases={ {k: round(v*1e3,3) for k,v in res.phases.items()} } bins={res.report["gpu_bins"]} fb={res.report["sort_fallbacks"]}", flush=True)
     return ok_rp and ok_ci and ok_v
 
 ok = True
