@@ -13,6 +13,7 @@
 
 #include "pbg.h"
 #include "pbg_kernels.cuh"
+#include "pbg_heavy.cuh"
 #include "pbg_sort.cuh"
 
 namespace {
@@ -84,9 +85,12 @@ enum Scalar : int {
     S_ERR,             // error bits (u32 in low word)
     S_FALLBACKS,       // bins sorted by the LSD fallback
     S_NNZ,             // nnz(C) from the distinct-count scan
+    S_HEAVY_PAD,       // padded tuples of heavy rows (scratch size)
+    S_ITEMS,           // heavy-row items after a split pass
+    S_NWORK,           // work bins
     S_COUNT
 };
-constexpr int kTickets = 8;
+constexpr int kTickets = 32;  // one u32 ticket per single-pass scan / persistent kernel
 
 }  // namespace
 
@@ -96,6 +100,11 @@ struct pbg_context {
     DevBuf colflop_off, row_flop, row_off, flags, row_bin, bin_rs, bin_cnt, bin_off, cursor,
         bin_out, chunk_p0, keys, vals, ccol, cval, rowptr, zero_block, in_a_ptr, in_a_idx,
         in_a_val, in_b_ptr, in_b_idx, in_b_val;
+    // heavy rows + work bins
+    DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
+        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
+    DevBuf items[2][8];
+    DevBuf wb[7];
     size_t zero_bytes = 0;
     cudaEvent_t ev[8] = {};
     bool ev_ok = false;
@@ -109,8 +118,13 @@ struct pbg_context {
         for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
                           &bin_off, &cursor, &bin_out, &chunk_p0, &keys, &vals, &ccol, &cval,
                           &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
-                          &in_b_idx, &in_b_val})
+                          &in_b_idx, &in_b_val, &heavy_excl, &hpad_excl, &bin_hidx, &hbin, &hoff,
+                          &hhead, &hcount, &skeys, &svals, &child_cnt, &child_pos, &hstat, &wcnt,
+                          &wpos, &wb_nnz, &wb_out})
             b->release();
+        for (auto& set : items)
+            for (auto& b : set) b.release();
+        for (auto& b : wb) b.release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
     }
@@ -189,7 +203,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     // ---- workspace ----
     const uint64_t tiles_k = (k + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
     const uint64_t tiles_m = (m + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-    const uint64_t status_words = tiles_k + 4 * tiles_m;
+    const uint64_t status_words = tiles_k + 8 * tiles_m;
     const size_t zero_bytes = (S_COUNT + kTickets) * 8 + status_words * 8;
     if ((rc = grow(ctx->zero_block, zero_bytes))) return rc;
     if ((rc = grow(ctx->colflop_off, (k + 1) * 8))) return rc;
@@ -217,6 +231,9 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     unsigned long long* stat_m2 = stat_m1 + tiles_m;
     unsigned long long* stat_m3 = stat_m2 + tiles_m;
     unsigned long long* stat_m4 = stat_m3 + tiles_m;
+    unsigned long long* stat_m5 = stat_m4 + tiles_m;
+    unsigned long long* stat_m6 = stat_m5 + tiles_m;
+    unsigned long long* stat_m7 = stat_m6 + tiles_m;
 
     auto* colflop_off = static_cast<uint64_t*>(ctx->colflop_off.p);
     auto* row_flop = static_cast<unsigned long long*>(ctx->row_flop.p);
@@ -227,7 +244,6 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     auto* bin_cnt = static_cast<uint64_t*>(ctx->bin_cnt.p);
     auto* bin_off = static_cast<uint64_t*>(ctx->bin_off.p);
     auto* cursor = static_cast<unsigned long long*>(ctx->cursor.p);
-    auto* bin_out = static_cast<uint64_t*>(ctx->bin_out.p);
     auto* rowptr = static_cast<uint64_t*>(ctx->rowptr.p);
 
     CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
@@ -284,12 +300,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     ctx->rep.heavy_bins = static_cast<uint32_t>(hs[S_HEAVY]);
     ctx->rep.bin_cap = static_cast<uint32_t>(cap);
     if (flop != hs[S_FLOP_LO]) return fail(PBG_ERR_INTERNAL, "flop scan and reduction disagree");
-    if (hs[S_HEAVY] != 0)
-        return fail(PBG_ERR_UNIMPLEMENTED,
-                    "a single output row generates " + std::to_string(hs[S_MAXBIN]) +
-                        " tuples, above the shared-memory bin capacity " + std::to_string(cap) +
-                        " (heavy-row path not built yet)");
     const uint64_t nb = hs[S_NBINS];
+    (void)nb;
     const uint64_t tcap = hs[S_TUPLE_CAP];
     ctx->rep.tuple_bytes = tcap * 12;
 
@@ -332,9 +344,122 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
-        // ---- distinct keys per bin -> output offset of every bin ----
-        uint64_t* bin_nnz = flags;  // free after k_binrows
+        // ---- work bins: regular bins + the key-range pieces of heavy rows ----
         const uint64_t* nb_dev = reinterpret_cast<const uint64_t*>(sc + S_NBINS);
+        const uint64_t H = hs[S_HEAVY];
+        if ((rc = grow(ctx->bin_hidx, (m + 1) * 4))) return rc;
+        if ((rc = grow(ctx->heavy_excl, (m + 2) * 8))) return rc;
+        if ((rc = grow(ctx->hpad_excl, (m + 2) * 8))) return rc;
+        if ((rc = grow(ctx->hbin, (H + 1) * 4))) return rc;
+        if ((rc = grow(ctx->hoff, (H + 1) * 8))) return rc;
+        if ((rc = grow(ctx->hhead, (H + 1) * 4))) return rc;
+        if ((rc = grow(ctx->hcount, (H + 1) * 4))) return rc;
+        auto* heavy_excl = static_cast<uint64_t*>(ctx->heavy_excl.p);
+        auto* hpad_excl = static_cast<uint64_t*>(ctx->hpad_excl.p);
+        auto* bin_hidx = static_cast<uint32_t*>(ctx->bin_hidx.p);
+        auto* hbin = static_cast<uint32_t*>(ctx->hbin.p);
+        auto* hoff = static_cast<uint64_t*>(ctx->hoff.p);
+        auto* hhead = static_cast<uint32_t*>(ctx->hhead.p);
+        auto* hcount = static_cast<uint32_t*>(ctx->hcount.p);
+        auto items_of = [&](int set, uint64_t cap_items, Items* it) -> int {
+            const size_t sz[8] = {8, 8, 4, 4, 4, 4, 4, 4};
+            for (int f = 0; f < 8; ++f) {
+                int r = grow(ctx->items[set][f], (cap_items + 1) * sz[f]);
+                if (r) return r;
+            }
+            it->loc = static_cast<uint64_t*>(ctx->items[set][0].p);
+            it->n = static_cast<uint64_t*>(ctx->items[set][1].p);
+            it->h = static_cast<uint32_t*>(ctx->items[set][2].p);
+            it->buf = static_cast<uint32_t*>(ctx->items[set][3].p);
+            it->sh = static_cast<uint32_t*>(ctx->items[set][4].p);
+            it->kind = static_cast<uint32_t*>(ctx->items[set][5].p);
+            it->keylo = static_cast<uint32_t*>(ctx->items[set][6].p);
+            it->keybits = static_cast<uint32_t*>(ctx->items[set][7].p);
+            return PBG_OK;
+        };
+        Items cur{};
+        int curset = 0;
+        uint64_t nitems = 0;
+        if ((rc = items_of(0, H, &cur))) return rc;
+        HeavyCtx hc{hbin, bin_off, hoff, keys, vals, nullptr, nullptr, cap};
+        if (H > 0) {
+            launch_scan(HeavyFlagIn{bin_cnt, cap}, heavy_excl, 0, nb_dev, m, stat_m5,
+                        tickets + 6, nullptr, nullptr, st);
+            launch_scan(HeavyPadIn{bin_cnt, cap}, hpad_excl, 0, nb_dev, m, stat_m6, tickets + 7,
+                        sc + S_HEAVY_PAD, nullptr, st);
+            L += 2;
+        }
+        k_heavy_init<<<blocks_for(m + 1, 256), 256, 0, st>>>(bin_cnt, nb_dev, heavy_excl,
+                                                            hpad_excl, cap, cb, hbin, hoff,
+                                                            bin_hidx, cur);
+        ++L;
+        if (H > 0) {
+            CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if ((rc = grow(ctx->skeys, hs[S_HEAVY_PAD] * 4 + 16))) return rc;
+            if ((rc = grow(ctx->svals, hs[S_HEAVY_PAD] * 8 + 16))) return rc;
+            hc.skeys = static_cast<uint32_t*>(ctx->skeys.p);
+            hc.svals = static_cast<double*>(ctx->svals.p);
+            nitems = H;
+            const int npass = (cb + HV_DBITS - 1) / HV_DBITS;
+            for (int pass = 0; pass < npass; ++pass) {
+                if ((rc = grow(ctx->child_cnt, (nitems + 1) * 8))) return rc;
+                if ((rc = grow(ctx->child_pos, (nitems + 2) * 8))) return rc;
+                const uint64_t tiles = (nitems + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+                if ((rc = grow(ctx->hstat, tiles * 8 + 64))) return rc;
+                auto* ccnt = static_cast<uint64_t*>(ctx->child_cnt.p);
+                auto* cpos = static_cast<uint64_t*>(ctx->child_pos.p);
+                auto* hst = static_cast<unsigned long long*>(ctx->hstat.p);
+                CUDA_TRY(cudaMemsetAsync(hst, 0, tiles * 8 + 64, st));
+                const unsigned g = static_cast<unsigned>(std::min<uint64_t>(nitems, 4ull * ctx->num_sms));
+                k_split_count<<<g, HV_NT, 0, st>>>(hc, cur, nitems, ccnt);
+                launch_scan(ArrayIn{ccnt}, cpos, nitems, nullptr, nitems, hst + 8,
+                            reinterpret_cast<unsigned int*>(hst), sc + S_ITEMS, nullptr, st);
+                CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaStreamSynchronize(st));
+                const uint64_t nout = hs[S_ITEMS];
+                Items nxt{};
+                if ((rc = items_of(curset ^ 1, nout, &nxt))) return rc;
+                k_split_scatter<<<g, HV_NT, 0, st>>>(hc, cur, nitems, cpos, nxt);
+                L += 3;
+                cur = nxt;
+                curset ^= 1;
+                nitems = nout;
+            }
+            CUDA_TRY(cudaMemsetAsync(hcount, 0, H * 4, st));
+            k_heavy_heads<<<blocks_for(nitems, 256), 256, 0, st>>>(cur.h, nitems, hhead, hcount);
+            ++L;
+        }
+        const uint64_t wcap = m + 1 + nitems;
+        if ((rc = grow(ctx->wcnt, (m + 1) * 8))) return rc;
+        if ((rc = grow(ctx->wpos, (m + 2) * 8))) return rc;
+        if ((rc = grow(ctx->wb_nnz, (wcap + 1) * 8))) return rc;
+        if ((rc = grow(ctx->wb_out, (wcap + 2) * 8))) return rc;
+        {
+            const size_t wsz[7] = {8, 8, 4, 4, 4, 4, 4};
+            for (int f = 0; f < 7; ++f)
+                if ((rc = grow(ctx->wb[f], (wcap + 1) * wsz[f]))) return rc;
+        }
+        WorkBins w{static_cast<uint64_t*>(ctx->wb[0].p), static_cast<uint64_t*>(ctx->wb[1].p),
+                   static_cast<uint32_t*>(ctx->wb[2].p), static_cast<uint32_t*>(ctx->wb[3].p),
+                   static_cast<uint32_t*>(ctx->wb[4].p), static_cast<uint32_t*>(ctx->wb[5].p),
+                   static_cast<uint32_t*>(ctx->wb[6].p)};
+        auto* wcnt = static_cast<uint64_t*>(ctx->wcnt.p);
+        auto* wpos = static_cast<uint64_t*>(ctx->wpos.p);
+        auto* wb_nnz = static_cast<uint64_t*>(ctx->wb_nnz.p);
+        auto* wb_out = static_cast<uint64_t*>(ctx->wb_out.p);
+        k_work_count<<<blocks_for(m + 1, 256), 256, 0, st>>>(
+            nb_dev, bin_hidx, hcount, cursor, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
+            reinterpret_cast<unsigned int*>(sc + S_ERR));
+        launch_scan(ArrayIn{wcnt}, wpos, 0, nb_dev, m, stat_m7, tickets + 8, sc + S_NWORK,
+                    nullptr, st);
+        k_work_fill<<<blocks_for(m + 1, 256), 256, 0, st>>>(nb_dev, bin_rs, bin_cnt, bin_off,
+                                                           bin_hidx, wpos, hhead, hcount, hc,
+                                                           cur, cb, w);
+        L += 3;
+        const uint64_t* nw_dev = reinterpret_cast<const uint64_t*>(sc + S_NWORK);
+
+        // ---- distinct keys per work bin -> output offset of every work bin ----
         static bool cnt_attr[64] = {};
         const size_t cnt_smem = CNT_SLOTS * 4;
         if (!cnt_attr[ctx->device & 63]) {
@@ -347,11 +472,18 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         int cnt_per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cnt_per_sm, k_bincount, CNT_NT, cnt_smem);
         k_bincount<<<static_cast<unsigned>(std::min<uint64_t>(
-                         nb, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
-                     CNT_NT, cnt_smem, st>>>(keys, bin_off, bin_cnt, nb_dev, cap, bin_nnz);
+                         wcap, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
+                     CNT_NT, cnt_smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
         ++L;
-        launch_scan(ArrayIn{bin_nnz}, bin_out, 0, nb_dev, m, stat_m4, tickets + 5,
-                    sc + S_NNZ, nullptr, st);
+        // wcap can exceed the m-sized status pool: give this scan its own words
+        {
+            const uint64_t tiles = (wcap + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+            if ((rc = grow(ctx->hstat, tiles * 8 + 64))) return rc;
+            auto* hst = static_cast<unsigned long long*>(ctx->hstat.p);
+            CUDA_TRY(cudaMemsetAsync(hst, 0, tiles * 8 + 64, st));
+            launch_scan(ArrayIn{wb_nnz}, wb_out, 0, nw_dev, wcap, hst + 8,
+                        reinterpret_cast<unsigned int*>(hst), sc + S_NNZ, nullptr, st);
+        }
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
@@ -364,29 +496,27 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             attr_set[ctx->device & 63] = true;
         }
         SortArgs sa{};
-        sa.bin_rs = bin_rs;
-        sa.bin_cnt = bin_cnt;
-        sa.bin_off = bin_off;
-        sa.cursor = cursor;
-        sa.nb_dev = nb_dev;
-        sa.bin_out = bin_out;
-        sa.bin_nnz = bin_nnz;
+        sa.w = w;
+        sa.nw_dev = nw_dev;
+        sa.wb_out = wb_out;
+        sa.wb_nnz = wb_nnz;
         sa.ticket = tickets + 4;
         sa.keys = keys;
         sa.vals = vals;
+        sa.skeys = hc.skeys ? hc.skeys : keys;
+        sa.svals = hc.svals ? hc.svals : vals;
         sa.ccol = static_cast<uint32_t*>(ctx->ccol.p);
         sa.cval = static_cast<double*>(ctx->cval.p);
         sa.rowptr = rowptr;
         sa.m = m;
         sa.col_bits = cb;
-        sa.tuples_total = sc + S_TUPLES_TOTAL;
         sa.merged_total = sc + S_MERGED_TOTAL;
         sa.err = reinterpret_cast<unsigned int*>(sc + S_ERR);
         sa.fallbacks = sc + S_FALLBACKS;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge, SM_NT, sizeof(SortSmem));
         const unsigned sm_blocks = static_cast<unsigned>(
-            std::min<uint64_t>(nb, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
+            std::min<uint64_t>(wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
         k_sortmerge<<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
@@ -400,7 +530,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ctx->rep.merged_total = hs[S_MERGED_TOTAL];
         ctx->rep.sort_fallbacks = hs[S_FALLBACKS];
         const unsigned err = static_cast<unsigned>(hs[S_ERR]);
-        if (err & 2u) return fail(PBG_ERR_UNIMPLEMENTED, "bin above shared-memory capacity");
+        if (err & 2u) return fail(PBG_ERR_INTERNAL, "a work bin exceeds the shared-memory capacity");
         if (err & 4u || hs[S_NNZ] != nnz)
             return fail(PBG_ERR_INTERNAL, "merged counts disagree with the distinct-key counts");
         if (err & 1u || hs[S_TUPLES_TOTAL] != flop)

@@ -98,6 +98,25 @@ struct ColFlopIn {
     }
 };
 
+// 1 for a bin above the shared-memory capacity (heavy row), else 0
+struct HeavyFlagIn {
+    const uint64_t* bin_cnt;
+    uint64_t cap;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        return bin_cnt[i] > cap ? 1u : 0u;
+    }
+};
+
+// padded tuple count of a heavy bin (its scratch size), 0 for other bins
+struct HeavyPadIn {
+    const uint64_t* bin_cnt;
+    uint64_t cap;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        const uint64_t n = bin_cnt[i];
+        return n > cap ? ((n + 3) & ~3ull) : 0u;
+    }
+};
+
 struct ArrayIn {
     const uint64_t* a;
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
@@ -365,81 +384,6 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
             kcur = __shfl_sync(FULL, kl, last);
             p += 32;
         }
-    }
-}
-
-// ------------------------------------------------------- bin nnz count --
-// Distinct keys per bin = the bin's merged count (its share of nnz(C)),
-// counted from the keys alone with a shared-memory hash set (load <= 1/8 for
-// a full bin, so probe chains stay short and warps rarely diverge). A scan of
-// these counts gives every bin its output offset before the sort+merge
-// kernel runs. Bins above `cap` are skipped (heavy-row path).
-constexpr int CNT_NT = 512;
-constexpr int CNT_SLOTS_LOG = 14;
-constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
-constexpr uint32_t CNT_EMPTY = 0xffffffffu;
-constexpr int CNT_PER = 8;  // keys per thread for a bin of CNT_NT*CNT_PER tuples
-
-__global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict__ keys,
-                                                   const uint64_t* __restrict__ bin_off,
-                                                   const uint64_t* __restrict__ bin_cnt,
-                                                   const uint64_t* nb_dev, uint64_t cap,
-                                                   uint64_t* bin_nnz) {
-    extern __shared__ __align__(16) uint32_t table[];  // CNT_SLOTS
-    __shared__ uint32_t s_red[2][CNT_NT / 32];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const uint64_t nb = *nb_dev;
-    for (int i = tid; i < CNT_SLOTS / 4; i += CNT_NT)
-        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
-    __syncthreads();
-    int par = 0;
-    for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const uint64_t n = bin_cnt[b];
-        if (n > cap || n > static_cast<uint64_t>(CNT_NT) * CNT_PER) {
-            if (tid == 0) bin_nnz[b] = 0;
-            continue;
-        }
-        const uint32_t* kb = keys + bin_off[b];
-        uint32_t slot[CNT_PER], kk[CNT_PER];
-        uint32_t fresh = 0;
-#pragma unroll
-        for (int j = 0; j < CNT_PER; ++j) {  // all loads in flight first
-            const uint32_t i = tid + j * CNT_NT;
-            kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
-        }
-#pragma unroll
-        for (int j = 0; j < CNT_PER; ++j) {
-            slot[j] = CNT_SLOTS;  // none
-            const uint32_t key = kk[j];
-            if (tid + j * CNT_NT < n) {
-                uint32_t h = (key * 0x9E3779B1u) >> (32 - CNT_SLOTS_LOG);
-                while (true) {
-                    const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
-                    if (old == CNT_EMPTY) {
-                        ++fresh;
-                        slot[j] = h;
-                        break;
-                    }
-                    if (old == key) break;
-                    h = (h + 1) & (CNT_SLOTS - 1);
-                }
-            }
-        }
-        fresh = warp_sum(fresh);
-        if (lane == 0) s_red[par][w] = fresh;
-        __syncthreads();
-        // reset only the slots this thread claimed: the table is clean for the
-        // next bin without a full clear
-#pragma unroll
-        for (int j = 0; j < CNT_PER; ++j)
-            if (slot[j] < CNT_SLOTS) table[slot[j]] = CNT_EMPTY;
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int i = 0; i < CNT_NT / 32; ++i) t += s_red[par][i];
-            bin_nnz[b] = t;
-        }
-        par ^= 1;
-        __syncthreads();
     }
 }
 

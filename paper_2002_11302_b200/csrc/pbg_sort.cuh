@@ -5,8 +5,10 @@
 // compress_bin_records (two-pointer merge, pb_spgemm.hpp:202-216) and
 // convert_csr (pb_spgemm.cpp:288-328).
 //
-// Persistent CTAs take bins in ticket order. A bin holds <= SM_CAP tuples
-// (u32 key = local_row << col_bits | col, f64 value). Per bin:
+// Persistent CTAs take work bins (a GPU bin, or one key range of a heavy
+// row, pbg_heavy.cuh) in ticket order. A work bin holds <= SM_CAP tuples
+// (u32 key = local_row << col_bits | col, f64 value) with keys in
+// [keylo, keylo + 2^keybits). Per work bin:
 //   0. the bin arrives in shared memory by two TMA bulk copies
 //      (cp.async.bulk, mbarrier completion) issued while the CTA was still
 //      busy with the previous bin;
@@ -30,6 +32,7 @@
 #include <cstdint>
 
 #include "pbg_device.cuh"
+#include "pbg_heavy.cuh"
 
 namespace pbg {
 
@@ -53,25 +56,22 @@ static_assert(SM_ITEMS == 8, "one uint4 of u16 counters per thread");
 static_assert(SM_NB * 2 / 16 == SM_NT, "counter scan layout");
 
 struct SortArgs {
-    const uint32_t* bin_rs;
-    const uint64_t* bin_cnt;
-    const uint64_t* bin_off;
-    const unsigned long long* cursor;
-    const uint64_t* nb_dev;
-    const uint64_t* bin_out;  // output offset of every bin (scan of k_bincount)
-    const uint64_t* bin_nnz;  // distinct keys per bin (k_bincount), cross-checked
+    WorkBins w;
+    const uint64_t* nw_dev;   // number of work bins
+    const uint64_t* wb_out;   // output offset of every work bin (scan of k_bincount)
+    const uint64_t* wb_nnz;   // distinct keys per work bin (k_bincount), cross-checked
     unsigned int* ticket;
-    const uint32_t* keys;  // tuples
+    const uint32_t* keys;     // tuples (main buffer)
     const double* vals;
-    uint32_t* ccol;        // C colids
-    double* cval;          // C values
+    const uint32_t* skeys;    // tuples (heavy-row scratch buffer)
+    const double* svals;
+    uint32_t* ccol;           // C colids
+    double* cval;             // C values
     uint64_t* rowptr;
     uint64_t m;
     int col_bits;
-    unsigned long long* tuples_total;
     unsigned long long* merged_total;
-    unsigned int* err;  // bit0 conservation, bit1 heavy bin reached the smem path,
-                        // bit2 merged count != k_bincount's distinct count
+    unsigned int* err;  // bit1 work bin above capacity, bit2 merged != distinct count
     unsigned long long* fallbacks;
 };
 
@@ -116,23 +116,32 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
         : "memory");
 }
 
-// Thread 0: take the next ticket and, for a bin that fits, start its copy
-// into buffer `buf` (generic-proxy accesses to it are finished: caller syncs).
+// Thread 0: take the next ticket and, for a work bin that fits, start its
+// copy into buffer `buf` (generic-proxy accesses to it are finished: caller
+// syncs). s_loaded: 1 = TMA copy in flight, 2 = load by hand (unaligned heavy
+// sub-bin), 0 = nothing to load (empty / uniform / error).
 __device__ __forceinline__ void prefetch_next(const SortArgs& a, SortSmem& sm, int buf,
-                                              uint64_t nb) {
+                                              uint64_t nw) {
     const uint64_t b = atomicAdd(a.ticket, 1u);
     sm.s_next = b;
     sm.s_loaded = 0;
-    if (b < nb) {
-        const uint64_t n = a.bin_cnt[b];
-        if (n > 0 && n <= SM_CAP) {
-            const uint64_t off = a.bin_off[b];
+    if (b < nw) {
+        const uint64_t n = a.w.n[b];
+        const uint32_t fl = a.w.flags[b];
+        if (n > 0 && n <= SM_CAP && !(fl & 2u)) {
+            const uint64_t off = a.w.off[b];
+            if (off & 3u) {
+                sm.s_loaded = 2;
+                return;
+            }
+            const uint32_t* ks = (fl & 1u) ? a.skeys : a.keys;
+            const double* vs = (fl & 1u) ? a.svals : a.vals;
             const uint32_t kb = static_cast<uint32_t>((n * 4 + 15) & ~15ull);
             const uint32_t vb = static_cast<uint32_t>((n * 8 + 15) & ~15ull);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.mbar, kb + vb);
-            bulk_g2s(sm.k[buf], a.keys + off, kb, &sm.mbar);
-            bulk_g2s(sm.v[buf], a.vals + off, vb, &sm.mbar);
+            bulk_g2s(sm.k[buf], ks + off, kb, &sm.mbar);
+            bulk_g2s(sm.v[buf], vs + off, vb, &sm.mbar);
             sm.s_loaded = 1;
         }
     }
@@ -169,7 +178,7 @@ __device__ __forceinline__ void scan_cnt(SortSmem& sm) {
 // 8-bit digits, ping-ponging with buffer `y`. Ranks from match.any per warp in
 // element order, per-(warp, digit) counters cnt[w*256+d] scanned digit-major.
 // Returns the buffer holding the result.
-__device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits) {
+__device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits, uint32_t keylo) {
     static_assert(SM_NW * 256 <= SM_NB, "LSD counters fit the bucket counters");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
@@ -190,7 +199,7 @@ __device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits) {
         for (int it = 0; it < SM_ITEMS; ++it) {
             const uint32_t idx = w * SM_PER_WARP + it * 32 + lane;
             const bool valid = idx < n;
-            const uint32_t d = valid ? ((kr[it] >> shift) & 0xffu) : 0x100u;
+            const uint32_t d = valid ? (((kr[it] - keylo) >> shift) & 0xffu) : 0x100u;
             const uint32_t peers = __match_any_sync(FULL, d);
             const uint16_t old = valid ? wc[d] : 0;
             rank[it] = old + __popc(peers & lt);
@@ -281,13 +290,13 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
 // Sort + merge the bin in buffer `in` using scratch buffer `scr`. Returns the
 // merged count; *res gets the buffer holding the merged output.
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
-                                   int bits, int* res) {
+                                   int bits, uint32_t keylo, int* res) {
     const int tid = threadIdx.x;
     uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);
     const int sh = bits > SM_NB_BITS ? bits - SM_NB_BITS : 0;
     // ---- 1. bucket histogram / scan / scatter in -> scr ----
     for (uint32_t i = tid; i < n; i += SM_NT) {
-        const uint32_t d = sm.k[in][i] >> sh;
+        const uint32_t d = (sm.k[in][i] - keylo) >> sh;
         atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
     }
     __syncthreads();
@@ -295,7 +304,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     __syncthreads();
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[in][i];
-        const uint32_t d = key >> sh;
+        const uint32_t d = (key - keylo) >> sh;
         const uint32_t old = atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
         const uint32_t pos = (old >> ((d & 1) * 16)) & 0xffffu;
         sm.k[scr][pos] = key;
@@ -306,7 +315,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     bool big = false;
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[scr][i];
-        const uint32_t d = key >> sh;
+        const uint32_t d = (key - keylo) >> sh;
         const uint32_t lo = d ? sm.cnt[d - 1] : 0u, hi = sm.cnt[d];
         if (hi - lo > SM_BMAX) {
             big = true;
@@ -325,7 +334,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     int sorted, other;
     if (any_big) {
         // clustered keys: stable LSD radix on scr (a permutation of the bin)
-        sorted = lsd_sort(sm, scr, in, n, bits);
+        sorted = lsd_sort(sm, scr, in, n, bits, keylo);
         other = sorted == scr ? in : scr;
         if (tid == 0) atomicAdd(a.fallbacks, 1ull);
     } else {
@@ -343,9 +352,9 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     return n;
 }
 
-// Write a resolved bin: colids / values at P, rowptr of its rows.
+// Write a work bin: colids / values at P, rowptr of the rows it starts.
 __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm, int buf,
-                                          uint64_t b, uint64_t nb, uint32_t rs, uint32_t re,
+                                          uint64_t b, uint64_t nw, uint32_t rs, uint32_t span,
                                           uint32_t U, uint64_t P) {
     const int tid = threadIdx.x;
     const int cb = a.col_bits;
@@ -359,7 +368,6 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
         __stcs(ovals + u, V[u]);
     }
     // rowptr[rs + r] = P + first merged entry of local row r (binary search)
-    const uint32_t span = re - rs;
     for (uint32_t r = tid; r < span; r += SM_NT) {
         const uint64_t target = static_cast<uint64_t>(r) << cb;
         uint32_t lo = 0, hi = U;
@@ -370,54 +378,88 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
         }
         a.rowptr[rs + r] = P + lo;
     }
-    if (tid == 0 && b == nb - 1) a.rowptr[a.m] = P + U;
+    if (tid == 0 && b == nw - 1) a.rowptr[a.m] = P + U;
+}
+
+// A uniform-key item (one column hit more than SM_CAP times in a heavy row):
+// its merged entry is the sum of all its values, reduced from global memory
+// in index order per thread, then across the block.
+__device__ __forceinline__ void reduce_uniform(const SortArgs& a, SortSmem& sm, uint64_t b,
+                                               int buf) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t fl = a.w.flags[b];
+    const uint64_t off = a.w.off[b], n = a.w.n[b];
+    const double* vs = ((fl & 1u) ? a.svals : a.vals) + off;
+    double s = 0.0;
+    for (uint64_t i = tid; i < n; i += SM_NT) s += vs[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    double* red = sm.v[buf] + 8;  // scratch words in the free buffer
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int i = 0; i < SM_NW; ++i) t += red[i];
+        sm.k[buf][0] = ((fl & 1u) ? a.skeys : a.keys)[off];
+        sm.v[buf][0] = t;
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(SM_NT, 4) k_sortmerge(SortArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x;
-    const uint64_t nb = *a.nb_dev;
+    const uint64_t nw = *a.nw_dev;
 
     if (tid == 0) {
         mbar_init(&sm.mbar, 1);
-        prefetch_next(a, sm, 0, nb);
+        prefetch_next(a, sm, 0, nw);
     }
     __syncthreads();
     uint32_t parity = 0;
-    int inb = 0;  // buffer the current bin was copied into
+    int inb = 0;  // buffer the current work bin is copied into
 
     while (true) {
         const uint64_t b = sm.s_next;
-        if (b >= nb) break;
-        const bool loaded = sm.s_loaded != 0;
-        const uint32_t rs = a.bin_rs[b], re = a.bin_rs[b + 1];
-        const uint64_t n64 = a.bin_cnt[b];
-        if (tid == 0) {
-            const uint64_t cur = a.cursor[b];
-            if (cur != n64) atomicOr(a.err, 1u);
-            atomicAdd(a.tuples_total, (unsigned long long)cur);
-            if (n64 > SM_CAP) atomicOr(a.err, 2u);
-        }
+        if (b >= nw) break;
+        const uint32_t loaded = sm.s_loaded;
+        const uint64_t n64 = a.w.n[b];
+        const uint32_t fl = a.w.flags[b];
+        const uint32_t rs = a.w.rs[b], span = a.w.span[b];
+        if (tid == 0 && n64 > SM_CAP && !(fl & 2u)) atomicOr(a.err, 2u);
         int res = inb;
         uint32_t U = 0;
         if (loaded) {
+            const uint32_t n = static_cast<uint32_t>(n64);
             reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
-            const uint32_t span = re - rs;
-            const int bits = (span > 1 ? 32 - __clz(span - 1) : 0) + a.col_bits;
-            mbar_wait(&sm.mbar, parity);
-            parity ^= 1;
+            if (loaded == 1) {
+                mbar_wait(&sm.mbar, parity);
+                parity ^= 1;
+            } else {  // unaligned heavy sub-bin: plain coalesced loads
+                const uint64_t off = a.w.off[b];
+                const uint32_t* ks = ((fl & 1u) ? a.skeys : a.keys) + off;
+                const double* vs = ((fl & 1u) ? a.svals : a.vals) + off;
+                for (uint32_t i = tid; i < n; i += SM_NT) {
+                    sm.k[inb][i] = ks[i];
+                    sm.v[inb][i] = vs[i];
+                }
+            }
             __syncthreads();
-            U = sort_merge_bin(a, sm, inb, inb ^ 1, static_cast<uint32_t>(n64), bits, &res);
+            U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(a.w.keybits[b]),
+                               a.w.keylo[b], &res);
+        } else if (fl & 2u) {
+            reduce_uniform(a, sm, b, inb);
+            U = 1;
         }
         __syncthreads();
-        // next bin's copy into the free buffer overlaps this bin's output
+        // next work bin's copy into the free buffer overlaps this one's output
         if (tid == 0) {
-            prefetch_next(a, sm, res ^ 1, nb);
-            if (loaded && U != a.bin_nnz[b]) atomicOr(a.err, 4u);
+            prefetch_next(a, sm, res ^ 1, nw);
+            if (U != a.wb_nnz[b]) atomicOr(a.err, 4u);
             atomicAdd(a.merged_total, (unsigned long long)U);
         }
-        write_bin(a, sm, res, b, nb, rs, re, U, a.bin_out[b]);
+        write_bin(a, sm, res, b, nw, rs, span, U, a.wb_out[b]);
         inb = res ^ 1;
         __syncthreads();
     }

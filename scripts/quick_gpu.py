@@ -22,6 +22,15 @@ for scale, d in [(4, 2), (8, 3), (12, 4)]:
 for bc in (256, 1024):
     csr = M.make_matrix("er", 10, 6, 2); ok &= check(f"er10 cap{bc}", M.csr_to_csc(csr), csr, api.PbConfig(bin_cap=bc))
 csr = M.make_matrix("rmat", 10, 4, 7); ok &= check("rmat10", M.csr_to_csc(csr), csr)
+for sc in (13, 15):
+    csr = M.make_matrix("rmat", sc, 16, 7); ok &= check(f"rmat{sc} (heavy rows)", M.csr_to_csc(csr), csr)
+csr = M.make_matrix("er", 11, 8, 3); ok &= check("er11 cap64 (many heavy)", M.csr_to_csc(csr), csr, api.PbConfig(bin_cap=64))
+import numpy as np
+K, n = 6000, 512
+a = M.coo_to_csr(4, K, np.r_[np.zeros(K, int), [1, 2]], np.r_[np.arange(K), [0, 1]], np.r_[np.linspace(0.5, 1.5, K), [2.0, 3.0]])
+rows = np.r_[np.arange(K), np.arange(K)]; cols = np.r_[np.zeros(K, int), np.arange(K) % 100 + 1]
+b = M.coo_to_csr(K, n, rows, cols, np.linspace(1.0, 2.0, 2 * K))
+ok &= check("uniform-key column", M.csr_to_csc(a), b)
 a, b = M.make_config("C1"); ok &= check("C1", a, b)
 s = M.stencil27(16); ok &= check("stencil16", M.csr_to_csc(s), s)
 if "--big" in sys.argv:

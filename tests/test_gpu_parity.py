@@ -1,0 +1,279 @@
+"""GPU parity: the sm_100a path, called through the C-ABI, against the
+reference (golden fixtures and oracle/_ref) and the C restatement.
+
+Bar (BASELINE.json north_star): rowptr / colids bit-exact, fp64 values within
+1e-12 relative. Full-size configs that the CPU cannot multiply in seconds are
+checked through size-independent properties (conservation, linearity, known
+nnz, exact integer values) and band parity (rows of a band vs the oracle's
+product of that band).
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2002_11302_b200 import api, bands, matrices as M
+
+from helpers import (RTOL, assert_csr_matches, assert_valid_csr, assert_values_close,
+                     golden_cases)
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def gpu(a, b, **kw):
+    return api.pb_multiply(a, b, api.PbConfig(device=0, **kw))
+
+
+def check_vs(res, ref):
+    assert_csr_matches(res.c.rowptr, res.c.colids, res.c.values, ref.rowptr, ref.colids,
+                       ref.values)
+    assert res.tuples_into_sort == ref.flop
+    assert res.merged_total == ref.colids.size
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c[0]["name"])
+def test_golden_reference_fixtures(case):
+    meta, a, b, exp = case
+    res = gpu(a, b, nbins=meta["nbins"], balanced_bins=meta["balanced"],
+              l2_bytes=meta["l2_bytes"])
+    assert_csr_matches(res.c.rowptr, res.c.colids, res.c.values, exp["c_rowptr"],
+                       exp["c_colids"], exp["c_values"])
+    assert res.sym.flop == meta["flop"]
+    assert res.sym.nbins == meta["ref_nbins"]
+    assert np.array_equal(res.sym.per_column_flop, exp["per_column_flop"])
+    assert np.array_equal(res.sym.per_bin_flop, exp["per_bin_flop"])
+    assert np.array_equal(res.sym.bin_row_starts, exp["bin_row_starts"])
+    assert res.tuples_into_sort == meta["flop"]          # acceptance criterion 6
+    assert res.merged_total == meta["nnz_c"] == res.c.nnz
+
+
+def test_known_answers():
+    d2 = M.coo_to_csr(2, 2, [0, 0, 1, 1], [0, 1, 0, 1], [1.0, 2.0, 3.0, 4.0])
+    r = gpu(M.csr_to_csc(d2), d2)
+    assert list(r.c.values) == [7.0, 10.0, 15.0, 22.0] and r.sym.flop == 8
+    # cancellation keeps an exact zero as a structural nonzero
+    a = M.coo_to_csr(2, 2, [0, 0], [0, 1], [1.0, -1.0])
+    b = M.coo_to_csr(2, 2, [0, 1], [1, 1], [1.0, 1.0])
+    z = gpu(M.csr_to_csc(a), b)
+    assert z.c.nnz == 1 and z.c.values[0] == 0.0
+    # empty product
+    e = M.coo_to_csr(16, 16, [], [])
+    r = gpu(M.csr_to_csc(e), e)
+    assert r.c.nnz == 0 and r.sym.flop == 0 and np.all(r.c.rowptr == 0)
+
+
+def test_identity_times_a():
+    csr = M.make_matrix("rmat", 7, 5, seed=3)
+    eye = M.coo_to_csr(csr.nrows, csr.nrows, np.arange(csr.nrows), np.arange(csr.nrows))
+    r = gpu(M.csr_to_csc(eye), csr)
+    assert_csr_matches(r.c.rowptr, r.c.colids, r.c.values, csr.rowptr, csr.colids, csr.values,
+                       rtol=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_sweep_vs_oracle(seed):
+    """acceptance.cpp:62-115 shape: random ER/RMAT pairs, scales 4..10."""
+    rng = np.random.default_rng(1000 + seed)
+    scale = int(rng.integers(4, 11))
+    mats = []
+    for k in range(2):
+        kind = "er" if rng.integers(2) else "rmat"
+        ef = int(min(rng.integers(2, 17), 1 << scale))
+        mats.append(M.make_matrix(kind, scale, ef, seed=seed * 13 + k))
+    a, b = M.csr_to_csc(mats[0]), mats[1]
+    cap = [0, 2048, 1024, 512][seed % 4]
+    res = gpu(a, b, bin_cap=cap)
+    ref = oracle.multiply(a, b)
+    check_vs(res, ref)
+    assert_valid_csr(res.c)
+
+
+def test_rectangular():
+    r, c = M.gen_er(9, 4, 5)
+    a = M.coo_to_csr(512, 512, r, c)
+    a = M.CsrMatrix(300, 512, a.rowptr[:301].copy(), a.colids[:int(a.rowptr[300])].copy(),
+                    np.linspace(0.5, 1.5, int(a.rowptr[300])))
+    r2, c2 = M.gen_er(9, 3, 6)
+    b = M.coo_to_csr(512, 512, r2, c2, np.ones(r2.size))
+    b = M.CsrMatrix(512, 200, *_cols_below(b, 200))
+    res = gpu(M.csr_to_csc(a), b)
+    check_vs(res, oracle.multiply(M.csr_to_csc(a), b))
+
+
+def _cols_below(m, ncols):
+    keep = m.colids < ncols
+    rows = np.repeat(np.arange(m.nrows), np.diff(m.rowptr).astype(np.int64))[keep]
+    out = M.coo_to_csr(m.nrows, ncols, rows, m.colids[keep], m.values[keep])
+    return out.rowptr, out.colids, out.values
+
+
+def test_configuration_invariance():
+    """acceptance.cpp:197-226: identical pattern across nbins / lbin_bytes /
+    GPU bin capacity; values within tolerance."""
+    a = M.make_matrix("er", 12, 4, seed=99)
+    b = M.make_matrix("er", 12, 4, seed=100)
+    ac = M.csr_to_csc(a)
+    base = gpu(ac, b)
+    for nbins in (0, 1, 16, 1024):
+        for lbin in (16, 512, 4096):
+            for cap in (0, 512, 1536):
+                r = gpu(ac, b, nbins=nbins, lbin_bytes=lbin, bin_cap=cap)
+                assert_csr_matches(r.c.rowptr, r.c.colids, r.c.values, base.c.rowptr,
+                                   base.c.colids, base.c.values, rtol=1e-10)
+
+
+def test_value_sum_conservation():
+    """test_pb_spgemm.cpp:315-335 as linearity: sum(C) = sum_k colsum_A(k) * rowsum_B(k)."""
+    a = M.make_matrix("rmat", 10, 8, seed=81)
+    b = M.make_matrix("rmat", 10, 8, seed=82)
+    ac = M.csr_to_csc(a)
+    r = gpu(ac, b)
+    colsum = np.add.reduceat(ac.values, ac.colptr[:-1].astype(np.int64)) * (np.diff(ac.colptr) > 0)
+    rowsum = np.add.reduceat(b.values, b.rowptr[:-1].astype(np.int64)) * (np.diff(b.rowptr) > 0)
+    assert abs(r.c.values.sum() - float(colsum @ rowsum)) <= 1e-9 * abs(float(colsum @ rowsum))
+
+
+def test_row_bands_assemble_to_full_product():
+    """The multi-GPU partitioning on one GPU: bands multiplied separately and
+    concatenated equal the single product."""
+    csr = M.make_matrix("er", 14, 8, seed=12)
+    csc = M.csr_to_csc(csr)
+    full = gpu(csc, csr)
+    cuts = bands.plan_bands(csc, csr, 5)
+    parts = [gpu(bands.band_slab(csc, cuts, r), csr).c for r in range(5)]
+    asm = bands.assemble(parts, cuts, csr.ncols)
+    assert_csr_matches(asm.rowptr, asm.colids, asm.values, full.c.rowptr, full.c.colids,
+                       full.c.values)
+
+
+def test_device_path_matches_host_path():
+    import torch
+    csr = M.make_matrix("er", 13, 6, seed=21)
+    csc = M.csr_to_csc(csr)
+    host = gpu(csc, csr)
+    dev = torch.device("cuda", 0)
+    t = lambda x, dt: torch.from_numpy(x.view(dt)).to(dev)  # noqa: E731
+    A = (t(csc.colptr, np.int64), t(csc.rowids, np.int32), t(csc.values, np.float64))
+    B = (t(csr.rowptr, np.int64), t(csr.colids, np.int32), t(csr.values, np.float64))
+    ctx = api.DeviceContext(0)
+    for _ in range(2):  # reuse of the grow-only workspace
+        nnz, rep = ctx.multiply(ctx.view(csc.nrows, csc.ncols, *A),
+                                ctx.view(csr.nrows, csr.ncols, *B), api.PbConfig(device=0))
+    assert nnz == host.c.nnz and rep["flop"] == host.sym.flop
+    assert ctx.launches() > 0
+    import ctypes
+    rp, ci, va = ctx.result_pointers()
+    got_rp = torch.empty(csc.nrows + 1, dtype=torch.int64, device=dev)
+    got_ci = torch.empty(nnz, dtype=torch.int32, device=dev)
+    got_va = torch.empty(nnz, dtype=torch.float64, device=dev)
+    cudart = ctypes.CDLL("libcudart.so.12")
+    for dst, src, nbytes in ((got_rp, rp, (csc.nrows + 1) * 8), (got_ci, ci, nnz * 4),
+                             (got_va, va, nnz * 8)):
+        assert cudart.cudaMemcpy(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src),
+                                 ctypes.c_size_t(nbytes), 3) == 0
+    assert_csr_matches(got_rp.cpu().numpy().view(np.uint64), got_ci.cpu().numpy().view(np.uint32),
+                       got_va.cpu().numpy(), host.c.rowptr, host.c.colids, host.c.values)
+
+
+def test_parameter_errors_on_gpu():
+    a = M.make_matrix("er", 6, 3, seed=1)
+    ac = M.csr_to_csc(a)
+    with pytest.raises(api.ParameterError):
+        gpu(ac, a, nbins=6)
+    with pytest.raises(api.ParameterError):
+        gpu(ac, a, lbin_bytes=0)
+    bad = M.CsrMatrix(32, 64, np.zeros(33, np.uint64), np.zeros(0, np.uint32), np.zeros(0))
+    with pytest.raises(api.ParameterError):
+        gpu(ac, bad)
+
+
+# ---------------------------------------------------------------- configs --
+def test_config_C1_vs_oracle():
+    a, b = M.make_config("C1")
+    res = gpu(a, b)
+    ref = oracle.multiply(a, b)
+    check_vs(res, ref)
+    cf = ref.flop / ref.colids.size
+    assert 1.0 <= cf <= 1.05  # acceptance criterion 4 (ER squared: cf in [1, 1.05])
+
+
+@pytest.mark.slow
+def test_config_C2_vs_reference():
+    a, b = M.make_config("C2")
+    res = gpu(a, b)
+    impl = "reference" if oracle.ref_available() else "port"
+    ref = oracle.multiply(a, b, impl=impl, nthreads=0, stepwise=False)
+    assert res.sym.flop == 268435456
+    check_vs(res, ref)
+
+
+def _band_parity(a, b, res, nbands=3, rows=4096):
+    """Rows of a few bands of the GPU product vs the oracle's band products
+    (SURVEY.md §8c band parity)."""
+    rng = np.random.default_rng(5)
+    starts = sorted(rng.choice(a.nrows - rows, size=nbands, replace=False))
+    for r0 in list(starts) + [a.nrows - rows]:
+        slab = M.row_band(a, int(r0), int(r0) + rows)
+        ref = oracle.multiply(slab, b, impl="reference" if oracle.ref_available() else "port",
+                              nthreads=0 if oracle.ref_available() else 1)
+        lo, hi = int(res.c.rowptr[r0]), int(res.c.rowptr[r0 + rows])
+        assert np.array_equal(res.c.rowptr[r0:r0 + rows + 1] - res.c.rowptr[r0], ref.rowptr)
+        assert np.array_equal(res.c.colids[lo:hi], ref.colids)
+        assert_values_close(res.c.values[lo:hi], ref.values)
+
+
+@pytest.mark.slow
+def test_config_C4_stencil_properties_and_bands():
+    a, b = M.make_config("C4")
+    res = gpu(a, b)
+    assert res.sym.flop == 1489355288 and res.c.nnz == 254840104
+    assert res.tuples_into_sort == res.sym.flop and res.merged_total == res.c.nnz
+    assert_valid_csr(res.c)
+    # interior row of (27-pt)^2: 125 entries, diagonal 26*26 + 26*1 = 702, exact
+    n = 128
+    i = (64 * n + 64) * n + 64
+    lo, hi = int(res.c.rowptr[i]), int(res.c.rowptr[i + 1])
+    assert hi - lo == 125
+    assert res.c.values[lo + int(np.searchsorted(res.c.colids[lo:hi], i))] == 702.0
+    assert np.all(res.c.values == np.round(res.c.values))  # integer arithmetic stays exact
+    _band_parity(a, b, res, rows=2048)
+
+
+@pytest.mark.slow
+def test_config_C5a_properties_and_bands():
+    a, b = M.make_config("C5a")
+    res = gpu(a, b)
+    assert res.sym.flop == 1073741824 and res.c.nnz == 1073740073
+    assert res.tuples_into_sort == res.sym.flop and res.merged_total == res.c.nnz
+    rp = res.c.rowptr
+    assert rp[0] == 0 and rp[-1] == res.c.nnz and np.all(rp[1:] >= rp[:-1])
+    _band_parity(a, b, res, rows=8192)
+
+
+def test_small_rmat_vs_oracle():
+    for scale in (10, 11, 12):
+        csr = M.make_matrix("rmat", scale, 8, seed=scale)
+        a = M.csr_to_csc(csr)
+        res = gpu(a, csr)
+        check_vs(res, oracle.multiply(a, csr))
+
+
+def test_cpp_dropin_on_gpu(tmp_path):
+    import subprocess
+    from paper_2002_11302_b200 import build
+    shim = build.build_shim()
+    exe = tmp_path / "dropin_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "cpp" / "dropin_test.cpp"), "-L", str(shim.parent),
+                    "-lspgemm_b200", f"-Wl,-rpath,{shim.parent}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_smoke_entry():
+    import sys
+    sys.path.insert(0, str(ROOT))
+    import __graft_entry__
+    __graft_entry__.smoke()
