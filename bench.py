@@ -56,22 +56,27 @@ def model_bytes(nnz_a, nnz_b, flop, nnz_c, b=16.0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled around the timed region
+    (B200_PROFILING.md clocks line). Started before warm-up so the first
+    sample exists when timing begins; rows are time-stamped and the ones
+    inside [start, stop] (plus the nearest on each side) are summarised."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self.proc = None
         self.thread = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -79,11 +84,23 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
 
+    def wait_first(self, timeout=5.0):
+        t = time.time()
+        while self.proc and not self.rows and time.time() - t < timeout:
+            time.sleep(0.02)
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
+        time.sleep(0.12)  # one more sample after the region
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
-                self.rows.append(parts)
+                self.rows.append((time.time(), parts))
 
     def stop(self):
         if self.proc:
@@ -94,16 +111,30 @@ class ClockSampler:
                 self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
-        if not self.rows:
+        rows = self.rows
+        if self.t0 is not None and self.t1 is not None and rows:
+            inside = [r for r in rows if self.t0 <= r[0] <= self.t1]
+            before = [r for r in rows if r[0] < self.t0][-1:]
+            after = [r for r in rows if r[0] > self.t1][:1]
+            rows = before + inside + after
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[3 + i].lower() == "active"})
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[1][0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1][1]) for r in rows) if v is not None]
+        pw = [v for v in (num(r[1][2]) for r in rows) if v is not None]
+        reasons = sorted({self.NAMES[i] for _, r in rows for i in range(4)
+                          if r[3 + i].strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "reasons": reasons,
+                "samples": len(rows),
+                "window_s": (self.t1 - self.t0) if self.t0 and self.t1 else None}
 
 
 def dist_env():
@@ -232,15 +263,14 @@ def run_gpu_arm(args):
     cfg = api.PbConfig(device=local)
     stream = torch.cuda.current_stream(dev)
 
-    reps = []
-    for _ in range(args.warmup):
-        reps.append(ctx.multiply(va, vb, cfg, stream.cuda_stream)[1])
-    flop_local = reps[-1]["flop"] if reps else 0
-    nnz_local = reps[-1]["nnz_c"] if reps else 0
-
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
+    for _ in range(args.warmup):
+        ctx.multiply(va, vb, cfg, stream.cuda_stream)
+    if sampler:
+        sampler.wait_first()
+        sampler.mark_start()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -255,6 +285,8 @@ def run_gpu_arm(args):
         step_reps.append(rep)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark_stop()
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None

@@ -130,8 +130,10 @@ def test_value_sum_conservation():
     b = M.make_matrix("rmat", 10, 8, seed=82)
     ac = M.csr_to_csc(a)
     r = gpu(ac, b)
-    colsum = np.add.reduceat(ac.values, ac.colptr[:-1].astype(np.int64)) * (np.diff(ac.colptr) > 0)
-    rowsum = np.add.reduceat(b.values, b.rowptr[:-1].astype(np.int64)) * (np.diff(b.rowptr) > 0)
+    colsum = np.bincount(np.repeat(np.arange(ac.ncols), np.diff(ac.colptr).astype(np.int64)),
+                         weights=ac.values, minlength=ac.ncols)
+    rowsum = np.bincount(np.repeat(np.arange(b.nrows), np.diff(b.rowptr).astype(np.int64)),
+                         weights=b.values, minlength=b.nrows)
     assert abs(r.c.values.sum() - float(colsum @ rowsum)) <= 1e-9 * abs(float(colsum @ rowsum))
 
 
@@ -252,12 +254,32 @@ def test_config_C5a_properties_and_bands():
     _band_parity(a, b, res, rows=8192)
 
 
-def test_small_rmat_vs_oracle():
-    for scale in (10, 11, 12):
+def test_rmat_heavy_rows_vs_oracle():
+    """RMAT rows above the shared-memory capacity take the heavy-row split
+    path (and uniform-key reduction for columns hit > capacity times)."""
+    for scale in (10, 12, 14):
         csr = M.make_matrix("rmat", scale, 8, seed=scale)
         a = M.csr_to_csc(csr)
         res = gpu(a, csr)
         check_vs(res, oracle.multiply(a, csr))
+
+
+def test_uniform_key_reduction():
+    """One output entry receiving more tuples than a bin holds (6000 > 2048)."""
+    K, n = 6000, 512
+    a = M.coo_to_csr(4, K, np.r_[np.zeros(K, int), [1, 2]], np.r_[np.arange(K), [0, 1]],
+                     np.r_[np.linspace(0.5, 1.5, K), [2.0, 3.0]])
+    rows = np.r_[np.arange(K), np.arange(K)]
+    cols = np.r_[np.zeros(K, int), np.arange(K) % 100 + 1]
+    b = M.coo_to_csr(K, n, rows, cols, np.linspace(1.0, 2.0, 2 * K))
+    ac = M.csr_to_csc(a)
+    check_vs(gpu(ac, b), oracle.multiply(ac, b))
+
+
+def test_tiny_bin_capacity_forces_heavy_split():
+    csr = M.make_matrix("er", 11, 8, seed=3)
+    a = M.csr_to_csc(csr)
+    check_vs(gpu(a, csr, bin_cap=64), oracle.multiply(a, csr))
 
 
 def test_cpp_dropin_on_gpu(tmp_path):
