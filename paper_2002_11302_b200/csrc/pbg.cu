@@ -104,6 +104,7 @@ struct pbg_context {
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
         child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
     DevBuf items[2][8];
+    DevBuf run_dst, run_src, run_len, run_rp;
     DevBuf wb[7];
     size_t zero_bytes = 0;
     cudaEvent_t ev[8] = {};
@@ -125,6 +126,7 @@ struct pbg_context {
         for (auto& set : items)
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
+        for (DevBuf* b : {&run_dst, &run_src, &run_len, &run_rp}) b->release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
     }
@@ -340,8 +342,25 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         ExpandArgs ea{A.ptr, A.idx,  A.val,   B.ptr,   B.idx, B.val, k,   chunk_p0, nchunks,
                       row_bin, bin_rs, bin_off, cursor, keys, vals, cb};
-        k_expand<<<exp_blocks, EXP_NT, 0, st>>>(ea);
-        ++L;
+#ifndef PBG_EXP_SPLIT
+#define PBG_EXP_SPLIT 0
+#endif
+        if (PBG_EXP_SPLIT) {
+            if ((rc = grow(ctx->run_dst, (nnz_a + 1) * 8))) return rc;
+            if ((rc = grow(ctx->run_src, (nnz_a + 1) * 8))) return rc;
+            if ((rc = grow(ctx->run_len, (nnz_a + 1) * 4))) return rc;
+            if ((rc = grow(ctx->run_rp, (nnz_a + 1) * 4))) return rc;
+            ea.run_dst = static_cast<uint64_t*>(ctx->run_dst.p);
+            ea.run_src = static_cast<uint64_t*>(ctx->run_src.p);
+            ea.run_len = static_cast<uint32_t*>(ctx->run_len.p);
+            ea.run_rp = static_cast<uint32_t*>(ctx->run_rp.p);
+            k_runs<<<blocks_for(k, 256), 256, 0, st>>>(ea);
+            k_expand_runs<<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            L += 2;
+        } else {
+            k_expand<<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            ++L;
+        }
         CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
         // ---- work bins: regular bins + the key-range pieces of heavy rows ----

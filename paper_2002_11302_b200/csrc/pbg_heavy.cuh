@@ -342,10 +342,31 @@ __global__ void k_work_fill(const uint64_t* nb_dev, const uint32_t* __restrict__
 // these counts gives every work bin its output offset before the sort+merge
 // kernel runs, so bins never wait on each other. Uniform-key items count 1.
 constexpr int CNT_NT = 512;
-constexpr int CNT_SLOTS_LOG = 14;
+#ifndef PBG_CNT_SLOTS_LOG
+#define PBG_CNT_SLOTS_LOG 14
+#endif
+constexpr int CNT_SLOTS_LOG = PBG_CNT_SLOTS_LOG;
 constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
 constexpr uint32_t CNT_EMPTY = 0xffffffffu;
-constexpr int CNT_PER = 8;  // keys per thread for a bin of CNT_NT*CNT_PER tuples
+constexpr int CNT_PER = 8;  // keys per thread: bins of up to CNT_NT*CNT_PER tuples
+
+__device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
+                                         const uint32_t* __restrict__ skeys, const WorkBins& w,
+                                         uint64_t b, uint64_t nw, uint64_t cap, uint32_t (&kk)[CNT_PER],
+                                         uint32_t& n) {
+    n = 0;
+    if (b >= nw) return;
+    const uint32_t fl = w.flags[b];
+    const uint64_t nn = w.n[b];
+    if ((fl & 2u) || nn > cap) return;
+    n = static_cast<uint32_t>(nn);
+    const uint32_t* kb = ((fl & 1u) ? skeys : keys) + w.off[b];
+#pragma unroll
+    for (int j = 0; j < CNT_PER; ++j) {
+        const uint32_t i = threadIdx.x + j * CNT_NT;
+        kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
+    }
+}
 
 __global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict__ keys,
                                                    const uint32_t* __restrict__ skeys,
@@ -359,30 +380,23 @@ __global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict_
         reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
     __syncthreads();
     int par = 0;
-    for (uint64_t b = blockIdx.x; b < nw; b += gridDim.x) {
-        const uint64_t n = w.n[b];
-        const uint32_t fl = w.flags[b];
-        if (fl & 2u) {  // uniform key: one merged entry
-            if (tid == 0) wb_nnz[b] = 1;
-            continue;
-        }
-        if (n > cap || n > static_cast<uint64_t>(CNT_NT) * CNT_PER) {
-            if (tid == 0) wb_nnz[b] = 0;  // cannot happen for a valid work list
-            continue;
-        }
-        const uint32_t* kb = ((fl & 1u) ? skeys : keys) + w.off[b];
-        uint32_t slot[CNT_PER], kk[CNT_PER];
-        uint32_t fresh = 0;
+    uint32_t kk[CNT_PER], n;
+    uint64_t b = blockIdx.x;
+    cnt_load(keys, skeys, w, b, nw, cap, kk, n);  // software pipeline: keys of bin b
+    for (; b < nw; b += gridDim.x) {
+        uint32_t cur[CNT_PER];
 #pragma unroll
-        for (int j = 0; j < CNT_PER; ++j) {  // all loads in flight first
-            const uint32_t i = tid + j * CNT_NT;
-            kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
-        }
+        for (int j = 0; j < CNT_PER; ++j) cur[j] = kk[j];
+        const uint32_t ncur = n;
+        const uint32_t fl = w.flags[b];
+        cnt_load(keys, skeys, w, b + gridDim.x, nw, cap, kk, n);  // next bin's keys in flight
+        uint32_t slot[CNT_PER];
+        uint32_t fresh = 0;
 #pragma unroll
         for (int j = 0; j < CNT_PER; ++j) {
             slot[j] = CNT_SLOTS;  // none
-            const uint32_t key = kk[j];
-            if (tid + j * CNT_NT < n) {
+            if (tid + j * CNT_NT < ncur) {
+                const uint32_t key = cur[j];
                 uint32_t h = (key * 0x9E3779B1u) >> (32 - CNT_SLOTS_LOG);
                 while (true) {
                     const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
@@ -407,7 +421,9 @@ __global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict_
         if (tid == 0) {
             uint32_t t = 0;
             for (int i = 0; i < CNT_NT / 32; ++i) t += s_red[par][i];
-            wb_nnz[b] = t;
+            // uniform-key items merge to one entry; a valid list has no other
+            // bin above the capacity
+            wb_nnz[b] = (fl & 2u) ? 1u : t;
         }
         par ^= 1;
         __syncthreads();

@@ -233,13 +233,25 @@ __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
                            unsigned long long* cursor, unsigned long long* heavy,
                            unsigned long long* maxbin) {
     const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (b >= *nb_dev) return;
-    const uint64_t c = row_off[bin_rs[b + 1]] - row_off[bin_rs[b]];
-    bin_cnt[b] = c;
-    bin_pad[b] = (c + 3) & ~3ull;
-    cursor[b] = 0;
-    if (c > cap) atomicAdd(heavy, 1ull);
-    atomicMax(maxbin, static_cast<unsigned long long>(c));
+    uint64_t c = 0;
+    if (b < *nb_dev) {
+        c = row_off[bin_rs[b + 1]] - row_off[bin_rs[b]];
+        bin_cnt[b] = c;
+        bin_pad[b] = (c + 3) & ~3ull;
+        cursor[b] = 0;
+    }
+    // warp-aggregated: one atomic per warp instead of one per bin
+    const uint32_t nh = __popc(__ballot_sync(FULL, c > cap));
+    uint64_t mx = c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = __shfl_xor_sync(FULL, mx, o);
+        mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nh) atomicAdd(heavy, static_cast<unsigned long long>(nh));
+        if (mx) atomicMax(maxbin, static_cast<unsigned long long>(mx));
+    }
 }
 
 // ---------------------------------------------------------------- expand --
@@ -280,9 +292,49 @@ struct ExpandArgs {
     uint32_t* keys;
     double* vals;
     int col_bits;
+    // run plan (k_runs -> k_expand_runs): one entry per A entry
+    uint64_t* run_dst;  // tuple offset reserved in the row's bin
+    uint64_t* run_src;  // first entry of B(k,:)
+    uint32_t* run_len;  // nnz(B(k,:))
+    uint32_t* run_rp;   // (row - bin_row_start) << col_bits
 };
 
 constexpr int EXP_NT = 256;
+#ifndef PBG_EXP_U
+#define PBG_EXP_U 4
+#endif
+#ifndef PBG_EXP_EVICT_LAST
+#define PBG_EXP_EVICT_LAST 1
+#endif
+constexpr int EXP_U = PBG_EXP_U;  // tuple steps in flight per lane
+
+// Tuple stores. With PBG_EXP_EVICT_LAST the lines carry an L2 evict_last
+// policy: a bin's partially written frontier line then survives the
+// streaming input reads until its neighbours complete it, instead of being
+// written back half-full (read-modify-write of the missing bytes).
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_tuple_key(uint32_t* p, uint32_t v) {
+#if PBG_EXP_EVICT_LAST
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v),
+                 "l"(l2_evict_last_policy())
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void st_tuple_val(double* p, double v) {
+#if PBG_EXP_EVICT_LAST
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v),
+                 "l"(l2_evict_last_policy())
+                 : "memory");
+#else
+    *p = v;
+#endif
+}
 constexpr int EXP_NW = EXP_NT / 32;
 
 // Outer-product expansion (expand_impl, pb_spgemm.cpp:180-246). One warp per
@@ -295,7 +347,10 @@ constexpr int EXP_NW = EXP_NT / 32;
 // run are coalesced and no lane idles on short runs. The 126 MB L2 plays the
 // role of the reference's thread-private local bins: each bin's write
 // frontier stays resident until its lines are full.
-__global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
+#ifndef PBG_EXP_MINB
+#define PBG_EXP_MINB 4
+#endif
+__global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
     __shared__ uint64_t s_dst[EXP_NW][32];
     __shared__ uint64_t s_bst[EXP_NW][32];
     __shared__ double s_av[EXP_NW][32];
@@ -341,7 +396,11 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
                     av = a.a_vals[pl];
                     const uint32_t bin = a.row_bin[r];
                     const uint32_t rs = a.bin_rs[bin];
+#ifdef PBG_DIAG_NOATOMIC
+                    const uint64_t pos = 0;  // timing experiment only (wrong output)
+#else
                     const uint64_t pos = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
+#endif
                     dst = a.bin_off[bin] + pos;
                     rp = static_cast<uint32_t>((static_cast<uint64_t>(r - rs)) << cb);
                 }
@@ -360,29 +419,178 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(ExpandArgs a) {
                 s_rp[w][rank] = rp;
             }
             __syncwarp();
+            // tuples, EXP_U steps of 32 per iteration: all B loads of the
+            // group are issued before any store so their latencies overlap
             uint32_t before = 0;
-            for (uint64_t s = 0; s < total; s += 32) {
-                const uint32_t bit =
-                    (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
-                const uint32_t mk = __reduce_or_sync(FULL, bit);
-                const uint64_t t = s + lane;
-                if (t < total) {
+            for (uint64_t s0 = 0; s0 < total; s0 += 32 * EXP_U) {
+                uint32_t kv[EXP_U];
+                double bv[EXP_U], avv[EXP_U];
+                uint32_t rpv[EXP_U];
+                uint64_t dv[EXP_U];
+                bool ok[EXP_U];
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+                    const uint64_t s = s0 + 32 * u;
+                    const uint32_t bit =
+                        (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
+                    const uint32_t mk = __reduce_or_sync(FULL, bit);
+                    const uint64_t t = s + lane;
+                    ok[u] = t < total;
                     const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-                    const int ri = before + __popc(mk & upto) - 1;
+                    int ri = static_cast<int>(before + __popc(mk & upto)) - 1;
+                    ri = ok[u] ? ri : 0;
                     const uint64_t q = t - s_st[w][ri];
                     const uint64_t src = s_bst[w][ri] + q;
-                    const uint32_t key = s_rp[w][ri] | a.b_colids[src];
-                    const double v = s_av[w][ri] * a.b_vals[src];
-                    const uint64_t d = s_dst[w][ri] + q;
-                    a.keys[d] = key;
-                    a.vals[d] = v;
+                    kv[u] = ok[u] ? __ldg(a.b_colids + src) : 0u;
+                    bv[u] = ok[u] ? __ldg(a.b_vals + src) : 0.0;
+                    rpv[u] = s_rp[w][ri];
+                    avv[u] = s_av[w][ri];
+                    dv[u] = s_dst[w][ri] + q;
+                    before += __popc(mk);
                 }
-                before += __popc(mk);
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+#ifdef PBG_DIAG_NOSTORE
+                    if (ok[u] && (rpv[u] | kv[u]) == 0xfffffffeu && avv[u] * bv[u] == 1.2345)
+#else
+                    if (ok[u])
+#endif
+                    {
+                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u]);
+                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u]);
+                    }
+                }
             }
             __syncwarp();
             const int last = (pend - p) < 32 ? static_cast<int>(pend - p) - 1 : 31;
             kcur = __shfl_sync(FULL, kl, last);
             p += 32;
+        }
+    }
+}
+
+
+// ----------------------------------------------------- expand, split form --
+// Phase 1 (k_runs): one thread per column k of A (the whole warp for long
+// columns) walks A(:,k): every A entry p is a run of nnz(B(k,:)) tuples into
+// its row's bin; the run's slots are reserved with one atomicAdd on the bin
+// cursor (the reference's `omp atomic capture`, pb_spgemm.cpp:196-214) and
+// the run plan (destination, B source, length, key row part) is stored.
+// Massively parallel and independent per run, so the dependent loads
+// (row -> bin -> cursor) of 16 M runs overlap across threads instead of
+// serialising inside the tuple-streaming warps.
+__global__ void __launch_bounds__(256) k_runs(ExpandArgs a) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t p0 = 0, p1 = 0, lb = 0, bst = 0;
+    if (i < a.a_ncols) {
+        p0 = a.a_colptr[i];
+        p1 = a.a_colptr[i + 1];
+        bst = a.b_rowptr[i];
+        lb = a.b_rowptr[i + 1] - bst;
+    }
+    const int cb = a.col_bits;
+    auto one = [&](uint64_t p, uint64_t len, uint64_t src) {
+        a.run_len[p] = static_cast<uint32_t>(len);
+        if (!len) return;
+        const uint32_t r = a.a_rowids[p];
+        const uint32_t bin = a.row_bin[r];
+        const uint64_t pos = atomicAdd(&a.cursor[bin], (unsigned long long)len);
+        a.run_dst[p] = a.bin_off[bin] + pos;
+        a.run_src[p] = src;
+        a.run_rp[p] = static_cast<uint32_t>(static_cast<uint64_t>(r - a.bin_rs[bin]) << cb);
+    };
+    const bool longcol = (p1 - p0) > 32;
+    if (!longcol)
+        for (uint64_t p = p0; p < p1; ++p) one(p, lb, bst);
+    uint32_t lm = __ballot_sync(FULL, longcol);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint64_t q0 = __shfl_sync(FULL, p0, src), q1 = __shfl_sync(FULL, p1, src);
+        const uint64_t qb = __shfl_sync(FULL, lb, src), qs = __shfl_sync(FULL, bst, src);
+        for (uint64_t p = q0 + lane; p < q1; p += 32) one(p, qb, qs);
+    }
+}
+
+// Phase 2 (k_expand_runs): one warp per chunk of runs; 32 runs per batch,
+// their plans read coalesced, lengths scanned, then the batch's tuples are
+// streamed flat (EXP_U steps of 32 in flight per lane).
+__global__ void __launch_bounds__(EXP_NT) k_expand_runs(ExpandArgs a) {
+    __shared__ uint64_t s_dst[EXP_NW][32];
+    __shared__ uint64_t s_bst[EXP_NW][32];
+    __shared__ double s_av[EXP_NW][32];
+    __shared__ uint64_t s_st[EXP_NW][32];
+    __shared__ uint32_t s_rp[EXP_NW][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lt = lanemask_lt();
+    for (uint64_t c = gw; c < a.nchunks; c += nw) {
+        const uint64_t pend = a.chunk_p0[c + 1];
+        for (uint64_t p = a.chunk_p0[c]; p < pend; p += 32) {
+            const uint64_t pl = p + lane;
+            const uint64_t lb = pl < pend ? a.run_len[pl] : 0;
+            const bool ne = lb != 0;
+            uint64_t dst = 0, bst = 0;
+            uint32_t rp = 0;
+            double av = 0.0;
+            if (ne) {
+                dst = a.run_dst[pl];
+                bst = a.run_src[pl];
+                rp = a.run_rp[pl];
+                av = a.a_vals[pl];
+            }
+            const uint32_t nemask = __ballot_sync(FULL, ne);
+            const int rank = __popc(nemask & lt);
+            const uint64_t incl = warp_inclusive_scan(lb);
+            const uint64_t start = incl - lb;
+            const uint64_t total = __shfl_sync(FULL, incl, 31);
+            __syncwarp();
+            if (ne) {
+                s_dst[w][rank] = dst;
+                s_bst[w][rank] = bst;
+                s_av[w][rank] = av;
+                s_st[w][rank] = start;
+                s_rp[w][rank] = rp;
+            }
+            __syncwarp();
+            uint32_t before = 0;
+            for (uint64_t s0 = 0; s0 < total; s0 += 32 * EXP_U) {
+                uint32_t kv[EXP_U];
+                double bv[EXP_U], avv[EXP_U];
+                uint32_t rpv[EXP_U];
+                uint64_t dv[EXP_U];
+                bool ok[EXP_U];
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+                    const uint64_t s = s0 + 32 * u;
+                    const uint32_t bit =
+                        (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
+                    const uint32_t mk = __reduce_or_sync(FULL, bit);
+                    const uint64_t t = s + lane;
+                    ok[u] = t < total;
+                    const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+                    int ri = static_cast<int>(before + __popc(mk & upto)) - 1;
+                    ri = ok[u] ? ri : 0;
+                    const uint64_t q = t - s_st[w][ri];
+                    const uint64_t src = s_bst[w][ri] + q;
+                    kv[u] = ok[u] ? __ldg(a.b_colids + src) : 0u;
+                    bv[u] = ok[u] ? __ldg(a.b_vals + src) : 0.0;
+                    rpv[u] = s_rp[w][ri];
+                    avv[u] = s_av[w][ri];
+                    dv[u] = s_dst[w][ri] + q;
+                    before += __popc(mk);
+                }
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+                    if (ok[u]) {
+                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u]);
+                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u]);
+                    }
+                }
+            }
+            __syncwarp();
         }
     }
 }
