@@ -72,6 +72,9 @@ typedef struct pbg_config {
     int32_t balanced_bins; /* reference-layout report only                 */
     int32_t device;        /* CUDA ordinal, -1 = current device            */
     uint32_t bin_cap;      /* GPU bin capacity in tuples, 0 = default 4096 */
+    /* reserved[0]: cap on tuples per round of the host path (0 = from free
+     * HBM); when flop exceeds it, pbg_multiply_begin runs flop-balanced row
+     * bands one after another and assembles C on the host. */
     uint64_t reserved[4];
 } pbg_config;
 

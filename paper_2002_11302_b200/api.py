@@ -54,6 +54,7 @@ class PbConfig:
     balanced_bins: bool = False
     device: int = -1
     bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
+    max_round_tuples: int = 0  # host path: tuples per bounded-memory round (0 = from free HBM)
 
     def to_c(self) -> _native.Config:
         c = _native.Config()
@@ -61,6 +62,7 @@ class PbConfig:
         c.nbins, c.lbin_bytes, c.l2_bytes = self.nbins, self.lbin_bytes, self.l2_bytes
         c.nthreads, c.balanced_bins = self.nthreads, int(self.balanced_bins)
         c.device, c.bin_cap = self.device, self.bin_cap
+        c.reserved[0] = self.max_round_tuples
         return c
 
 

@@ -136,6 +136,15 @@ struct pbg_handle {
     pbg_context* ctx = nullptr;
     pbg_config cfg{};
     double t_h2d = 0.0;
+    // bounded-memory rounds: C assembled on the host band by band
+    bool rounds = false;
+    uint32_t nrounds = 1;
+    std::vector<uint64_t> rowptr;
+    std::vector<uint32_t> colids;
+    std::vector<double> values;
+    std::vector<uint64_t> row_flop;   // host per-row flop (reference-layout report)
+    std::vector<uint64_t> col_flop;   // host per-column flop
+    pbg_report rep{};
 };
 
 namespace {
@@ -149,6 +158,8 @@ int set_device(int dev) {
     if (dev >= 0) CUDA_TRY(cudaSetDevice(dev));
     return PBG_OK;
 }
+
+uint32_t reference_nbins(const pbg_config& cfg, uint64_t flop, uint64_t m, int cb);
 
 int validate_view(const pbg_csx_view* v, const char* what) {
     if (!v) return fail(PBG_ERR_ARG, std::string(what) + " view is null");
@@ -476,6 +487,11 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                                                            bin_hidx, wpos, hhead, hcount, hc,
                                                            cur, cb, w);
         L += 3;
+        if (nitems) {
+            k_work_fill_items<<<blocks_for(nitems, 256), 256, 0, st>>>(wpos, bin_rs, hhead, hc, cur,
+                                                                       nitems, w);
+            ++L;
+        }
         const uint64_t* nw_dev = reinterpret_cast<const uint64_t*>(sc + S_NWORK);
 
         // ---- distinct keys per work bin -> output offset of every work bin ----
@@ -579,15 +595,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     ctx->rep.t_total = t_tot * 1e-3;
     ctx->rep.nnz_c = ctx->nnz_c;
     // reference-layout bin count (choose_nbins, pb_spgemm.cpp:109-114)
-    {
-        uint32_t nbr = cfg.nbins ? cfg.nbins : pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 12);
-        if (m > 0) {
-            uint64_t rpb = (m + nbr - 1) / nbr;
-            if (cfg.nbins == 0 && ceil_log2_u64(rpb) + cb > 32)
-                nbr = pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 16);
-        }
-        ctx->rep.nbins = nbr;
-    }
+    ctx->rep.nbins = reference_nbins(cfg, flop, m, cb);
     ctx->launches = L;
     ctx->have_result = true;
     return PBG_OK;
@@ -630,6 +638,162 @@ int copy_in(DevBuf& b, const void* src, size_t bytes, cudaStream_t st) {
     int rc = grow(b, bytes);
     if (rc) return rc;
     if (bytes) CUDA_TRY(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st));
+    return PBG_OK;
+}
+
+
+// The reference bin layout (pb_spgemm.cpp:107-137: uniform ranges of
+// ceil(m/nbins) rows, or balanced_starts :58-82) from a host per-row flop.
+int reference_layout(const pbg_config& cfg, uint32_t nbins, const std::vector<uint64_t>& rf,
+                     const std::vector<uint64_t>& colflop, uint64_t* per_column_flop,
+                     uint64_t* per_bin_flop, uint32_t* bin_row_starts, uint64_t flop,
+                     int col_bits) {
+    if (per_column_flop && !colflop.empty())
+        std::memcpy(per_column_flop, colflop.data(), colflop.size() * 8);
+    const uint64_t m = rf.size();
+    const uint32_t nb = nbins ? nbins : 1;
+    const uint64_t rpb = m ? (m + nb - 1) / nb : 0;
+    std::vector<uint32_t> starts(nb + 1);
+    for (uint32_t b = 0; b <= nb; ++b) starts[b] = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(b) * rpb, m));
+    std::vector<uint64_t> pbf(nb, 0);
+    for (uint64_t r = 0; r < m; ++r) pbf[rpb ? r / rpb : 0] += rf[r];
+    if (cfg.balanced_bins) {
+        const uint32_t tb = ceil_log2_u64(rpb) + col_bits <= 32 ? 12 : 16;
+        const uint64_t maxb = pbf.empty() ? 0 : *std::max_element(pbf.begin(), pbf.end());
+        if (maxb * tb > cfg.l2_bytes) {
+            std::fill(starts.begin(), starts.end(), static_cast<uint32_t>(m));
+            starts[0] = 0;
+            const double target = static_cast<double>(flop) / nb;
+            uint64_t acc = 0;
+            uint32_t bin = 1;
+            for (uint64_t r = 0; r < m && bin < nb; ++r) {
+                acc += rf[r];
+                if (static_cast<double>(acc) >= target * bin) starts[bin++] = static_cast<uint32_t>(r + 1);
+            }
+            std::fill(pbf.begin(), pbf.end(), 0);
+            for (uint32_t b = 0; b < nb; ++b)
+                for (uint64_t r = starts[b]; r < starts[b + 1]; ++r) pbf[b] += rf[r];
+        }
+    }
+    if (per_bin_flop) std::memcpy(per_bin_flop, pbf.data(), nb * 8);
+    if (bin_row_starts) std::memcpy(bin_row_starts, starts.data(), (nb + 1) * 4);
+    return PBG_OK;
+}
+
+uint32_t reference_nbins(const pbg_config& cfg, uint64_t flop, uint64_t m, int cb) {
+    uint32_t nbr = cfg.nbins ? cfg.nbins : pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 12);
+    if (m > 0) {
+        const uint64_t rpb = (m + nbr - 1) / nbr;
+        if (cfg.nbins == 0 && ceil_log2_u64(rpb) + cb > 32)
+            nbr = pbg_choose_nbins(flop, static_cast<uint32_t>(m), cfg.l2_bytes, 16);
+    }
+    return nbr;
+}
+
+// Bounded-memory rounds: flop-balanced row bands of A, each
+// extracted on the host as its own CSC, multiplied on the device against the
+// resident B, and its CSR band appended on the host. Every band is the
+// reference product of those rows (C(r0:r1,:) = A(r0:r1,:) * B).
+int multiply_in_rounds(pbg_handle* h, const pbg_csx_view& a, const pbg_csx_view& b,
+                       const pbg_config& cfg, uint32_t nrounds, cudaStream_t st) {
+    pbg_context* ctx = h->ctx;
+    int rc;
+    const uint64_t m = a.nrows, k = a.ncols;
+    // per-row / per-column flop on the host
+    h->row_flop.assign(m, 0);
+    h->col_flop.assign(k, 0);
+    for (uint64_t j = 0; j < k; ++j) {
+        const uint64_t lb = b.ptr[j + 1] - b.ptr[j];
+        h->col_flop[j] = (a.ptr[j + 1] - a.ptr[j]) * lb;
+        for (uint64_t p = a.ptr[j]; p < a.ptr[j + 1]; ++p) h->row_flop[a.idx[p]] += lb;
+    }
+    uint64_t flop = 0;
+    for (uint64_t r = 0; r < m; ++r) flop += h->row_flop[r];
+    std::vector<uint32_t> cuts(nrounds + 1, static_cast<uint32_t>(m));
+    cuts[0] = 0;
+    {
+        unsigned __int128 acc = 0;
+        uint32_t j = 1;
+        for (uint64_t r = 0; r < m && j < nrounds; ++r) {
+            acc += h->row_flop[r];
+            while (j < nrounds && acc * nrounds >= (unsigned __int128)flop * j) cuts[j++] = static_cast<uint32_t>(r + 1);
+        }
+    }
+    // B stays resident for every round
+    rc = copy_in(ctx->in_b_ptr, b.ptr, (uint64_t(b.nrows) + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_idx, b.idx, b.nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_val, b.val, b.nnz * 8, st);
+    if (rc) return rc;
+    const pbg_csx_view db{b.nrows, b.ncols, b.nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                          static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                          static_cast<const double*>(ctx->in_b_val.p)};
+    h->rounds = true;
+    h->nrounds = nrounds;
+    h->rowptr.assign(m + 1, 0);
+    h->colids.clear();
+    h->values.clear();
+    pbg_report tot{};
+    std::vector<uint64_t> sp(k + 1);
+    std::vector<uint32_t> si;
+    std::vector<double> sv;
+    std::vector<uint64_t> brow;
+    for (uint32_t rd = 0; rd < nrounds; ++rd) {
+        const uint32_t r0 = cuts[rd], r1 = cuts[rd + 1];
+        // host row slab of A (rows renumbered from 0), pbgh_csc_row_band semantics
+        si.clear();
+        sv.clear();
+        sp[0] = 0;
+        for (uint64_t j = 0; j < k; ++j) {
+            const uint32_t* lo = std::lower_bound(a.idx + a.ptr[j], a.idx + a.ptr[j + 1], r0);
+            const uint32_t* hi = std::lower_bound(lo, a.idx + a.ptr[j + 1], r1);
+            for (const uint32_t* q = lo; q < hi; ++q) {
+                si.push_back(*q - r0);
+                sv.push_back(a.val[q - a.idx]);
+            }
+            sp[j + 1] = si.size();
+        }
+        rc = copy_in(ctx->in_a_ptr, sp.data(), (k + 1) * 8, st);
+        if (!rc) rc = copy_in(ctx->in_a_idx, si.data(), si.size() * 4, st);
+        if (!rc) rc = copy_in(ctx->in_a_val, sv.data(), sv.size() * 8, st);
+        if (rc) return rc;
+        const pbg_csx_view da{r1 - r0, a.ncols, si.size(), static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                              static_cast<const double*>(ctx->in_a_val.p)};
+        if ((rc = run_pipeline(ctx, da, db, cfg, st))) return rc;
+        const uint64_t base = h->colids.size(), bn = ctx->nnz_c;
+        brow.resize(uint64_t(r1 - r0) + 1);
+        CUDA_TRY(cudaMemcpy(brow.data(), ctx->rowptr.p, brow.size() * 8, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < uint64_t(r1 - r0); ++r) h->rowptr[r0 + r] = base + brow[r];
+        h->colids.resize(base + bn);
+        h->values.resize(base + bn);
+        if (bn) {
+            CUDA_TRY(cudaMemcpy(h->colids.data() + base, ctx->ccol.p, bn * 4, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(h->values.data() + base, ctx->cval.p, bn * 8, cudaMemcpyDeviceToHost));
+        }
+        const pbg_report& r = ctx->rep;
+        tot.t_symbolic += r.t_symbolic;
+        tot.t_expand += r.t_expand;
+        tot.t_sort += r.t_sort;
+        tot.t_total += r.t_total;
+        tot.t_count += r.t_count;
+        tot.t_sortmerge_kernel += r.t_sortmerge_kernel;
+        tot.flop += r.flop;
+        tot.tuples_into_sort += r.tuples_into_sort;
+        tot.merged_total += r.merged_total;
+        tot.gpu_bins += r.gpu_bins;
+        tot.heavy_bins += r.heavy_bins;
+        tot.sort_fallbacks += r.sort_fallbacks;
+        tot.tuple_bytes = std::max(tot.tuple_bytes, r.tuple_bytes);
+        tot.bin_cap = r.bin_cap;
+    }
+    h->rowptr[m] = h->colids.size();
+    tot.nnz_c = h->colids.size();
+    tot.nnz_a = a.nnz;
+    tot.nnz_b = b.nnz;
+    tot.nbins = reference_nbins(cfg, flop, m, ctx->col_bits);
+    h->rep = tot;
+    if (tot.flop != flop || tot.merged_total != tot.nnz_c)
+        return fail(PBG_ERR_INTERNAL, "round totals disagree with the full product");
     return PBG_OK;
 }
 
@@ -727,37 +891,10 @@ int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg_in, uint64_t* p
         for (uint64_t i = 0; i < k; ++i) per_column_flop[i] = off[i + 1] - off[i];
     }
     if (!per_bin_flop && !bin_row_starts) return PBG_OK;
-    // The reference bin layout (pb_spgemm.cpp:107-137) from the device's
-    // per-row flop.
     std::vector<uint64_t> rf(m);
     if (m && ctx->flop) CUDA_TRY(cudaMemcpy(rf.data(), ctx->row_flop.p, m * 8, cudaMemcpyDeviceToHost));
-    const uint32_t nb = ctx->rep.nbins ? ctx->rep.nbins : 1;
-    const uint64_t rpb = m ? (m + nb - 1) / nb : 0;
-    std::vector<uint32_t> starts(nb + 1);
-    for (uint32_t b = 0; b <= nb; ++b) starts[b] = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(b) * rpb, m));
-    std::vector<uint64_t> pbf(nb, 0);
-    for (uint64_t r = 0; r < m; ++r) pbf[rpb ? r / rpb : 0] += rf[r];
-    if (cfg.balanced_bins) {
-        const uint32_t tb = ceil_log2_u64(rpb) + ctx->col_bits <= 32 ? 12 : 16;
-        const uint64_t maxb = pbf.empty() ? 0 : *std::max_element(pbf.begin(), pbf.end());
-        if (maxb * tb > cfg.l2_bytes) {  // balanced_starts, pb_spgemm.cpp:58-82
-            std::fill(starts.begin(), starts.end(), static_cast<uint32_t>(m));
-            starts[0] = 0;
-            const double target = static_cast<double>(ctx->flop) / nb;
-            uint64_t acc = 0;
-            uint32_t bin = 1;
-            for (uint64_t r = 0; r < m && bin < nb; ++r) {
-                acc += rf[r];
-                if (static_cast<double>(acc) >= target * bin) starts[bin++] = static_cast<uint32_t>(r + 1);
-            }
-            std::fill(pbf.begin(), pbf.end(), 0);
-            for (uint32_t b = 0; b < nb; ++b)
-                for (uint64_t r = starts[b]; r < starts[b + 1]; ++r) pbf[b] += rf[r];
-        }
-    }
-    if (per_bin_flop) std::memcpy(per_bin_flop, pbf.data(), nb * 8);
-    if (bin_row_starts) std::memcpy(bin_row_starts, starts.data(), (nb + 1) * 4);
-    return PBG_OK;
+    return reference_layout(cfg, ctx->rep.nbins, rf, {}, nullptr, per_bin_flop, bin_row_starts,
+                            ctx->flop, ctx->col_bits);
 }
 
 int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
@@ -783,43 +920,72 @@ int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_c
     h->ctx = ctx;
     h->cfg = cfg;
     cudaStream_t st = nullptr;
+    // ---- memory plan: one pass, or bounded-memory rounds over row bands ----
+    // (configs whose tuples + C exceed HBM run band by band)
+    uint64_t flop = 0;
+    for (uint64_t i = 0; i < a->ncols; ++i) flop += (a->ptr[i + 1] - a->ptr[i]) * (b->ptr[i + 1] - b->ptr[i]);
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t inputs = (uint64_t(a->ncols) + uint64_t(b->nrows) + 2) * 8 + (a->nnz + b->nnz) * 12;
+    const uint64_t work_rows = (uint64_t(a->nrows) + 2) * 96;
+    const uint64_t reserve = 2ull << 30;
+    uint64_t budget = free_b > inputs + work_rows + reserve ? free_b - inputs - work_rows - reserve : 0;
+    // 12 B tuples + a C upper bound of 12 B per tuple, plus run plans / scratch slack
+    uint64_t per_tuple = 24 + 4;
+    uint64_t max_tuples = budget / per_tuple;
+    if (cfg.reserved[0]) max_tuples = std::min<uint64_t>(max_tuples, cfg.reserved[0]);
+    const uint32_t nrounds = (flop > max_tuples && max_tuples > 0)
+                                 ? static_cast<uint32_t>((flop + max_tuples - 1) / max_tuples)
+                                 : 1u;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    cudaEventRecord(e0, st);
-    rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
-    if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
-    if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
-    if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
-    cudaEventRecord(e1, st);
-    if (!rc) {
-        pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
-                        static_cast<const uint32_t*>(ctx->in_a_idx.p),
-                        static_cast<const double*>(ctx->in_a_val.p)};
-        pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
-                        static_cast<const uint32_t*>(ctx->in_b_idx.p),
-                        static_cast<const double*>(ctx->in_b_val.p)};
-        rc = run_pipeline(ctx, da, db, cfg, st);
+    if (nrounds == 1) {
+        cudaEventRecord(e0, st);
+        rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
+        if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
+        if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
+        if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
+        if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
+        if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
+        cudaEventRecord(e1, st);
+        if (!rc) {
+            pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                            static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                            static_cast<const double*>(ctx->in_a_val.p)};
+            pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                            static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                            static_cast<const double*>(ctx->in_b_val.p)};
+            rc = run_pipeline(ctx, da, db, cfg, st);
+        }
+        float ms = 0;
+        if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
+            h->t_h2d = ms * 1e-3;
+    } else {
+        rc = multiply_in_rounds(h, *a, *b, cfg, nrounds, st);
     }
-    float ms = 0;
-    if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
-        h->t_h2d = ms * 1e-3;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (rc) {
         pbg_release(h);
         return rc;
     }
-    if (nnz_c) *nnz_c = ctx->nnz_c;
+    if (nnz_c) *nnz_c = h->rounds ? h->colids.size() : ctx->nnz_c;
     *out = h;
     return PBG_OK;
 }
 
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
                        pbg_report* rep) {
-    if (!h || !h->ctx || !h->ctx->have_result) return fail(PBG_ERR_ARG, "invalid handle");
+    if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");
+    if (h->rounds) {
+        if (rowptr) std::memcpy(rowptr, h->rowptr.data(), h->rowptr.size() * 8);
+        if (colids) std::memcpy(colids, h->colids.data(), h->colids.size() * 4);
+        if (values) std::memcpy(values, h->values.data(), h->values.size() * 8);
+        if (rep) *rep = h->rep;
+        return PBG_OK;
+    }
+    if (!h->ctx->have_result) return fail(PBG_ERR_ARG, "invalid handle");
     pbg_context* ctx = h->ctx;
     CUDA_TRY(cudaSetDevice(ctx->device));
     cudaEvent_t e0, e1;
@@ -848,6 +1014,9 @@ int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double
 int pbg_symbolic_fetch(pbg_handle* h, uint64_t* per_column_flop, uint64_t* per_bin_flop,
                        uint32_t* bin_row_starts) {
     if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");
+    if (h->rounds)
+        return reference_layout(h->cfg, h->rep.nbins, h->row_flop, h->col_flop, per_column_flop,
+                                per_bin_flop, bin_row_starts, h->rep.flop, h->ctx->col_bits);
     return pbg_context_symbolic(h->ctx, &h->cfg, per_column_flop, per_bin_flop, bin_row_starts);
 }
 

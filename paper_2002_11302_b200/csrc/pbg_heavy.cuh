@@ -321,18 +321,27 @@ __global__ void k_work_fill(const uint64_t* nb_dev, const uint32_t* __restrict__
         w.flags[p] = 0;
         return;
     }
-    const uint32_t first = head[h], cnt = hcount[h];
-    for (uint32_t j = 0; j < cnt; ++j) {
-        const uint32_t it = first + j;
-        const uint64_t q = p + j;
-        w.off[q] = item_base(c, h, fin.buf[it]) + fin.loc[it];
-        w.n[q] = fin.n[it];
-        w.rs[q] = rs;
-        w.span[q] = j == 0 ? 1u : 0u;
-        w.keylo[q] = fin.keylo[it];
-        w.keybits[q] = fin.keybits[it];
-        w.flags[q] = (fin.buf[it] ? 1u : 0u) | (fin.kind[it] == IT_UNIFORM ? 2u : 0u) | 4u;
-    }
+    // heavy row: its items are filled by k_work_fill_items (one thread each)
+}
+
+// Work bins of heavy-row items: item `it` of row h lands at wpos[bin] + (it - head[h]).
+__global__ void k_work_fill_items(const uint64_t* __restrict__ wpos,
+                                  const uint32_t* __restrict__ bin_rs,
+                                  const uint32_t* __restrict__ head, HeavyCtx c, Items fin,
+                                  uint64_t nitems, WorkBins w) {
+    const uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (it >= nitems) return;
+    const uint32_t h = fin.h[it];
+    const uint32_t b = c.hbin[h];
+    const uint32_t j = static_cast<uint32_t>(it) - head[h];
+    const uint64_t q = wpos[b] + j;
+    w.off[q] = item_base(c, h, fin.buf[it]) + fin.loc[it];
+    w.n[q] = fin.n[it];
+    w.rs[q] = bin_rs[b];
+    w.span[q] = j == 0 ? 1u : 0u;
+    w.keylo[q] = fin.keylo[it];
+    w.keybits[q] = fin.keybits[it];
+    w.flags[q] = (fin.buf[it] ? 1u : 0u) | (fin.kind[it] == IT_UNIFORM ? 2u : 0u) | 4u;
 }
 
 // ------------------------------------------------------ work-bin counts --

@@ -287,20 +287,73 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
     return tot;
 }
 
+// Duplicate-heavy bin (its distinct count from k_bincount is <= n/2, e.g.
+// the 27-point stencil squared, cf ~ 6): sum duplicates first in a
+// shared-memory hash table (buffer `scr`, load <= 1/2), then compact the
+// distinct (key, sum) pairs back into `in`. Returns the distinct count.
+__device__ uint32_t hash_premerge(SortSmem& sm, int in, int scr, uint32_t n) {
+    const int tid = threadIdx.x;
+    uint32_t* HK = sm.k[scr];
+    double* HV = sm.v[scr];
+    for (uint32_t i = tid; i < SM_CAP; i += SM_NT) {
+        HK[i] = 0xffffffffu;
+        HV[i] = 0.0;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += SM_NT) {
+        const uint32_t key = sm.k[in][i];
+        const double v = sm.v[in][i];
+        uint32_t h = (key * 0x9E3779B1u) >> (32 - __builtin_ctz(SM_CAP));
+        while (true) {
+            const uint32_t old = atomicCAS(&HK[h], 0xffffffffu, key);
+            if (old == 0xffffffffu || old == key) {
+                atomicAdd(&HV[h], v);
+                break;
+            }
+            h = (h + 1) & (SM_CAP - 1);
+        }
+    }
+    __syncthreads();
+    // compact occupied slots (ITEMS consecutive slots per thread)
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < SM_ITEMS; ++j) cnt += HK[tid * SM_ITEMS + j] != 0xffffffffu;
+    uint32_t tot;
+    uint32_t o = block_exclusive_scan<SM_NT>(cnt, sm.s_warp32, tot);
+#pragma unroll
+    for (int j = 0; j < SM_ITEMS; ++j) {
+        const uint32_t slot = tid * SM_ITEMS + j;
+        if (HK[slot] != 0xffffffffu) {
+            sm.k[in][o] = HK[slot];
+            sm.v[in][o] = HV[slot];
+            ++o;
+        }
+    }
+    __syncthreads();
+    return tot;
+}
+
 // Sort + merge the bin in buffer `in` using scratch buffer `scr`. Returns the
 // merged count; *res gets the buffer holding the merged output.
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
-                                   int bits, uint32_t keylo, int* res) {
+                                   int bits, uint32_t keylo, uint32_t distinct, int* res) {
     const int tid = threadIdx.x;
+    if (distinct * 2 <= n && n >= 64) {
+        n = hash_premerge(sm, in, scr, n);  // now n distinct keys, no duplicates
+        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+    }
     uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);
     const int sh = bits > SM_NB_BITS ? bits - SM_NB_BITS : 0;
     // ---- 1. bucket histogram / scan / scatter in -> scr ----
+    // (keeping the histogram's returned slot in registers to save the second
+    // atomic was measured slower: register pressure at 64 regs spills)
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t d = (sm.k[in][i] - keylo) >> sh;
         atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
     }
     __syncthreads();
-    scan_cnt(sm);
+    scan_cnt(sm);  // cnt[d] = start of bucket d
     __syncthreads();
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[in][i];
@@ -311,10 +364,24 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         sm.v[scr][pos] = sm.v[in][i];
     }
     __syncthreads();
-    // ---- 2. rank inside buckets scr -> in (cnt[d] = end of bucket d) ----
+    // cnt[d] is now the END of bucket d
+    // ---- 2. rank inside buckets scr -> in ----
     // (a fixed +-3 neighbour window without loops was measured slower: the
     // loop runs ~2 trips for buckets of ~1 tuple)
     bool big = false;
+    if (sh == 0) {
+        // a bucket is a single key: bucket order is sorted order, nothing to
+        // rank (duplicate-heavy keys, e.g. RMAT heavy-row pieces)
+        __syncthreads();
+        *res = scr;
+        bool dupz = false;
+        for (uint32_t i = tid + 1; i < n; i += SM_NT) dupz |= sm.k[scr][i] == sm.k[scr][i - 1];
+        if (__syncthreads_or(dupz)) {
+            *res = in;
+            return merge_dups(sm, scr, in, n);
+        }
+        return n;
+    }
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[scr][i];
         const uint32_t d = (key - keylo) >> sh;
@@ -449,7 +516,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             }
             __syncthreads();
             U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(a.w.keybits[b]),
-                               a.w.keylo[b], &res);
+                               a.w.keylo[b], static_cast<uint32_t>(a.wb_nnz[b]), &res);
         } else if (fl & 2u) {
             reduce_uniform(a, sm, b, inb);
             U = 1;

@@ -191,6 +191,11 @@ CONFIGS = {
     "C4": ("stencil", 128, None),
     "C5a": ("er", 24, 8),
     "C5b": ("rmat", 24, 8),
+    # scaled-down development configs (same generators)
+    "R16": ("rmat", 16, 16),
+    "R18": ("rmat", 18, 16),
+    "S64": ("stencil", 64, None),
+    "E22": ("er", 22, 8),
 }
 
 CONFIG_NAMES = {
@@ -200,6 +205,10 @@ CONFIG_NAMES = {
     "C4": "27-point stencil 128^3 (26 / -1), C=A*A",
     "C5a": "ER n=2^24 d=8, C=A*A, fp64 U[0,1)",
     "C5b": "RMAT scale 24 ef 8 (dedup, no self-loops), C=A*A, fp64 U[0,1)",
+    "R16": "dev: RMAT scale 16 ef 16, C=A*A",
+    "R18": "dev: RMAT scale 18 ef 16, C=A*A",
+    "S64": "dev: 27-point stencil 64^3, C=A*A",
+    "E22": "dev: ER n=2^22 d=8, C=A*A",
 }
 
 

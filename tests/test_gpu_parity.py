@@ -150,6 +150,23 @@ def test_row_bands_assemble_to_full_product():
                        full.c.values)
 
 
+def test_bounded_memory_rounds_match_single_pass():
+    """Forced row-band rounds (host path) give the single-pass product and
+    the same reference-layout symbolic report."""
+    for kind, scale in (("er", 13), ("rmat", 12)):
+        csr = M.make_matrix(kind, scale, 8, seed=17)
+        a = M.csr_to_csc(csr)
+        one = gpu(a, csr)
+        rounds = gpu(a, csr, max_round_tuples=max(one.sym.flop // 5, 1))
+        assert_csr_matches(rounds.c.rowptr, rounds.c.colids, rounds.c.values, one.c.rowptr,
+                           one.c.colids, one.c.values)
+        assert rounds.sym.flop == one.sym.flop and rounds.sym.nbins == one.sym.nbins
+        assert np.array_equal(rounds.sym.per_column_flop, one.sym.per_column_flop)
+        assert np.array_equal(rounds.sym.per_bin_flop, one.sym.per_bin_flop)
+        assert rounds.tuples_into_sort == one.sym.flop
+        assert rounds.merged_total == one.c.nnz
+
+
 def test_device_path_matches_host_path():
     import torch
     csr = M.make_matrix("er", 13, 6, seed=21)
