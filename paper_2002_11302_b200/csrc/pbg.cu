@@ -931,7 +931,7 @@ int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_c
     const uint64_t reserve = 2ull << 30;
     uint64_t budget = free_b > inputs + work_rows + reserve ? free_b - inputs - work_rows - reserve : 0;
     // 12 B tuples + a C upper bound of 12 B per tuple, plus run plans / scratch slack
-    uint64_t per_tuple = 24 + 4;
+    uint64_t per_tuple = 40;  // tuples 12 + C bound 12 + heavy scratch 12 + headroom
     uint64_t max_tuples = budget / per_tuple;
     if (cfg.reserved[0]) max_tuples = std::min<uint64_t>(max_tuples, cfg.reserved[0]);
     const uint32_t nrounds = (flop > max_tuples && max_tuples > 0)
