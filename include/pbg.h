@@ -74,7 +74,8 @@ typedef struct pbg_config {
     uint32_t bin_cap;      /* GPU bin capacity in tuples, 0 = default 4096 */
     /* reserved[0]: cap on tuples per round of the host path (0 = from free
      * HBM); when flop exceeds it, pbg_multiply_begin runs flop-balanced row
-     * bands one after another and assembles C on the host. */
+     * bands one after another and assembles C on the host.
+     * reserved[1]: force the number of expand row bands (0 = auto). */
     uint64_t reserved[4];
 } pbg_config;
 
@@ -94,6 +95,8 @@ typedef struct pbg_report {
     uint32_t bin_cap;
     uint64_t tuple_bytes;      /* bytes of tuple storage (12 B per tuple + pad)   */
     uint64_t sort_fallbacks;   /* bins sorted by the LSD fallback (clustered keys) */
+    uint32_t expand_bands;     /* row bands the expand ran in (L2 write frontier) */
+    uint32_t pad0;
     double t_count;            /* per-bin distinct-key count + offset scan (in t_sort) */
     double t_sortmerge_kernel; /* the sort+merge+CSR kernel alone (in t_sort)     */
 } pbg_report;

@@ -55,6 +55,7 @@ class PbConfig:
     device: int = -1
     bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
     max_round_tuples: int = 0  # host path: tuples per bounded-memory round (0 = from free HBM)
+    expand_bands: int = 0  # force the row bands of the expand (0 = auto, L2 frontier rule)
 
     def to_c(self) -> _native.Config:
         c = _native.Config()
@@ -63,6 +64,7 @@ class PbConfig:
         c.nthreads, c.balanced_bins = self.nthreads, int(self.balanced_bins)
         c.device, c.bin_cap = self.device, self.bin_cap
         c.reserved[0] = self.max_round_tuples
+        c.reserved[1] = self.expand_bands
         return c
 
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -96,6 +97,7 @@ constexpr int kTickets = 32;  // one u32 ticket per single-pass scan / persisten
 
 struct pbg_context {
     int device = 0;
+    bool rowflop32 = true;  // row_flop holds u32 counters (nnz(B) < 2^32)
     int num_sms = 148;
     DevBuf colflop_off, row_flop, row_off, flags, row_bin, bin_rs, bin_cnt, bin_off, cursor,
         bin_out, chunk_p0, keys, vals, ccol, cval, rowptr, zero_block, in_a_ptr, in_a_idx,
@@ -104,7 +106,8 @@ struct pbg_context {
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
         child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
     DevBuf items[2][8];
-    DevBuf run_dst, run_src, run_len, run_rp;
+    DevBuf row_pack;
+    DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
     DevBuf wb[7];
     size_t zero_bytes = 0;
     cudaEvent_t ev[8] = {};
@@ -126,7 +129,9 @@ struct pbg_context {
         for (auto& set : items)
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
-        for (DevBuf* b : {&run_dst, &run_src, &run_len, &run_rp}) b->release();
+        for (DevBuf* b : {&row_pack, &va_colptr, &va_rowids, &va_vals,
+                          &vcolflop, &bcuts, &vstat})
+            b->release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
     }
@@ -271,18 +276,30 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         A.ptr, B.ptr, k, sc + S_FLOP_LO, sc + S_FLOP_HI);
     ++L;
     if (m > 0) {
-        CUDA_TRY(cudaMemsetAsync(row_flop, 0, m * 8, st));
-        if (k > 0) {
-            k_rowflop<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, B.ptr, k, row_flop);
-            ++L;
+        ctx->rowflop32 = B.nnz < (1ull << 32);
+        CUDA_TRY(cudaMemsetAsync(row_flop, 0, m * (ctx->rowflop32 ? 4 : 8), st));
+        if (ctx->rowflop32) {
+            auto* rf32 = reinterpret_cast<uint32_t*>(row_flop);
+            if (k > 0) {
+                k_rowflop<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, B.ptr, k, rf32);
+                ++L;
+            }
+            launch_scan(ArrayIn32{rf32}, row_off, m, nullptr, m, stat_m1, tickets + 1, nullptr,
+                        sc + S_MAXROW, st);
+            k_binflags<<<blocks_for(m, 256), 256, 0, st>>>(rf32, row_off, m, BinParams{cap, maxr},
+                                                           sc + S_MAXROW, flags);
+        } else {
+            if (k > 0) {
+                k_rowflop<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, B.ptr, k, row_flop);
+                ++L;
+            }
+            launch_scan(ArrayIn{reinterpret_cast<const uint64_t*>(row_flop)}, row_off, m, nullptr,
+                        m, stat_m1, tickets + 1, nullptr, sc + S_MAXROW, st);
+            k_binflags<<<blocks_for(m, 256), 256, 0, st>>>(
+                reinterpret_cast<const uint64_t*>(row_flop), row_off, m, BinParams{cap, maxr},
+                sc + S_MAXROW, flags);
         }
-        launch_scan(ArrayIn{reinterpret_cast<const uint64_t*>(row_flop)}, row_off, m, nullptr, m,
-                    stat_m1, tickets + 1, nullptr, sc + S_MAXROW, st);
-        ++L;
-        k_binflags<<<blocks_for(m, 256), 256, 0, st>>>(reinterpret_cast<const uint64_t*>(row_flop),
-                                                       row_off, m, BinParams{cap, maxr},
-                                                       sc + S_MAXROW, flags);
-        ++L;
+        L += 2;
         launch_scan(ArrayIn{flags}, flags, m, nullptr, m, stat_m2, tickets + 2, sc + S_NBINS,
                     nullptr, st);
         ++L;
@@ -290,7 +307,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         k_binsizes<<<blocks_for(m, 256), 256, 0, st>>>(
             bin_rs, row_off, reinterpret_cast<const uint64_t*>(sc + S_NBINS), cap, bin_cnt,
-            bin_off, cursor, sc + S_HEAVY, sc + S_MAXBIN);
+            bin_off, sc + S_HEAVY, sc + S_MAXBIN);
         ++L;
         launch_scan(ArrayIn{bin_off}, bin_off, 0, reinterpret_cast<const uint64_t*>(sc + S_NBINS),
                     m, stat_m3, tickets + 3, sc + S_TUPLE_CAP, nullptr, st);
@@ -314,7 +331,6 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     ctx->rep.bin_cap = static_cast<uint32_t>(cap);
     if (flop != hs[S_FLOP_LO]) return fail(PBG_ERR_INTERNAL, "flop scan and reduction disagree");
     const uint64_t nb = hs[S_NBINS];
-    (void)nb;
     const uint64_t tcap = hs[S_TUPLE_CAP];
     ctx->rep.tuple_bytes = tcap * 12;
 
@@ -341,6 +357,51 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         auto* vals = static_cast<double*>(ctx->vals.p);
 
         // ---- expand (pb_spgemm.cpp:180-258) ----
+        // row-banded when the bins' write frontier would overflow L2
+        // (k_band_*: ~384 B of partially written lines per bin)
+#ifndef PBG_FRONTIER_BYTES
+#define PBG_FRONTIER_BYTES (40ull << 20)
+#endif
+        int g = static_cast<int>(std::min<uint64_t>(16, (nb * 384 + PBG_FRONTIER_BYTES - 1) / PBG_FRONTIER_BYTES));
+        if (cfg.reserved[1]) g = static_cast<int>(cfg.reserved[1]);  // test hook
+        if (const char* e = getenv("PBG_EXPAND_BANDS")) g = atoi(e);  // tuning hook
+        if (g < 1) g = 1;
+        if (static_cast<uint64_t>(g) > nb) g = static_cast<int>(nb);
+        const uint64_t* xa_colptr = A.ptr;
+        const uint32_t* xa_rowids = A.idx;
+        const double* xa_vals = A.val;
+        const uint64_t* xcolflop = colflop_off;
+        uint64_t kv = k;
+        if (g > 1) {
+            kv = k * static_cast<uint64_t>(g);
+            if ((rc = grow(ctx->bcuts, (g + 1) * 4))) return rc;
+            if ((rc = grow(ctx->va_colptr, (kv + 2) * 8))) return rc;
+            if ((rc = grow(ctx->vcolflop, (kv + 2) * 8))) return rc;
+            if ((rc = grow(ctx->va_rowids, (nnz_a + 1) * 4))) return rc;
+            if ((rc = grow(ctx->va_vals, (nnz_a + 1) * 8))) return rc;
+            const uint64_t vt = (kv + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+            if ((rc = grow(ctx->vstat, (2 * vt + 16) * 8))) return rc;
+            auto* bc = static_cast<uint32_t*>(ctx->bcuts.p);
+            auto* vcp = static_cast<uint64_t*>(ctx->va_colptr.p);
+            auto* vcf = static_cast<uint64_t*>(ctx->vcolflop.p);
+            auto* vst = static_cast<unsigned long long*>(ctx->vstat.p);
+            CUDA_TRY(cudaMemsetAsync(vst, 0, (2 * vt + 16) * 8, st));
+            k_band_cuts<<<1, 32, 0, st>>>(bin_rs, reinterpret_cast<const uint64_t*>(sc + S_NBINS), g, bc);
+            k_band_count<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, k, bc, g, vcp);
+            launch_scan(ArrayIn{vcp}, vcp, kv, nullptr, kv, vst + 16, reinterpret_cast<unsigned int*>(vst),
+                        nullptr, nullptr, st);
+            k_band_copy<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, A.val, k, g, vcp,
+                                                            static_cast<uint32_t*>(ctx->va_rowids.p),
+                                                            static_cast<double*>(ctx->va_vals.p));
+            launch_scan(VColFlopIn{vcp, B.ptr, k}, vcf, kv, nullptr, kv, vst + 16 + vt,
+                        reinterpret_cast<unsigned int*>(vst) + 2, nullptr, nullptr, st);
+            L += 5;
+            xa_colptr = vcp;
+            xa_rowids = static_cast<const uint32_t*>(ctx->va_rowids.p);
+            xa_vals = static_cast<const double*>(ctx->va_vals.p);
+            xcolflop = vcf;
+        }
+        ctx->rep.expand_bands = static_cast<uint32_t>(g);
         const unsigned exp_blocks = 8u * ctx->num_sms;
         const uint64_t warps = static_cast<uint64_t>(exp_blocks) * EXP_NW;
         uint64_t ch = 256;
@@ -348,30 +409,31 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         const uint64_t nchunks = (flop + ch - 1) / ch;
         if ((rc = grow(ctx->chunk_p0, (nchunks + 1) * 8))) return rc;
         auto* chunk_p0 = static_cast<uint64_t*>(ctx->chunk_p0.p);
-        k_chunks<<<blocks_for(nchunks + 1, 256), 256, 0, st>>>(colflop_off, A.ptr, B.ptr, k,
+        k_chunks<<<blocks_for(nchunks + 1, 256), 256, 0, st>>>(xcolflop, xa_colptr, B.ptr, kv, k,
                                                               nnz_a, ch, nchunks, chunk_p0);
         ++L;
-        ExpandArgs ea{A.ptr, A.idx,  A.val,   B.ptr,   B.idx, B.val, k,   chunk_p0, nchunks,
-                      row_bin, bin_rs, bin_off, cursor, keys, vals, cb};
-#ifndef PBG_EXP_SPLIT
-#define PBG_EXP_SPLIT 0
-#endif
-        if (PBG_EXP_SPLIT) {
-            if ((rc = grow(ctx->run_dst, (nnz_a + 1) * 8))) return rc;
-            if ((rc = grow(ctx->run_src, (nnz_a + 1) * 8))) return rc;
-            if ((rc = grow(ctx->run_len, (nnz_a + 1) * 4))) return rc;
-            if ((rc = grow(ctx->run_rp, (nnz_a + 1) * 4))) return rc;
-            ea.run_dst = static_cast<uint64_t*>(ctx->run_dst.p);
-            ea.run_src = static_cast<uint64_t*>(ctx->run_src.p);
-            ea.run_len = static_cast<uint32_t*>(ctx->run_len.p);
-            ea.run_rp = static_cast<uint32_t*>(ctx->run_rp.p);
-            k_runs<<<blocks_for(k, 256), 256, 0, st>>>(ea);
-            k_expand_runs<<<exp_blocks, EXP_NT, 0, st>>>(ea);
-            L += 2;
+        // bin cursors start at the bins' offsets (atomicAdd returns the slot)
+        CUDA_TRY(cudaMemcpyAsync(cursor, bin_off, nb * 8, cudaMemcpyDeviceToDevice, st));
+        int lbits = 0;
+        while ((1ull << lbits) < maxr) ++lbits;
+        const bool pack32 = nb < (1ull << (32 - lbits));
+        if ((rc = grow(ctx->row_pack, (m + 1) * (pack32 ? 4 : 8)))) return rc;
+        ExpandArgs ea{xa_colptr, xa_rowids, xa_vals, B.ptr, B.idx, B.val, kv, k, chunk_p0, nchunks,
+                      ctx->row_pack.p, lbits, cursor, keys, vals, cb};
+        if (pack32) {
+            k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
+                                                         static_cast<uint32_t*>(ctx->row_pack.p));
+            k_expand<uint32_t><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         } else {
-            k_expand<<<exp_blocks, EXP_NT, 0, st>>>(ea);
-            ++L;
+            k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
+                                                         static_cast<uint64_t*>(ctx->row_pack.p));
+            k_expand<uint64_t><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         }
+        L += 2;
+#if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE)
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return fail(PBG_ERR_INTERNAL, "diagnostic build: stopped after the expand");
+#endif
         CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
 
         // ---- work bins: regular bins + the key-range pieces of heavy rows ----
@@ -479,7 +541,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         auto* wb_nnz = static_cast<uint64_t*>(ctx->wb_nnz.p);
         auto* wb_out = static_cast<uint64_t*>(ctx->wb_out.p);
         k_work_count<<<blocks_for(m + 1, 256), 256, 0, st>>>(
-            nb_dev, bin_hidx, hcount, cursor, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
+            nb_dev, bin_hidx, hcount, cursor, bin_off, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
             reinterpret_cast<unsigned int*>(sc + S_ERR));
         launch_scan(ArrayIn{wcnt}, wpos, 0, nb_dev, m, stat_m7, tickets + 8, sc + S_NWORK,
                     nullptr, st);
@@ -892,7 +954,15 @@ int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg_in, uint64_t* p
     }
     if (!per_bin_flop && !bin_row_starts) return PBG_OK;
     std::vector<uint64_t> rf(m);
-    if (m && ctx->flop) CUDA_TRY(cudaMemcpy(rf.data(), ctx->row_flop.p, m * 8, cudaMemcpyDeviceToHost));
+    if (m && ctx->flop) {
+        if (ctx->rowflop32) {
+            std::vector<uint32_t> r32(m);
+            CUDA_TRY(cudaMemcpy(r32.data(), ctx->row_flop.p, m * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t r = 0; r < m; ++r) rf[r] = r32[r];
+        } else {
+            CUDA_TRY(cudaMemcpy(rf.data(), ctx->row_flop.p, m * 8, cudaMemcpyDeviceToHost));
+        }
+    }
     return reference_layout(cfg, ctx->rep.nbins, rf, {}, nullptr, per_bin_flop, bin_row_starts,
                             ctx->flop, ctx->col_bits);
 }

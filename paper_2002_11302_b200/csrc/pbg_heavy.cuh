@@ -273,6 +273,7 @@ __global__ void k_heavy_heads(const uint32_t* __restrict__ item_h, uint64_t nite
 __global__ void k_work_count(const uint64_t* nb_dev, const uint32_t* __restrict__ bin_hidx,
                              const uint32_t* __restrict__ hcount,
                              const unsigned long long* __restrict__ cursor,
+                             const uint64_t* __restrict__ bin_off,
                              const uint64_t* __restrict__ bin_cnt, uint64_t* wcnt,
                              unsigned long long* tuples_total, unsigned int* err) {
     const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -280,7 +281,7 @@ __global__ void k_work_count(const uint64_t* nb_dev, const uint32_t* __restrict_
     if (b < *nb_dev) {
         const uint32_t h = bin_hidx[b];
         wcnt[b] = h == 0xffffffffu ? 1 : hcount[h];
-        cur = cursor[b];
+        cur = cursor[b] - bin_off[b];  // cursors start at the bin's offset
         if (cur != bin_cnt[b]) atomicOr(err, 1u);
     }
     cur = warp_sum(cur);

@@ -121,6 +121,10 @@ struct ArrayIn {
     const uint64_t* a;
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
 };
+struct ArrayIn32 {
+    const uint32_t* a;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
+};
 
 // 128-bit accumulation of the per-column flop so an overflow of the 64-bit
 // total is detected exactly (pb_spgemm.cpp:103-105). also rejects totals the
@@ -157,11 +161,14 @@ __global__ void k_colflop_total(const uint64_t* __restrict__ a_colptr,
 
 // row_flop[r] += nnz(B(k,:)) for every A(r,k)  (bin_flop / balanced_starts,
 // pb_spgemm.cpp:36-82, at row granularity). Thread per column; long columns
-// are walked by the whole warp.
+// are walked by the whole warp. Counters are 32-bit whenever nnz(B) < 2^32
+// (a row's flop never exceeds nnz(B)): half the scattered-RED footprint, so
+// the m counters stay L2-resident for larger m.
+template <typename T>
 __global__ void k_rowflop(const uint64_t* __restrict__ a_colptr,
                           const uint32_t* __restrict__ a_rowids,
                           const uint64_t* __restrict__ b_rowptr, uint64_t k,
-                          unsigned long long* row_flop) {
+                          T* row_flop) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     uint64_t p0 = 0, p1 = 0, lb = 0;
@@ -174,7 +181,7 @@ __global__ void k_rowflop(const uint64_t* __restrict__ a_colptr,
     }
     const bool longcol = (p1 - p0) > 64;
     if (!longcol)
-        for (uint64_t p = p0; p < p1; ++p) atomicAdd(&row_flop[a_rowids[p]], (unsigned long long)lb);
+        for (uint64_t p = p0; p < p1; ++p) atomicAdd(&row_flop[a_rowids[p]], static_cast<T>(lb));
     uint32_t lm = __ballot_sync(FULL, longcol);
     while (lm) {
         const int src = __ffs(lm) - 1;
@@ -182,7 +189,7 @@ __global__ void k_rowflop(const uint64_t* __restrict__ a_colptr,
         const uint64_t q0 = __shfl_sync(FULL, p0, src), q1 = __shfl_sync(FULL, p1, src);
         const uint64_t qb = __shfl_sync(FULL, lb, src);
         for (uint64_t p = q0 + lane; p < q1; p += 32)
-            atomicAdd(&row_flop[a_rowids[p]], (unsigned long long)qb);
+            atomicAdd(&row_flop[a_rowids[p]], static_cast<T>(qb));
     }
 }
 
@@ -195,7 +202,8 @@ struct BinParams {
     uint32_t maxr;  // rows per bin (2^(32-col_bits), <= 1024)
 };
 
-__global__ void k_binflags(const uint64_t* __restrict__ row_flop,
+template <typename T>
+__global__ void k_binflags(const T* __restrict__ row_flop,
                            const uint64_t* __restrict__ row_off, uint64_t m, BinParams bp,
                            const unsigned long long* max_row_flop, uint64_t* flags) {
     const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -225,12 +233,23 @@ __global__ void k_binrows(const uint64_t* __restrict__ flag_excl, uint64_t m, ui
     if (r == m - 1) bin_rs[e1] = static_cast<uint32_t>(m);
 }
 
+// row -> bin << lbits | (row - bin row start): the expand's single dependent
+// lookup per run (u32 when nbins < 2^(32 - lbits), else u64).
+template <typename P>
+__global__ void k_rowpack(const uint32_t* __restrict__ row_bin,
+                          const uint32_t* __restrict__ bin_rs, uint64_t m, int lbits, P* pack) {
+    const uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const uint32_t b = row_bin[r];
+    pack[r] = (static_cast<P>(b) << lbits) | static_cast<P>(r - bin_rs[b]);
+}
+
 // Per-bin tuple count, 4-tuple padded capacity (16-B aligned key runs),
-// cursor reset, heavy-bin count.
+// heavy-bin count.
 __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
                            const uint64_t* __restrict__ row_off, const uint64_t* nb_dev,
                            uint64_t cap, uint64_t* bin_cnt, uint64_t* bin_pad,
-                           unsigned long long* cursor, unsigned long long* heavy,
+                           unsigned long long* heavy,
                            unsigned long long* maxbin) {
     const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     uint64_t c = 0;
@@ -238,7 +257,6 @@ __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
         c = row_off[bin_rs[b + 1]] - row_off[bin_rs[b]];
         bin_cnt[b] = c;
         bin_pad[b] = (c + 3) & ~3ull;
-        cursor[b] = 0;
     }
     // warp-aggregated: one atomic per warp instead of one per bin
     const uint32_t nh = __popc(__ballot_sync(FULL, c > cap));
@@ -257,10 +275,12 @@ __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
 // ---------------------------------------------------------------- expand --
 // Chunk c owns the runs (A entries) whose tuple range starts in
 // [c*CH, (c+1)*CH); chunk_p0[c] is its first A entry.
+// With row-banded expand (k_band_*), A's columns are virtual: v = band * kb
+// + j, and B's row for v is j = v % kb (kb = A's real column count).
 __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
                          const uint64_t* __restrict__ a_colptr,
-                         const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t nnz_a,
-                         uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0) {
+                         const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t kb,
+                         uint64_t nnz_a, uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0) {
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (c > nchunks) return;
     if (c == nchunks) {
@@ -269,7 +289,8 @@ __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
     }
     const uint64_t t0 = c * ch;
     const uint64_t col = last_le(colflop_off, 0, k, t0);  // off[col] <= t0 < off[col+1]
-    const uint64_t lb = b_rowptr[col + 1] - b_rowptr[col];
+    const uint64_t bj = col % kb;
+    const uint64_t lb = b_rowptr[bj + 1] - b_rowptr[bj];
     const uint64_t rel = t0 - colflop_off[col];
     const uint64_t i = (rel + lb - 1) / lb;
     chunk_p0[c] = a_colptr[col] + i;
@@ -282,21 +303,16 @@ struct ExpandArgs {
     const uint64_t* b_rowptr;
     const uint32_t* b_colids;
     const double* b_vals;
-    uint64_t a_ncols;
+    uint64_t a_ncols;   // (virtual) columns of A
+    uint64_t b_rows;    // real columns of A = rows of B (virtual column v reads B row v % b_rows)
     const uint64_t* chunk_p0;
     uint64_t nchunks;
-    const uint32_t* row_bin;
-    const uint32_t* bin_rs;
-    const uint64_t* bin_off;
-    unsigned long long* cursor;
+    const void* row_pack;          // per row: bin << lbits | (row - bin row start), u32 or u64
+    int lbits;
+    unsigned long long* cursor;    // per bin: next free tuple slot (absolute)
     uint32_t* keys;
     double* vals;
     int col_bits;
-    // run plan (k_runs -> k_expand_runs): one entry per A entry
-    uint64_t* run_dst;  // tuple offset reserved in the row's bin
-    uint64_t* run_src;  // first entry of B(k,:)
-    uint32_t* run_len;  // nnz(B(k,:))
-    uint32_t* run_rp;   // (row - bin_row_start) << col_bits
 };
 
 constexpr int EXP_NT = 256;
@@ -350,6 +366,7 @@ constexpr int EXP_NW = EXP_NT / 32;
 #ifndef PBG_EXP_MINB
 #define PBG_EXP_MINB 4
 #endif
+template <typename P>
 __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
     __shared__ uint64_t s_dst[EXP_NW][32];
     __shared__ uint64_t s_bst[EXP_NW][32];
@@ -364,12 +381,23 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
 
     for (uint64_t c = gw; c < a.nchunks; c += nw) {
         uint64_t p = a.chunk_p0[c];
+#ifdef PBG_DIAG_SEQSTORE
+        uint64_t tpos = c * 8192;  // timing experiment only (wrong output)
+#endif
         const uint64_t pend = a.chunk_p0[c + 1];
         if (p >= pend) continue;
         uint64_t kcur = warp_last_le(a.a_colptr, 0, a.a_ncols, p);
         while (p < pend) {
             const uint64_t pl = p + lane;
             const bool valid = pl < pend;
+            // the run's row, value and packed bin are independent of its
+            // column: issued first so their latency overlaps the search
+            P pack = 0;
+            double av = 0.0;
+            if (valid) {
+                av = a.a_vals[pl];
+                pack = static_cast<const P*>(a.row_pack)[a.a_rowids[pl]];
+            }
             // column of run pl: kcur + #{j : colptr[kcur+1+j] <= pl}
             const uint64_t bi = kcur + 1 + lane;
             const uint64_t bnd = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
@@ -387,22 +415,14 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
             if (valid && cnt == 32) kl = last_le(a.a_colptr, kcur, a.a_ncols, pl);
             uint64_t lb = 0, bst = 0, dst = 0;
             uint32_t rp = 0;
-            double av = 0.0;
             if (valid) {
-                bst = a.b_rowptr[kl];
-                lb = a.b_rowptr[kl + 1] - bst;
+                const uint64_t bj = kl < a.b_rows ? kl : kl % a.b_rows;
+                bst = a.b_rowptr[bj];
+                lb = a.b_rowptr[bj + 1] - bst;
                 if (lb) {
-                    const uint32_t r = a.a_rowids[pl];
-                    av = a.a_vals[pl];
-                    const uint32_t bin = a.row_bin[r];
-                    const uint32_t rs = a.bin_rs[bin];
-#ifdef PBG_DIAG_NOATOMIC
-                    const uint64_t pos = 0;  // timing experiment only (wrong output)
-#else
-                    const uint64_t pos = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
-#endif
-                    dst = a.bin_off[bin] + pos;
-                    rp = static_cast<uint32_t>((static_cast<uint64_t>(r - rs)) << cb);
+                    const P bin = pack >> a.lbits;
+                    dst = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
+                    rp = static_cast<uint32_t>(pack & ((P(1) << a.lbits) - 1)) << cb;
                 }
             }
             const bool ne = lb != 0;
@@ -445,7 +465,11 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
                     bv[u] = ok[u] ? __ldg(a.b_vals + src) : 0.0;
                     rpv[u] = s_rp[w][ri];
                     avv[u] = s_av[w][ri];
+#ifdef PBG_DIAG_SEQSTORE
+                    dv[u] = (tpos + t) % (1ull << 28);
+#else
                     dv[u] = s_dst[w][ri] + q;
+#endif
                     before += __popc(mk);
                 }
 #pragma unroll
@@ -465,135 +489,79 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
             const int last = (pend - p) < 32 ? static_cast<int>(pend - p) - 1 : 31;
             kcur = __shfl_sync(FULL, kl, last);
             p += 32;
+#ifdef PBG_DIAG_SEQSTORE
+            tpos += total;
+#endif
         }
     }
 }
 
 
-// ----------------------------------------------------- expand, split form --
-// Phase 1 (k_runs): one thread per column k of A (the whole warp for long
-// columns) walks A(:,k): every A entry p is a run of nnz(B(k,:)) tuples into
-// its row's bin; the run's slots are reserved with one atomicAdd on the bin
-// cursor (the reference's `omp atomic capture`, pb_spgemm.cpp:196-214) and
-// the run plan (destination, B source, length, key row part) is stored.
-// Massively parallel and independent per run, so the dependent loads
-// (row -> bin -> cursor) of 16 M runs overlap across threads instead of
-// serialising inside the tuple-streaming warps.
-__global__ void __launch_bounds__(256) k_runs(ExpandArgs a) {
-    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    uint64_t p0 = 0, p1 = 0, lb = 0, bst = 0;
-    if (i < a.a_ncols) {
-        p0 = a.a_colptr[i];
-        p1 = a.a_colptr[i + 1];
-        bst = a.b_rowptr[i];
-        lb = a.b_rowptr[i + 1] - bst;
+
+// ------------------------------------------------------- row-banded expand --
+// The expand's write frontier is one partially filled line per bin array;
+// with ~10^5 bins it no longer fits the 126 MB L2 and half-written sectors are
+// evicted (DRAM read-modify-write). Expanding G row bands one after another
+// (A re-ordered band-major: virtual column v = band * k + j holds A(band
+// rows, j)) keeps only nbins/G bins active at a time. Bands are unions of
+// whole bins, so bins, offsets and cursors are unchanged.
+struct VColFlopIn {
+    const uint64_t* va_colptr;
+    const uint64_t* b_rowptr;
+    uint64_t kb;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+        const uint64_t j = v % kb;
+        return (va_colptr[v + 1] - va_colptr[v]) * (b_rowptr[j + 1] - b_rowptr[j]);
     }
-    const int cb = a.col_bits;
-    auto one = [&](uint64_t p, uint64_t len, uint64_t src) {
-        a.run_len[p] = static_cast<uint32_t>(len);
-        if (!len) return;
-        const uint32_t r = a.a_rowids[p];
-        const uint32_t bin = a.row_bin[r];
-        const uint64_t pos = atomicAdd(&a.cursor[bin], (unsigned long long)len);
-        a.run_dst[p] = a.bin_off[bin] + pos;
-        a.run_src[p] = src;
-        a.run_rp[p] = static_cast<uint32_t>(static_cast<uint64_t>(r - a.bin_rs[bin]) << cb);
-    };
-    const bool longcol = (p1 - p0) > 32;
-    if (!longcol)
-        for (uint64_t p = p0; p < p1; ++p) one(p, lb, bst);
-    uint32_t lm = __ballot_sync(FULL, longcol);
-    while (lm) {
-        const int src = __ffs(lm) - 1;
-        lm &= lm - 1;
-        const uint64_t q0 = __shfl_sync(FULL, p0, src), q1 = __shfl_sync(FULL, p1, src);
-        const uint64_t qb = __shfl_sync(FULL, lb, src), qs = __shfl_sync(FULL, bst, src);
-        for (uint64_t p = q0 + lane; p < q1; p += 32) one(p, qb, qs);
+};
+
+// count[v = s*k + j] = #A(:,j) entries with rows in band s
+__global__ void k_band_count(const uint64_t* __restrict__ a_colptr,
+                             const uint32_t* __restrict__ a_rowids, uint64_t k,
+                             const uint32_t* __restrict__ cuts, int g, uint64_t* vcnt) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
+    uint64_t lo = p0;
+    for (int s = 0; s < g; ++s) {
+        const uint32_t r1 = cuts[s + 1];
+        uint64_t l = lo, h = p1;  // first p in [lo, p1) with rowid >= r1
+        while (l < h) {
+            const uint64_t mid = (l + h) >> 1;
+            if (a_rowids[mid] < r1) l = mid + 1;
+            else h = mid;
+        }
+        vcnt[static_cast<uint64_t>(s) * k + j] = l - lo;
+        lo = l;
     }
 }
 
-// Phase 2 (k_expand_runs): one warp per chunk of runs; 32 runs per batch,
-// their plans read coalesced, lengths scanned, then the batch's tuples are
-// streamed flat (EXP_U steps of 32 in flight per lane).
-__global__ void __launch_bounds__(EXP_NT) k_expand_runs(ExpandArgs a) {
-    __shared__ uint64_t s_dst[EXP_NW][32];
-    __shared__ uint64_t s_bst[EXP_NW][32];
-    __shared__ double s_av[EXP_NW][32];
-    __shared__ uint64_t s_st[EXP_NW][32];
-    __shared__ uint32_t s_rp[EXP_NW][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t lt = lanemask_lt();
-    for (uint64_t c = gw; c < a.nchunks; c += nw) {
-        const uint64_t pend = a.chunk_p0[c + 1];
-        for (uint64_t p = a.chunk_p0[c]; p < pend; p += 32) {
-            const uint64_t pl = p + lane;
-            const uint64_t lb = pl < pend ? a.run_len[pl] : 0;
-            const bool ne = lb != 0;
-            uint64_t dst = 0, bst = 0;
-            uint32_t rp = 0;
-            double av = 0.0;
-            if (ne) {
-                dst = a.run_dst[pl];
-                bst = a.run_src[pl];
-                rp = a.run_rp[pl];
-                av = a.a_vals[pl];
-            }
-            const uint32_t nemask = __ballot_sync(FULL, ne);
-            const int rank = __popc(nemask & lt);
-            const uint64_t incl = warp_inclusive_scan(lb);
-            const uint64_t start = incl - lb;
-            const uint64_t total = __shfl_sync(FULL, incl, 31);
-            __syncwarp();
-            if (ne) {
-                s_dst[w][rank] = dst;
-                s_bst[w][rank] = bst;
-                s_av[w][rank] = av;
-                s_st[w][rank] = start;
-                s_rp[w][rank] = rp;
-            }
-            __syncwarp();
-            uint32_t before = 0;
-            for (uint64_t s0 = 0; s0 < total; s0 += 32 * EXP_U) {
-                uint32_t kv[EXP_U];
-                double bv[EXP_U], avv[EXP_U];
-                uint32_t rpv[EXP_U];
-                uint64_t dv[EXP_U];
-                bool ok[EXP_U];
-#pragma unroll
-                for (int u = 0; u < EXP_U; ++u) {
-                    const uint64_t s = s0 + 32 * u;
-                    const uint32_t bit =
-                        (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
-                    const uint32_t mk = __reduce_or_sync(FULL, bit);
-                    const uint64_t t = s + lane;
-                    ok[u] = t < total;
-                    const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-                    int ri = static_cast<int>(before + __popc(mk & upto)) - 1;
-                    ri = ok[u] ? ri : 0;
-                    const uint64_t q = t - s_st[w][ri];
-                    const uint64_t src = s_bst[w][ri] + q;
-                    kv[u] = ok[u] ? __ldg(a.b_colids + src) : 0u;
-                    bv[u] = ok[u] ? __ldg(a.b_vals + src) : 0.0;
-                    rpv[u] = s_rp[w][ri];
-                    avv[u] = s_av[w][ri];
-                    dv[u] = s_dst[w][ri] + q;
-                    before += __popc(mk);
-                }
-#pragma unroll
-                for (int u = 0; u < EXP_U; ++u) {
-                    if (ok[u]) {
-                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u]);
-                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u]);
-                    }
-                }
-            }
-            __syncwarp();
+__global__ void k_band_copy(const uint64_t* __restrict__ a_colptr,
+                            const uint32_t* __restrict__ a_rowids,
+                            const double* __restrict__ a_vals, uint64_t k, int g,
+                            const uint64_t* __restrict__ va_colptr, uint32_t* va_rowids,
+                            double* va_vals) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    uint64_t p = a_colptr[j];
+    for (int s = 0; s < g; ++s) {
+        const uint64_t v = static_cast<uint64_t>(s) * k + j;
+        const uint64_t d0 = va_colptr[v], d1 = va_colptr[v + 1];
+        for (uint64_t d = d0; d < d1; ++d, ++p) {
+            va_rowids[d] = a_rowids[p];
+            va_vals[d] = a_vals[p];
         }
     }
 }
+
+__global__ void k_band_cuts(const uint32_t* __restrict__ bin_rs, const uint64_t* nb_dev, int g,
+                            uint32_t* cuts) {
+    const int s = threadIdx.x;
+    if (s > g) return;
+    const uint64_t nb = *nb_dev;
+    cuts[s] = bin_rs[(nb * static_cast<uint64_t>(s)) / g];
+}
+
 
 __global__ void k_zero_u64(uint64_t* p, uint64_t n) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;

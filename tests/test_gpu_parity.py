@@ -150,6 +150,18 @@ def test_row_bands_assemble_to_full_product():
                        full.c.values)
 
 
+def test_expand_row_bands_invariant():
+    """Row-banded expand (forced 1..5 bands) gives the same product."""
+    csr = M.make_matrix("er", 13, 8, seed=5)
+    a = M.csr_to_csc(csr)
+    base = gpu(a, csr, expand_bands=1)
+    for g in (2, 3, 5):
+        r = gpu(a, csr, expand_bands=g)
+        assert r.report["expand_bands"] == g
+        assert_csr_matches(r.c.rowptr, r.c.colids, r.c.values, base.c.rowptr, base.c.colids,
+                           base.c.values)
+
+
 def test_bounded_memory_rounds_match_single_pass():
     """Forced row-band rounds (host path) give the single-pass product and
     the same reference-layout symbolic report."""
