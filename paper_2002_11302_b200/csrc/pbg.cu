@@ -86,6 +86,7 @@ enum Scalar : int {
     S_ERR,             // error bits (u32 in low word)
     S_FALLBACKS,       // bins sorted by the LSD fallback
     S_NNZ,             // nnz(C) from the distinct-count scan
+    S_TILES,           // split tiles of the current heavy level
     S_HEAVY_PAD,       // padded tuples of heavy rows (scratch size)
     S_ITEMS,           // heavy-row items after a split pass
     S_NWORK,           // work bins
@@ -106,7 +107,7 @@ struct pbg_context {
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
         child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
     DevBuf items[2][8];
-    DevBuf row_pack;
+    DevBuf row_pack, tile_pos, tile_item, hv_hist;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
     DevBuf wb[7];
     size_t zero_bytes = 0;
@@ -129,7 +130,7 @@ struct pbg_context {
         for (auto& set : items)
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
-        for (DevBuf* b : {&row_pack, &va_colptr, &va_rowids, &va_vals,
+        for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &va_colptr, &va_rowids, &va_vals,
                           &vcolflop, &bcuts, &vstat})
             b->release();
         if (ev_ok)
@@ -493,31 +494,63 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             hc.skeys = static_cast<uint32_t*>(ctx->skeys.p);
             hc.svals = static_cast<double*>(ctx->svals.p);
             nitems = H;
-            const int npass = (cb + HV_DBITS - 1) / HV_DBITS;
-            for (int pass = 0; pass < npass; ++pass) {
+            static bool hv_attr[64] = {};
+            if (!hv_attr[ctx->device & 63]) {
+                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(sizeof(HvScatterSmem))));
+                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter,
+                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                hv_attr[ctx->device & 63] = true;
+            }
+            // split levels (all SPLIT items of a level share sh); usually one
+            for (int sh = cb; sh > HV_DENSE_BITS;) {
+                const int d = hv_digit(sh);
+                const uint64_t nbk = 1ull << d;
                 if ((rc = grow(ctx->child_cnt, (nitems + 1) * 8))) return rc;
                 if ((rc = grow(ctx->child_pos, (nitems + 2) * 8))) return rc;
+                if ((rc = grow(ctx->tile_pos, (nitems + 2) * 8))) return rc;
+                if ((rc = grow(ctx->hv_hist, (nitems + 1) * nbk * 4))) return rc;
                 const uint64_t tiles = (nitems + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-                if ((rc = grow(ctx->hstat, tiles * 8 + 64))) return rc;
+                if ((rc = grow(ctx->hstat, 2 * tiles * 8 + 256))) return rc;
                 auto* ccnt = static_cast<uint64_t*>(ctx->child_cnt.p);
                 auto* cpos = static_cast<uint64_t*>(ctx->child_pos.p);
+                auto* tpos = static_cast<uint64_t*>(ctx->tile_pos.p);
+                auto* hist = static_cast<uint32_t*>(ctx->hv_hist.p);
                 auto* hst = static_cast<unsigned long long*>(ctx->hstat.p);
-                CUDA_TRY(cudaMemsetAsync(hst, 0, tiles * 8 + 64, st));
-                const unsigned g = static_cast<unsigned>(std::min<uint64_t>(nitems, 4ull * ctx->num_sms));
-                k_split_count<<<g, HV_NT, 0, st>>>(hc, cur, nitems, ccnt);
-                launch_scan(ArrayIn{ccnt}, cpos, nitems, nullptr, nitems, hst + 8,
-                            reinterpret_cast<unsigned int*>(hst), sc + S_ITEMS, nullptr, st);
+                CUDA_TRY(cudaMemsetAsync(hst, 0, 2 * tiles * 8 + 256, st));
+                CUDA_TRY(cudaMemsetAsync(hist, 0, nitems * nbk * 4, st));
+                launch_scan(SplitTilesIn{cur.n, cur.kind}, tpos, nitems, nullptr, nitems, hst + 16,
+                            reinterpret_cast<unsigned int*>(hst), sc + S_TILES, nullptr, st);
+                CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaStreamSynchronize(st));
+                const uint64_t ntiles = hs[S_TILES];
+                if (ntiles == 0) break;
+                if ((rc = grow(ctx->tile_item, ntiles * 4))) return rc;
+                auto* titem = static_cast<uint32_t*>(ctx->tile_item.p);
+                k_hv_tilemap<<<blocks_for(nitems * 32, 256), 256, 0, st>>>(tpos, nitems, titem);
+                const unsigned gt = static_cast<unsigned>(std::min<uint64_t>(ntiles, 8ull * ctx->num_sms));
+                k_hv_hist<<<gt, HV_NT, 0, st>>>(hc, cur, nitems, tpos, titem, sh, d, hist);
+                const unsigned gi = static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms));
+                k_hv_plan<<<gi, HV_PT, 0, st>>>(cur, nitems, d, cap, hist, ccnt);
+                launch_scan(ArrayIn{ccnt}, cpos, nitems, nullptr, nitems, hst + 16 + tiles,
+                            reinterpret_cast<unsigned int*>(hst) + 2, sc + S_ITEMS, nullptr, st);
                 CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
                 CUDA_TRY(cudaStreamSynchronize(st));
                 const uint64_t nout = hs[S_ITEMS];
                 Items nxt{};
                 if ((rc = items_of(curset ^ 1, nout, &nxt))) return rc;
-                k_split_scatter<<<g, HV_NT, 0, st>>>(hc, cur, nitems, cpos, nxt);
-                L += 3;
+                k_hv_scatter<<<gt, HV_NT, sizeof(HvScatterSmem), st>>>(hc, cur, nitems, tpos, titem,
+                                                                      sh, d, hist);
+                k_hv_children<<<gi, HV_PT, 0, st>>>(hc, cur, nitems, sh, d, hist, cpos, nxt);
+                L += 7;
                 cur = nxt;
                 curset ^= 1;
                 nitems = nout;
+                sh -= d;
             }
+            k_hv_dense<<<static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms)), HV_NT,
+                         0, st>>>(hc, cur, nitems);
+            ++L;
             CUDA_TRY(cudaMemsetAsync(hcount, 0, H * 4, st));
             k_heavy_heads<<<blocks_for(nitems, 256), 256, 0, st>>>(cur.h, nitems, hhead, hcount);
             ++L;

@@ -48,7 +48,10 @@ constexpr int SM_NW = SM_NT / 32;
 constexpr int SM_CAP = PBG_SM_CAP;            // max tuples per smem bin
 constexpr int SM_NB = SM_CAP;                 // buckets of the MSD pass
 constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
-constexpr int SM_BMAX = 32;                   // largest bucket ranked in place
+#ifndef PBG_SM_BMAX
+#define PBG_SM_BMAX 128
+#endif
+constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
 constexpr int SM_ITEMS = SM_CAP / SM_NT;      // 8
 constexpr int SM_PER_WARP = SM_CAP / SM_NW;
 constexpr int SM_NBUF = 2;                    // ping, pong
@@ -119,7 +122,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 // Thread 0: take the next ticket and, for a work bin that fits, start its
 // copy into buffer `buf` (generic-proxy accesses to it are finished: caller
 // syncs). s_loaded: 1 = TMA copy in flight, 2 = load by hand (unaligned heavy
-// sub-bin), 0 = nothing to load (empty / uniform / error).
+// sub-bin), 0 = nothing to load (empty / merged / error).
 __device__ __forceinline__ void prefetch_next(const SortArgs& a, SortSmem& sm, int buf,
                                               uint64_t nw) {
     const uint64_t b = atomicAdd(a.ticket, 1u);
@@ -450,29 +453,24 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
     if (tid == 0 && b == nw - 1) a.rowptr[a.m] = P + U;
 }
 
-// A uniform-key item (one column hit more than SM_CAP times in a heavy row):
-// its merged entry is the sum of all its values, reduced from global memory
-// in index order per thread, then across the block.
-__device__ __forceinline__ void reduce_uniform(const SortArgs& a, SortSmem& sm, uint64_t b,
-                                               int buf) {
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+// A MERGED heavy sub-bin (k_hv_dense: already sorted, duplicates summed, may
+// exceed SM_CAP): copied from global memory straight to C.
+__device__ void write_merged(const SortArgs& a, uint64_t b, uint64_t nw, uint64_t P, uint32_t U) {
+    const int tid = threadIdx.x;
+    const int cb = a.col_bits;
+    const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
     const uint32_t fl = a.w.flags[b];
-    const uint64_t off = a.w.off[b], n = a.w.n[b];
-    const double* vs = ((fl & 1u) ? a.svals : a.vals) + off;
-    double s = 0.0;
-    for (uint64_t i = tid; i < n; i += SM_NT) s += vs[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    double* red = sm.v[buf] + 8;  // scratch words in the free buffer
-    if (lane == 0) red[w] = s;
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0.0;
-        for (int i = 0; i < SM_NW; ++i) t += red[i];
-        sm.k[buf][0] = ((fl & 1u) ? a.skeys : a.keys)[off];
-        sm.v[buf][0] = t;
+    const uint64_t off = a.w.off[b];
+    const uint32_t* K = ((fl & 1u) ? a.skeys : a.keys) + off;
+    const double* V = ((fl & 1u) ? a.svals : a.vals) + off;
+    for (uint32_t u = tid; u < U; u += SM_NT) {
+        __stcs(a.ccol + P + u, K[u] & colmask);
+        __stcs(a.cval + P + u, V[u]);
     }
-    __syncthreads();
+    if (tid == 0) {
+        if (a.w.span[b]) a.rowptr[a.w.rs[b]] = P;  // single-row sub-bin owning the row start
+        if (b == nw - 1) a.rowptr[a.m] = P + U;
+    }
 }
 
 __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
@@ -499,6 +497,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         if (tid == 0 && n64 > SM_CAP && !(fl & 2u)) atomicOr(a.err, 2u);
         int res = inb;
         uint32_t U = 0;
+        bool merged = false;
         if (loaded) {
             const uint32_t n = static_cast<uint32_t>(n64);
             reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
@@ -518,8 +517,8 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(a.w.keybits[b]),
                                a.w.keylo[b], static_cast<uint32_t>(a.wb_nnz[b]), &res);
         } else if (fl & 2u) {
-            reduce_uniform(a, sm, b, inb);
-            U = 1;
+            U = static_cast<uint32_t>(n64);
+            merged = true;
         }
         __syncthreads();
         // next work bin's copy into the free buffer overlaps this one's output
@@ -528,7 +527,8 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             if (U != a.wb_nnz[b]) atomicOr(a.err, 4u);
             atomicAdd(a.merged_total, (unsigned long long)U);
         }
-        write_bin(a, sm, res, b, nw, rs, span, U, a.wb_out[b]);
+        if (merged) write_merged(a, b, nw, a.wb_out[b], U);
+        else write_bin(a, sm, res, b, nw, rs, span, U, a.wb_out[b]);
         inb = res ^ 1;
         __syncthreads();
     }
