@@ -516,40 +516,44 @@ struct VColFlopIn {
 };
 
 // count[v = s*k + j] = #A(:,j) entries with rows in band s
+__device__ __forceinline__ int band_of(uint32_t r, const uint32_t* __restrict__ cuts, int g) {
+    int s = 0;
+    while (s + 1 < g && r >= cuts[s + 1]) ++s;
+    return s;
+}
+
+// A(band s rows, j) counts. Row ids inside a column need not be sorted.
 __global__ void k_band_count(const uint64_t* __restrict__ a_colptr,
                              const uint32_t* __restrict__ a_rowids, uint64_t k,
                              const uint32_t* __restrict__ cuts, int g, uint64_t* vcnt) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= k) return;
     const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
-    uint64_t lo = p0;
     for (int s = 0; s < g; ++s) {
-        const uint32_t r1 = cuts[s + 1];
-        uint64_t l = lo, h = p1;  // first p in [lo, p1) with rowid >= r1
-        while (l < h) {
-            const uint64_t mid = (l + h) >> 1;
-            if (a_rowids[mid] < r1) l = mid + 1;
-            else h = mid;
-        }
-        vcnt[static_cast<uint64_t>(s) * k + j] = l - lo;
-        lo = l;
+        uint64_t c = 0;
+        for (uint64_t p = p0; p < p1; ++p) c += band_of(a_rowids[p], cuts, g) == s;
+        vcnt[static_cast<uint64_t>(s) * k + j] = c;
     }
 }
 
+// Band-major copy of A (stable inside each column).
 __global__ void k_band_copy(const uint64_t* __restrict__ a_colptr,
                             const uint32_t* __restrict__ a_rowids,
-                            const double* __restrict__ a_vals, uint64_t k, int g,
+                            const double* __restrict__ a_vals, uint64_t k,
+                            const uint32_t* __restrict__ cuts, int g,
                             const uint64_t* __restrict__ va_colptr, uint32_t* va_rowids,
                             double* va_vals) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= k) return;
-    uint64_t p = a_colptr[j];
+    const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
     for (int s = 0; s < g; ++s) {
-        const uint64_t v = static_cast<uint64_t>(s) * k + j;
-        const uint64_t d0 = va_colptr[v], d1 = va_colptr[v + 1];
-        for (uint64_t d = d0; d < d1; ++d, ++p) {
-            va_rowids[d] = a_rowids[p];
+        uint64_t d = va_colptr[static_cast<uint64_t>(s) * k + j];
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint32_t r = a_rowids[p];
+            if (band_of(r, cuts, g) != s) continue;
+            va_rowids[d] = r;
             va_vals[d] = a_vals[p];
+            ++d;
         }
     }
 }

@@ -160,6 +160,17 @@ def test_expand_row_bands_invariant():
         assert r.report["expand_bands"] == g
         assert_csr_matches(r.c.rowptr, r.c.colids, r.c.values, base.c.rowptr, base.c.colids,
                            base.c.values)
+    # row ids inside A's columns need not be sorted (the reference never
+    # requires it): reverse every column and band again
+    rev = M.CscMatrix(a.nrows, a.ncols, a.colptr, a.rowids.copy(), a.values.copy())
+    for j in range(a.ncols):
+        p0, p1 = int(a.colptr[j]), int(a.colptr[j + 1])
+        rev.rowids[p0:p1] = a.rowids[p0:p1][::-1]
+        rev.values[p0:p1] = a.values[p0:p1][::-1]
+    for g in (1, 3):
+        r = gpu(rev, csr, expand_bands=g)
+        assert_csr_matches(r.c.rowptr, r.c.colids, r.c.values, base.c.rowptr, base.c.colids,
+                           base.c.values)
 
 
 def test_bounded_memory_rounds_match_single_pass():
