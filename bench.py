@@ -9,9 +9,15 @@ n=2^20, d=16), the config BASELINE.json quotes its multiply count on.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
     python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
 
-N>1 (torchrun): output rows are cut into N flop-balanced bands; rank r
-multiplies its CSC row-slab of A by all of B (broadcast once over NCCL at
-setup) with no collective in the timed region ("scaling": "strong").
+N>1 (torchrun), the path shards by output rows with no exchange step:
+  --scaling weak (default): rank r multiplies its own C2-sized row block A_r
+      (the config's generator with seed 1+r) of the row-stacked
+      A = [A_0; ...; A_{N-1}] by the shared B (the seed-1 matrix, built on
+      every rank from the same seed), so per-GPU work is fixed as N grows;
+  --scaling strong: the config's rows are cut into N flop-balanced bands and
+      rank r multiplies its CSC row-slab by all of B (broadcast once over NCCL
+      at setup).
+No collective runs in the timed region; the step time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -200,7 +206,7 @@ def run_reference_arm(args):
         "metric": "SpGEMM mults/sec", "value": res["value"], "unit": "mult/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8d generators)",
         "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}"},
         "impl": "reference",
@@ -219,23 +225,40 @@ def run_gpu_arm(args):
     from paper_2002_11302_b200 import api
 
     ws, rank, local = dist_env()
+    # test hooks: PBG_BENCH_DEVICE pins every rank to one device and
+    # PBG_BENCH_BACKEND=gloo replaces NCCL, so the N>1 control flow can be
+    # exercised on a single GPU (no kernel waits on another rank's kernel)
+    local = int(os.environ.get("PBG_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("PBG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     a_csc, a_csr = build_inputs(args.config)
     n = a_csr.nrows
-    nnz_a = a_csc.nnz
-    # row bands (flop-balanced), rank r owns rows [cuts[r], cuts[r+1])
-    rf = M.row_flop(a_csc, a_csr)
-    if ws > 1:
-        cuts = M.band_cuts(rf, ws)
-        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-        a_band = M.row_band(a_csc, r0, r1)
-    else:
+    weak = ws > 1 and args.scaling == "weak"
+    if weak:
+        # rank r: its own row block A_r of the row-stacked A, times the shared B
+        if rank > 0:
+            a_csc = M.make_config(args.config, seed=1 + rank)[0]
+        rf = M.row_flop(a_csc, a_csr)
         r0, r1 = 0, n
         a_band = a_csc
+    else:
+        # row bands (flop-balanced), rank r owns rows [cuts[r], cuts[r+1])
+        rf = M.row_flop(a_csc, a_csr)
+        if ws > 1:
+            cuts = M.band_cuts(rf, ws)
+            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+            a_band = M.row_band(a_csc, r0, r1)
+        else:
+            r0, r1 = 0, n
+            a_band = a_csc
+    nnz_a = a_band.nnz
     # bounded-memory rounds: a rank whose tuples (+ C upper bound) exceed its
     # HBM budget multiplies its band as R flop-balanced sub-bands per step
     band_flop = int(rf[r0:r1].sum())
@@ -258,7 +281,7 @@ def run_gpu_arm(args):
 
     A_slabs = [(to_dev(s.colptr, np.int64), to_dev(s.rowids, np.int32),
                 to_dev(s.values, np.float64)) for s in slabs]
-    if ws > 1:  # B broadcast once from rank 0 over NCCL (setup, untimed)
+    if ws > 1 and not weak:  # B broadcast once from rank 0 over NCCL (setup, untimed)
         if rank == 0:
             Bt = [to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
                   to_dev(a_csr.values, np.float64)]
@@ -332,11 +355,12 @@ def run_gpu_arm(args):
     t_sym = statistics.mean(r["t_symbolic"] for r in step_reps)
     stats = torch.tensor([t_local, t_sort, t_exp, t_sym, t_count], dtype=torch.float64, device=dev)
     sums = torch.tensor([flop_local, nnz_local, a_band.nnz], dtype=torch.float64, device=dev)
+    nnz_a_local = a_band.nnz
     if ws > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
     t_step, t_sort_max, t_exp_max, t_sym_max, t_count_max = stats.tolist()
-    flop, nnz_c, _ = (int(x) for x in sums.tolist())
+    flop, nnz_c, nnz_a = (int(x) for x in sums.tolist())
 
     # e2e through the public API with host buffers (pinned), N>1: each rank its band
     e2e = None
@@ -381,7 +405,7 @@ def run_gpu_arm(args):
     peak, peak_src = peak_hbm()
     b_exp, b_sort, b_tot = model_bytes(nnz_a, a_csr.nnz, flop, nnz_c)
     # dominant kernel = the longer of expand and sort/merge (rank 0's own band)
-    my_b_exp, my_b_sort, _ = model_bytes(a_band.nnz, a_csr.nnz, flop_local, nnz_local)
+    my_b_exp, my_b_sort, _ = model_bytes(nnz_a_local, a_csr.nnz, flop_local, nnz_local)
     kern = ("k_sortmerge", my_b_sort, t_sort) if t_sort >= t_exp else ("k_expand", my_b_exp, t_exp)
     achieved = kern[1] / kern[2] / 1e9
     traffic = None
@@ -416,14 +440,18 @@ def run_gpu_arm(args):
         "metric": "SpGEMM mults/sec", "value": flop / t_step, "unit": "mult/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if (ws > 1 and not weak) else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded generators of SURVEY.md §8d; no dataset)",
         "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}",
                    "n": n, "nnz_a": nnz_a, "flop": flop, "nnz_c": nnz_c,
                    "model_bytes": b_tot, "model_GBps": b_tot / t_step / 1e9,
                    "model_frac_of_peak_per_gpu": b_tot / t_step / 1e9 / (peak * ws),
                    "l2": "inputs+tuples larger than L2 (tuples alone are 12 B x flop)",
-                   "partition": (f"{ws} flop-balanced row bands" if ws > 1 else "single GPU") +
+                   "partition": ((f"weak: rank r multiplies its own {args.config}-sized row block "
+                                  f"A_r (seed 1+r) of the row-stacked A by the shared B"
+                                  if weak else f"strong: {ws} flop-balanced row bands")
+                                 if ws > 1 else "single GPU") +
                      (f", {rounds} bounded-memory rounds per rank" if rounds > 1 else "")},
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -450,6 +478,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: per-GPU work fixed (weak, default) or total work fixed (strong)")
     ap.add_argument("--max-round-tuples", type=int, default=0,
                     help="force bounded-memory rounds of at most this many mults")
     args = ap.parse_args()
