@@ -38,8 +38,7 @@ def _run(cmd):
 
 
 def build_pbg(force: bool = False) -> Path:
-    deps = [CSRC / "pbg.cu", CSRC / "pbg_kernels.cuh", CSRC / "pbg_sort.cuh", CSRC / "pbg_device.cuh",
-            INCLUDE / "pbg.h"]
+    deps = [CSRC / "pbg.cu", *sorted(CSRC.glob("*.cuh")), INCLUDE / "pbg.h"]
     if force or not _newer(LIBPBG, deps):
         tmp = LIBPBG.with_suffix(".so.tmp")
         _run([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
