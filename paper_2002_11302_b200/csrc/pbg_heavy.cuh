@@ -556,7 +556,10 @@ __global__ void k_work_fill_items(const uint64_t* __restrict__ wpos,
 // a full bin, so probe chains stay short and warps rarely diverge). A scan of
 // these counts gives every work bin its output offset before the sort+merge
 // kernel runs, so bins never wait on each other. Uniform-key items count 1.
-constexpr int CNT_NT = 512;
+#ifndef PBG_CNT_NT
+#define PBG_CNT_NT 512
+#endif
+constexpr int CNT_NT = PBG_CNT_NT;
 #ifndef PBG_CNT_SLOTS_LOG
 #define PBG_CNT_SLOTS_LOG 14
 #endif

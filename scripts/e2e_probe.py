@@ -27,3 +27,20 @@ torch.cuda.synchronize(); t0 = time.perf_counter(); h.copy_(x); torch.cuda.synch
 print("raw D2H GB/s", x.numel() * 8 / (time.perf_counter() - t0) / 1e9)
 t0 = time.perf_counter(); x.copy_(h); torch.cuda.synchronize()
 print("raw H2D GB/s", x.numel() * 8 / (time.perf_counter() - t0) / 1e9)
+# begin / fetch split
+import ctypes as C
+from paper_2002_11302_b200 import _native
+lib = _native.pbg()
+for i in range(3):
+    va = api._view(a.nrows, a.ncols, ah.colptr, ah.rowids, ah.values)
+    vb = api._view(b.nrows, b.ncols, bh.rowptr, bh.colids, bh.values)
+    cc = api.PbConfig().to_c(); h = C.c_void_p(); nz = C.c_uint64(0)
+    t0 = time.perf_counter()
+    rc = lib.pbg_multiply_begin(C.byref(va), C.byref(vb), C.byref(cc), C.byref(h), C.byref(nz))
+    t1 = time.perf_counter()
+    rep = _native.Report()
+    rc2 = lib.pbg_multiply_fetch(h, out[0].ctypes.data, out[1].ctypes.data, out[2].ctypes.data, C.byref(rep))
+    t2 = time.perf_counter()
+    lib.pbg_release(h)
+    t3 = time.perf_counter()
+    print(f"begin {1e3*(t1-t0):.2f} ms fetch {1e3*(t2-t1):.2f} ms release {1e3*(t3-t2):.2f} ms  (h2d {rep.t_h2d*1e3:.2f} total {rep.t_total*1e3:.2f} d2h {rep.t_d2h*1e3:.2f})")
