@@ -832,16 +832,17 @@ int multiply_in_rounds(pbg_handle* h, const pbg_csx_view& a, const pbg_csx_view&
     std::vector<uint64_t> brow;
     for (uint32_t rd = 0; rd < nrounds; ++rd) {
         const uint32_t r0 = cuts[rd], r1 = cuts[rd + 1];
-        // host row slab of A (rows renumbered from 0), pbgh_csc_row_band semantics
+        // host row slab of A (rows renumbered from 0), pbgh_csc_row_band
+        // semantics; row ids inside a column need not be sorted
         si.clear();
         sv.clear();
         sp[0] = 0;
         for (uint64_t j = 0; j < k; ++j) {
-            const uint32_t* lo = std::lower_bound(a.idx + a.ptr[j], a.idx + a.ptr[j + 1], r0);
-            const uint32_t* hi = std::lower_bound(lo, a.idx + a.ptr[j + 1], r1);
-            for (const uint32_t* q = lo; q < hi; ++q) {
-                si.push_back(*q - r0);
-                sv.push_back(a.val[q - a.idx]);
+            for (uint64_t q = a.ptr[j]; q < a.ptr[j + 1]; ++q) {
+                const uint32_t r = a.idx[q];
+                if (r < r0 || r >= r1) continue;
+                si.push_back(r - r0);
+                sv.push_back(a.val[q]);
             }
             sp[j + 1] = si.size();
         }

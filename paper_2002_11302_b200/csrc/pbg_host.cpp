@@ -254,15 +254,13 @@ int pbgh_csc_row_band(uint32_t nrows, uint32_t ncols, const uint64_t* colptr,
                       uint64_t* colptr_out, uint32_t* rowids_out, double* vals_out,
                       uint64_t* nnz_out) {
     if (r0 > r1 || r1 > nrows) return 1;
-    std::vector<uint64_t> lo(ncols), cnt(ncols);
+    // row ids inside a column need not be sorted: filter, keeping their order
+    std::vector<uint64_t> cnt(ncols);
 #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < static_cast<int64_t>(ncols); ++j) {
-        const uint32_t* b = rowids + colptr[j];
-        const uint32_t* e = rowids + colptr[j + 1];
-        const uint32_t* l = std::lower_bound(b, e, r0);
-        const uint32_t* h = std::lower_bound(l, e, r1);
-        lo[j] = static_cast<uint64_t>(l - rowids);
-        cnt[j] = static_cast<uint64_t>(h - l);
+        uint64_t c = 0;
+        for (uint64_t q = colptr[j]; q < colptr[j + 1]; ++q) c += rowids[q] >= r0 && rowids[q] < r1;
+        cnt[j] = c;
     }
     uint64_t total = 0;
     for (uint32_t j = 0; j < ncols; ++j) total += cnt[j];
@@ -270,11 +268,16 @@ int pbgh_csc_row_band(uint32_t nrows, uint32_t ncols, const uint64_t* colptr,
     if (!colptr_out) return 0;
     prefix(cnt, colptr_out);
 #pragma omp parallel for schedule(static)
-    for (int64_t j = 0; j < static_cast<int64_t>(ncols); ++j)
-        for (uint64_t i = 0; i < cnt[j]; ++i) {
-            rowids_out[colptr_out[j] + i] = rowids[lo[j] + i] - r0;
-            vals_out[colptr_out[j] + i] = vals[lo[j] + i];
+    for (int64_t j = 0; j < static_cast<int64_t>(ncols); ++j) {
+        uint64_t o = colptr_out[j];
+        for (uint64_t q = colptr[j]; q < colptr[j + 1]; ++q) {
+            const uint32_t r = rowids[q];
+            if (r < r0 || r >= r1) continue;
+            rowids_out[o] = r - r0;
+            vals_out[o] = vals[q];
+            ++o;
         }
+    }
     return 0;
 }
 

@@ -188,6 +188,15 @@ def test_bounded_memory_rounds_match_single_pass():
         assert np.array_equal(rounds.sym.per_bin_flop, one.sym.per_bin_flop)
         assert rounds.tuples_into_sort == one.sym.flop
         assert rounds.merged_total == one.c.nnz
+        # unsorted row ids inside A's columns: the host slabs filter, not bisect
+        rev = M.CscMatrix(a.nrows, a.ncols, a.colptr, a.rowids.copy(), a.values.copy())
+        for j in range(a.ncols):
+            p0, p1 = int(a.colptr[j]), int(a.colptr[j + 1])
+            rev.rowids[p0:p1] = a.rowids[p0:p1][::-1]
+            rev.values[p0:p1] = a.values[p0:p1][::-1]
+        rr = gpu(rev, csr, max_round_tuples=max(one.sym.flop // 5, 1))
+        assert_csr_matches(rr.c.rowptr, rr.c.colids, rr.c.values, one.c.rowptr, one.c.colids,
+                           one.c.values)
 
 
 def test_device_path_matches_host_path():

@@ -108,3 +108,24 @@ def test_row_band_and_cuts():
     # the bands' entries partition A's entries
     assert sum(M.row_band(csc, int(cuts[r]), int(cuts[r + 1])).nnz for r in range(4)) == csc.nnz
     assert np.array_equal(bands.plan_bands(csc, csr, 4), cuts)
+
+
+def test_row_band_unsorted_columns():
+    """row_band keeps the entries of [r0, r1) in their column order even when
+    the row ids inside a column are not sorted (the reference never requires
+    sorted CSC columns)."""
+    csr = M.make_matrix("er", 8, 5, seed=3)
+    csc = M.csr_to_csc(csr)
+    rev = M.CscMatrix(csc.nrows, csc.ncols, csc.colptr, csc.rowids.copy(), csc.values.copy())
+    for j in range(csc.ncols):
+        p0, p1 = int(csc.colptr[j]), int(csc.colptr[j + 1])
+        rev.rowids[p0:p1] = csc.rowids[p0:p1][::-1]
+        rev.values[p0:p1] = csc.values[p0:p1][::-1]
+    r0, r1 = 60, 170
+    got = M.row_band(rev, r0, r1)
+    exp = M.row_band(csc, r0, r1)
+    assert np.array_equal(got.colptr, exp.colptr)
+    for j in range(csc.ncols):
+        p0, p1 = int(exp.colptr[j]), int(exp.colptr[j + 1])
+        assert np.array_equal(got.rowids[p0:p1], exp.rowids[p0:p1][::-1])
+        assert np.array_equal(got.values[p0:p1], exp.values[p0:p1][::-1])
