@@ -380,3 +380,77 @@ def test_smoke_entry():
     sys.path.insert(0, str(ROOT))
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+def _raw_csr(nrows, ncols, rows, cols, vals):
+    """CSR straight from entry lists in the given order: duplicates and
+    unsorted columns inside a row are kept (the reference accepts any CSR)."""
+    rows = np.asarray(rows, np.int64)
+    order = np.argsort(rows, kind="stable")
+    rowptr = np.zeros(nrows + 1, np.uint64)
+    np.add.at(rowptr, rows + 1, 1)
+    rowptr = np.cumsum(rowptr).astype(np.uint64)
+    return M.CsrMatrix(nrows, ncols, rowptr, np.asarray(cols, np.uint32)[order],
+                       np.asarray(vals, np.float64)[order])
+
+
+def _raw_csc(nrows, ncols, rows, cols, vals):
+    t = _raw_csr(ncols, nrows, cols, rows, vals)
+    return M.CscMatrix(nrows, ncols, t.rowptr, t.colids, t.values)
+
+
+def test_duplicate_and_unsorted_input_entries():
+    """Repeated (row, col) entries in A or B and unsorted indices inside a
+    column/row are summed like any other duplicate tuples."""
+    rng = np.random.default_rng(7)
+    n, nnz = 300, 4000
+    ar, ac = rng.integers(0, n, nnz), rng.integers(0, n, nnz)
+    br, bc = rng.integers(0, n, nnz), rng.integers(0, n, nnz)
+    ar[:500], ac[:500] = ar[500:1000], ac[500:1000]  # explicit duplicates
+    av, bv = rng.random(nnz), rng.random(nnz)
+    a = _raw_csc(n, n, ar, ac, av)
+    b = _raw_csr(n, n, br, bc, bv)
+    res = gpu(a, b)
+    check_vs(res, oracle.multiply(a, b))
+    dense = np.zeros((n, n))
+    np.add.at(dense, (ar, ac), av)
+    db = np.zeros((n, n))
+    np.add.at(db, (br, bc), bv)
+    exp = dense @ db
+    got = np.zeros((n, n))
+    rows = np.repeat(np.arange(n), np.diff(res.c.rowptr).astype(np.int64))
+    got[rows, res.c.colids] = res.c.values
+    assert np.allclose(got, exp, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("ncols", [(1 << 31) - 1, 1 << 31, (1 << 32) - 1])
+def test_widest_column_space(ncols):
+    """col_bits 31 / 32: one row per GPU bin, keys are the columns themselves
+    (the reference widens to 64-bit keys here, pb_spgemm.cpp:153)."""
+    rng = np.random.default_rng(ncols & 0xffff)
+    m, k, nnz = 50, 40, 600
+    a = _raw_csc(m, k, rng.integers(0, m, nnz), rng.integers(0, k, nnz), rng.random(nnz))
+    cols = np.concatenate([rng.integers(0, ncols, nnz - 20), np.full(20, ncols - 1)])
+    b = _raw_csr(k, ncols, rng.integers(0, k, nnz), cols, rng.random(nnz))
+    res = gpu(a, b)
+    check_vs(res, oracle.multiply(a, b))
+    assert res.c.colids.max() == ncols - 1
+
+
+def test_empty_rows_and_columns():
+    """Whole empty column bands of A, empty rows of B, empty output rows."""
+    csr = M.make_matrix("er", 11, 6, seed=31)
+    a = M.csr_to_csc(csr)
+    keep = (np.arange(a.ncols) % 3) != 0
+    nnz_per = np.diff(a.colptr).astype(np.int64) * keep
+    colptr = np.concatenate([[0], np.cumsum(nnz_per)]).astype(np.uint64)
+    mask = np.repeat(keep, np.diff(a.colptr).astype(np.int64))
+    a2 = M.CscMatrix(a.nrows, a.ncols, colptr, a.rowids[mask], a.values[mask])
+    rkeep = (np.arange(csr.nrows) % 5) != 0
+    rn = np.diff(csr.rowptr).astype(np.int64) * rkeep
+    rowptr = np.concatenate([[0], np.cumsum(rn)]).astype(np.uint64)
+    rmask = np.repeat(rkeep, np.diff(csr.rowptr).astype(np.int64))
+    b2 = M.CsrMatrix(csr.nrows, csr.ncols, rowptr, csr.colids[rmask], csr.values[rmask])
+    res = gpu(a2, b2)
+    check_vs(res, oracle.multiply(a2, b2))
+    assert_valid_csr(res.c)
