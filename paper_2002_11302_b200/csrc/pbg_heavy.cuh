@@ -11,8 +11,8 @@
 //         (a key range of one heavy row) is cut into tiles spread over all
 //         CTAs; tile histograms on the next d key bits are summed per item,
 //         consecutive buckets are grouped into children of <= SM_CAP tuples,
-//         and each tile is counting-sorted by bucket in shared memory and
-//         written out as contiguous bucket segments into the other buffer
+//         and each tile reserves one range per (tile, bucket) and writes its
+//         tuples into those bucket segments of the other buffer
 //         (main <-> scratch). d is chosen so that a child still above SM_CAP
 //         (one bucket) spans <= 4096 columns.
 //   dense reduce: such a child is summed in a 4096-slot shared-memory
@@ -104,9 +104,12 @@ __global__ void k_heavy_init(const uint64_t* __restrict__ bin_cnt, const uint64_
 //   k_hv_plan    per item: bucket starts (-> scatter cursors) and children
 //                (consecutive buckets grouped to <= cap tuples, window rule
 //                as k_binflags); child counts are scanned on the host side
-//   k_hv_scatter tile: counting sort by bucket in shared memory, one global
-//                reservation per (tile, bucket), then the bucket segments are
-//                written out contiguously (coalesced) to the other buffer
+//   k_hv_scatter tile: ranks by bucket (one shared atomic per tuple), one
+//                global reservation per (tile, bucket), tuples written from
+//                registers into their bucket segment of the other buffer (a
+//                segment is finished by one CTA within microseconds, so L2
+//                assembles whole lines; staging the tile in bucket order in
+//                shared memory first was measured 4 % slower)
 //   k_hv_children child descriptors at the scanned positions
 // A child above cap is one bucket; if its key range is <= 2^HV_DENSE_BITS
 // it is reduced by k_hv_dense, else split again on the next level.
@@ -251,12 +254,8 @@ __global__ void __launch_bounds__(HV_PT) k_hv_plan(Items it, uint64_t nitems, ui
 }
 
 struct HvScatterSmem {
-    uint32_t k[HV_TILE];  // the tile in bucket order
-    double v[HV_TILE];
-    uint32_t cnt[1 << HV_MAXD];   // tile histogram -> local cursor
-    uint32_t lst[1 << HV_MAXD];   // local bucket starts
+    uint32_t cnt[1 << HV_MAXD];   // tile histogram
     uint32_t gb[1 << HV_MAXD];    // reserved global start of the tile's bucket segment
-    uint32_t s_warp[HV_NT / 32 + 1];
 };
 
 __global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, uint64_t nitems,
@@ -302,45 +301,25 @@ __global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, u
             }
         }
         __syncthreads();
-        {  // local starts + one global reservation per non-empty bucket
-            constexpr int PER = (1 << HV_MAXD) / HV_NT;  // 2
-            uint32_t v[PER], s = 0;
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const uint32_t q = tid * PER + j;
-                v[j] = q < nbk ? sm.cnt[q] : 0u;
-                s += v[j];
-            }
-            uint32_t tot;
-            uint32_t run = block_exclusive_scan<HV_NT>(s, sm.s_warp, tot);
+        {  // one global reservation per non-empty bucket
             uint32_t* cur = cursor + static_cast<uint64_t>(tl.i) * nbk;
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const uint32_t q = tid * PER + j;
-                if (q < nbk) {
-                    sm.lst[q] = run;
-                    if (v[j]) sm.gb[q] = atomicAdd(cur + q, v[j]);
-                }
-                run += v[j];
+            for (uint32_t q = tid; q < nbk; q += HV_NT) {
+                const uint32_t v = sm.cnt[q];
+                if (v) sm.gb[q] = atomicAdd(cur + q, v);
             }
         }
         __syncthreads();
+        // straight from registers to the reserved global segment: lanes of a
+        // store hit different buckets, but each segment is completed by this
+        // CTA within microseconds, so L2 assembles full lines
 #pragma unroll
         for (int j = 0; j < TPT; ++j) {
             const uint32_t q = tid + j * HV_NT;
             if (q < tl.m) {
-                const uint32_t pos = sm.lst[rb[j] >> 16] + (rb[j] & 0xffffu);
-                sm.k[pos] = kk[j];
-                sm.v[pos] = vv[j];
+                const uint64_t dst = static_cast<uint64_t>(sm.gb[rb[j] >> 16]) + (rb[j] & 0xffffu);
+                DK[dst] = kk[j];
+                DV[dst] = vv[j];
             }
-        }
-        __syncthreads();
-        for (uint32_t q = tid; q < tl.m; q += HV_NT) {
-            const uint32_t key = sm.k[q];
-            const uint32_t bk = (key >> s2) & mask;
-            const uint64_t dst = static_cast<uint64_t>(sm.gb[bk]) + (q - sm.lst[bk]);
-            DK[dst] = key;
-            DV[dst] = sm.v[q];
         }
         __syncthreads();
     }
