@@ -413,10 +413,25 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
             seen[q] = 0;
         }
         __syncthreads();
-        for (uint64_t q = tid; q < n; q += HV_NT) {
-            const uint32_t slot = __ldcs(K + q) - keylo;
-            atomicAdd(&acc[slot], __ldcs(V + q));
-            seen[slot] = 1;
+        // 8 tuples per thread in flight: the loads of a batch are issued
+        // before its shared-memory adds
+        constexpr int DU = 8;
+        for (uint64_t q0 = 0; q0 < n; q0 += static_cast<uint64_t>(DU) * HV_NT) {
+            uint32_t ks[DU];
+            double vs[DU];
+#pragma unroll
+            for (int u = 0; u < DU; ++u) {
+                const uint64_t q = q0 + tid + static_cast<uint64_t>(u) * HV_NT;
+                ks[u] = q < n ? __ldcs(K + q) : 0xffffffffu;
+                vs[u] = q < n ? __ldcs(V + q) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < DU; ++u) {
+                if (ks[u] == 0xffffffffu) continue;
+                const uint32_t slot = ks[u] - keylo;
+                atomicAdd(&acc[slot], vs[u]);
+                seen[slot] = 1;
+            }
         }
         __syncthreads();
         uint32_t cnt = 0;
