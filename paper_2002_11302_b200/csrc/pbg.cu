@@ -401,7 +401,11 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             xcolflop = vcf;
         }
         ctx->rep.expand_bands = static_cast<uint32_t>(g);
-        const unsigned exp_blocks = 8u * ctx->num_sms;
+        // short runs (ER, stencil): the scattered run stores bound the kernel
+        // and 2 CTAs per SM issue them best (measured 3-6 % faster than 8);
+        // long runs (RMAT) stream B and want every warp
+        unsigned exp_blocks = (flop < 64 * nnz_a ? 2u : 8u) * ctx->num_sms;
+        if (const char* e = getenv("PBG_EXP_BLOCKS")) exp_blocks = static_cast<unsigned>(atoi(e));  // tuning hook
         const uint64_t warps = static_cast<uint64_t>(exp_blocks) * EXP_NW;
         uint64_t ch = 256;
         while (ch < 16384 && flop / ch > warps * 4) ch <<= 1;
@@ -599,6 +603,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         }
         int cnt_per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cnt_per_sm, k_bincount, CNT_NT, cnt_smem);
+        if (const char* e = getenv("PBG_CNT_PER_SM")) cnt_per_sm = atoi(e);  // tuning hook
         k_bincount<<<static_cast<unsigned>(std::min<uint64_t>(
                          wcap, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
                      CNT_NT, cnt_smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
@@ -643,6 +648,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         sa.fallbacks = sc + S_FALLBACKS;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge, SM_NT, sizeof(SortSmem));
+        if (const char* e = getenv("PBG_SORT_PER_SM")) per_sm = atoi(e);  // tuning hook
         const unsigned sm_blocks = static_cast<unsigned>(
             std::min<uint64_t>(wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
         k_sortmerge<<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
