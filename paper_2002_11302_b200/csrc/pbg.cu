@@ -365,6 +365,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         int g = static_cast<int>(cfg.reserved[1]);                    // caller / test hook
         if (const char* e = getenv("PBG_EXPAND_BANDS")) g = atoi(e);  // tuning hook
         if (g < 1) g = 1;
+        if (g > BAND_MAX) g = BAND_MAX;
         if (static_cast<uint64_t>(g) > nb) g = static_cast<int>(nb);
         const uint64_t* xa_colptr = A.ptr;
         const uint32_t* xa_rowids = A.idx;

@@ -522,39 +522,57 @@ __device__ __forceinline__ int band_of(uint32_t r, const uint32_t* __restrict__ 
     return s;
 }
 
-// A(band s rows, j) counts. Row ids inside a column need not be sorted.
+constexpr int BAND_MAX = 16;
+
+// A(band s rows, j) counts, one pass over each column (per-band counters in
+// registers). Row ids inside a column need not be sorted.
 __global__ void k_band_count(const uint64_t* __restrict__ a_colptr,
                              const uint32_t* __restrict__ a_rowids, uint64_t k,
                              const uint32_t* __restrict__ cuts, int g, uint64_t* vcnt) {
+    __shared__ uint32_t s_cuts[BAND_MAX + 1];
+    if (threadIdx.x <= g) s_cuts[threadIdx.x] = cuts[threadIdx.x];
+    __syncthreads();
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= k) return;
     const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
-    for (int s = 0; s < g; ++s) {
-        uint64_t c = 0;
-        for (uint64_t p = p0; p < p1; ++p) c += band_of(a_rowids[p], cuts, g) == s;
-        vcnt[static_cast<uint64_t>(s) * k + j] = c;
+    uint32_t c[BAND_MAX];
+#pragma unroll
+    for (int s = 0; s < BAND_MAX; ++s) c[s] = 0;
+    for (uint64_t p = p0; p < p1; ++p) {
+        const int bnd = band_of(a_rowids[p], s_cuts, g);
+#pragma unroll
+        for (int s = 0; s < BAND_MAX; ++s) c[s] += bnd == s;
     }
+#pragma unroll
+    for (int s = 0; s < BAND_MAX; ++s)
+        if (s < g) vcnt[static_cast<uint64_t>(s) * k + j] = c[s];
 }
 
-// Band-major copy of A (stable inside each column).
+// Band-major copy of A (stable inside each column), one pass per column.
 __global__ void k_band_copy(const uint64_t* __restrict__ a_colptr,
                             const uint32_t* __restrict__ a_rowids,
                             const double* __restrict__ a_vals, uint64_t k,
                             const uint32_t* __restrict__ cuts, int g,
                             const uint64_t* __restrict__ va_colptr, uint32_t* va_rowids,
                             double* va_vals) {
+    __shared__ uint32_t s_cuts[BAND_MAX + 1];
+    if (threadIdx.x <= g) s_cuts[threadIdx.x] = cuts[threadIdx.x];
+    __syncthreads();
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= k) return;
     const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
-    for (int s = 0; s < g; ++s) {
-        uint64_t d = va_colptr[static_cast<uint64_t>(s) * k + j];
-        for (uint64_t p = p0; p < p1; ++p) {
-            const uint32_t r = a_rowids[p];
-            if (band_of(r, cuts, g) != s) continue;
-            va_rowids[d] = r;
-            va_vals[d] = a_vals[p];
-            ++d;
-        }
+    uint64_t d[BAND_MAX];
+#pragma unroll
+    for (int s = 0; s < BAND_MAX; ++s) d[s] = s < g ? va_colptr[static_cast<uint64_t>(s) * k + j] : 0;
+    for (uint64_t p = p0; p < p1; ++p) {
+        const uint32_t r = a_rowids[p];
+        const int bnd = band_of(r, s_cuts, g);
+        uint64_t q = 0;
+#pragma unroll
+        for (int s = 0; s < BAND_MAX; ++s)
+            if (bnd == s) q = d[s]++;
+        va_rowids[q] = r;
+        va_vals[q] = a_vals[p];
     }
 }
 
