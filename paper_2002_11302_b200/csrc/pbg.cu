@@ -119,6 +119,9 @@ struct pbg_context {
     pbg_report rep{};
     uint32_t launches = 0;
     bool have_result = false;
+    // host path: tuple budget of a single pass (0 = no check); run_pipeline
+    // returns kNeedsRounds after the symbolic phase when flop exceeds it
+    uint64_t round_tuples = 0;
     ~pbg_context() {
         for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
                           &bin_off, &cursor, &bin_out, &chunk_p0, &keys, &vals, &ccol, &cval,
@@ -154,6 +157,8 @@ struct pbg_handle {
 };
 
 namespace {
+
+constexpr int kNeedsRounds = -1;  // internal: the single pass does not fit HBM
 
 int set_device(int dev) {
     int count = 0;
@@ -324,6 +329,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         return fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits");
     const uint64_t flop = hs[S_FLOP];
     ctx->flop = flop;
+    if (ctx->round_tuples && flop > ctx->round_tuples) return kNeedsRounds;
     ctx->rep.flop = flop;
     ctx->rep.nnz_a = A.nnz;
     ctx->rep.nnz_b = B.nnz;
@@ -1030,47 +1036,51 @@ int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_c
     h->cfg = cfg;
     cudaStream_t st = nullptr;
     // ---- memory plan: one pass, or bounded-memory rounds over row bands ----
-    // (configs whose tuples + C exceed HBM run band by band)
-    uint64_t flop = 0;
-    for (uint64_t i = 0; i < a->ncols; ++i) flop += (a->ptr[i + 1] - a->ptr[i]) * (b->ptr[i + 1] - b->ptr[i]);
+    // (configs whose tuples + C exceed HBM run band by band).
+    // The pass starts optimistically; its symbolic phase knows flop exactly
+    // and stops before any tuple storage is allocated when it does not fit.
     size_t free_b = 0, total_b = 0;
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t inputs = (uint64_t(a->ncols) + uint64_t(b->nrows) + 2) * 8 + (a->nnz + b->nnz) * 12;
     const uint64_t work_rows = (uint64_t(a->nrows) + 2) * 96;
     const uint64_t reserve = 2ull << 30;
-    uint64_t budget = free_b > inputs + work_rows + reserve ? free_b - inputs - work_rows - reserve : 0;
+    // HBM the pool already holds is reusable by this pass
+    const uint64_t held = ctx->keys.cap + ctx->vals.cap + ctx->ccol.cap + ctx->cval.cap +
+                          ctx->skeys.cap + ctx->svals.cap;
+    const uint64_t avail = free_b + held;
+    uint64_t budget = avail > inputs + work_rows + reserve ? avail - inputs - work_rows - reserve : 0;
     // 12 B tuples + a C upper bound of 12 B per tuple, plus run plans / scratch slack
-    uint64_t per_tuple = 40;  // tuples 12 + C bound 12 + heavy scratch 12 + headroom
-    uint64_t max_tuples = budget / per_tuple;
+    const uint64_t per_tuple = 40;  // tuples 12 + C bound 12 + heavy scratch 12 + headroom
+    uint64_t max_tuples = std::max<uint64_t>(budget / per_tuple, 1);
     if (cfg.reserved[0]) max_tuples = std::min<uint64_t>(max_tuples, cfg.reserved[0]);
-    const uint32_t nrounds = (flop > max_tuples && max_tuples > 0)
-                                 ? static_cast<uint32_t>((flop + max_tuples - 1) / max_tuples)
-                                 : 1u;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    if (nrounds == 1) {
-        cudaEventRecord(e0, st);
-        rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
-        if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
-        if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
-        if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
-        if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
-        if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
-        cudaEventRecord(e1, st);
-        if (!rc) {
-            pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
-                            static_cast<const uint32_t*>(ctx->in_a_idx.p),
-                            static_cast<const double*>(ctx->in_a_val.p)};
-            pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
-                            static_cast<const uint32_t*>(ctx->in_b_idx.p),
-                            static_cast<const double*>(ctx->in_b_val.p)};
-            rc = run_pipeline(ctx, da, db, cfg, st);
-        }
-        float ms = 0;
-        if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
-            h->t_h2d = ms * 1e-3;
-    } else {
+    cudaEventRecord(e0, st);
+    rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
+    cudaEventRecord(e1, st);
+    if (!rc) {
+        pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                        static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                        static_cast<const double*>(ctx->in_a_val.p)};
+        pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                        static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                        static_cast<const double*>(ctx->in_b_val.p)};
+        ctx->round_tuples = max_tuples;
+        rc = run_pipeline(ctx, da, db, cfg, st);
+        ctx->round_tuples = 0;
+    }
+    float ms = 0;
+    if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
+        h->t_h2d = ms * 1e-3;
+    if (rc == kNeedsRounds) {
+        const uint64_t flop = ctx->flop;
+        const uint32_t nrounds = static_cast<uint32_t>((flop + max_tuples - 1) / max_tuples);
         rc = multiply_in_rounds(h, *a, *b, cfg, nrounds, st);
     }
     cudaEventDestroy(e0);
