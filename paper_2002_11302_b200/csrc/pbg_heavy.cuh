@@ -560,7 +560,7 @@ constexpr int CNT_NT = PBG_CNT_NT;
 constexpr int CNT_SLOTS_LOG = PBG_CNT_SLOTS_LOG;
 constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
 constexpr uint32_t CNT_EMPTY = 0xffffffffu;
-constexpr int CNT_PER = 8;  // keys per thread: bins of up to CNT_NT*CNT_PER tuples
+constexpr int CNT_PER = 4096 / CNT_NT;  // keys per thread: bins of up to CNT_NT*CNT_PER = 4096 tuples
 
 __device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
                                          const uint32_t* __restrict__ skeys, const WorkBins& w,
