@@ -119,6 +119,17 @@ int pbg_multiply_begin(const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
  * be NULL. */
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
                        pbg_report* rep);
+/* coo_to_csr / coo_to_csc (convert.cpp:41-98) on the GPU, through the same
+ * pipeline: the conversion is the product A.B with A(major(e), e) = 1 and
+ * B(e, minor(e)) = val(e), so duplicates are summed (exact zeros kept) and
+ * minor indices ordered by the sort+merge path. to_csc = 0 gives the CSR
+ * (major = row), 1 the CSC (major = col). Entries outside nrows x ncols
+ * return PBG_ERR_ARG (validate, convert.cpp:8-37). Host arrays; the result
+ * is read with pbg_multiply_fetch (rowptr = the major pointer array) and
+ * freed with pbg_release. */
+int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint32_t* rows,
+                          const uint32_t* cols, const double* vals, int to_csc,
+                          const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_out);
 /* The reference SymbolicResult (pb_spgemm.hpp:48-55) on the REFERENCE bin
  * layout: per_column_flop[a.ncols], per_bin_flop[nbins], bin_row_starts
  * [nbins+1]; nbins from pbg_report.nbins. Any pointer may be NULL. */

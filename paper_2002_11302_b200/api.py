@@ -160,6 +160,53 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
     return PbResult(c, sym, phases, rep.tuples_into_sort, rep.merged_total, r)
 
 
+def _coo_convert(nrows, ncols, rows, cols, vals, to_csc, cfg):
+    cfg = cfg or PbConfig()
+    lib = _native.pbg()
+    r = np.ascontiguousarray(rows, dtype=np.uint32)
+    c = np.ascontiguousarray(cols, dtype=np.uint32)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    if not (r.size == c.size == v.size):
+        raise ValueError("rows, cols and vals must have one entry each")
+    nz = r.size
+    h = C.c_void_p()
+    out_nnz = C.c_uint64(0)
+    c_cfg = cfg.to_c()
+    p = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+    rc = lib.pbg_coo_convert_begin(nrows, ncols, nz, p(r), p(c), p(v), int(to_csc),
+                                   C.byref(c_cfg), C.byref(h), C.byref(out_nnz))
+    if rc:
+        if rc == _native.PBG_ERR_ARG:
+            raise ValueError(_native.last_error())
+        _raise(rc)
+    try:
+        k = out_nnz.value
+        nmajor = ncols if to_csc else nrows
+        ptr = np.empty(nmajor + 1, np.uint64)
+        idx = np.empty(max(k, 1), np.uint32)
+        val = np.empty(max(k, 1), np.float64)
+        rc = lib.pbg_multiply_fetch(h, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data, None)
+        if rc:
+            _raise(rc)
+    finally:
+        lib.pbg_release(h)
+    if to_csc:
+        return CscMatrix(nrows, ncols, ptr, idx[:k], val[:k])
+    return CsrMatrix(nrows, ncols, ptr, idx[:k], val[:k])
+
+
+def coo_to_csr(nrows: int, ncols: int, rows, cols, vals, cfg: PbConfig | None = None) -> CsrMatrix:
+    """coo_to_csr (convert.cpp:41-70, duplicates summed, columns sorted) on the
+    GPU, run as the product of a one-entry-per-column CSC with a
+    one-entry-per-row CSR through the same pipeline as pb_multiply."""
+    return _coo_convert(nrows, ncols, rows, cols, vals, False, cfg)
+
+
+def coo_to_csc(nrows: int, ncols: int, rows, cols, vals, cfg: PbConfig | None = None) -> CscMatrix:
+    """coo_to_csc (convert.cpp:82-89) on the GPU (see coo_to_csr)."""
+    return _coo_convert(nrows, ncols, rows, cols, vals, True, cfg)
+
+
 class DeviceContext:
     """Device-resident multiply: views over CUDA memory (e.g. torch tensors)."""
 

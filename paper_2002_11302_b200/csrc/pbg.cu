@@ -1094,6 +1094,83 @@ int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_c
     return PBG_OK;
 }
 
+int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint32_t* rows,
+                          const uint32_t* cols, const double* vals, int to_csc,
+                          const pbg_config* cfg_in, pbg_handle** out, uint64_t* nnz_out) {
+    using namespace pbg;
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    *out = nullptr;
+    if (nnz && (!rows || !cols || !vals)) return fail(PBG_ERR_ARG, "COO arrays are null");
+    if (nnz >= (1ull << 32)) return fail(PBG_ERR_ARG, "COO with 2^32 or more entries");
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    int rc;
+    if ((rc = validate_cfg(cfg))) return rc;
+    if ((rc = set_device(cfg.device))) return rc;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    pbg_context* ctx = pool_get(dev);
+    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
+    cudaStream_t st = nullptr;
+    // major = row (CSR) or col (CSC)
+    const uint32_t nmajor = to_csc ? ncols : nrows, nminor = to_csc ? nrows : ncols;
+    const uint32_t* major = to_csc ? cols : rows;
+    const uint32_t* minor = to_csc ? rows : cols;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    rc = copy_in(ctx->in_a_idx, major, nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_idx, minor, nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_val, vals, nnz * 8, st);
+    if (!rc) rc = grow(ctx->in_a_ptr, (nnz + 1) * 8);
+    if (!rc) rc = grow(ctx->in_b_ptr, (nnz + 1) * 8);
+    if (!rc) rc = grow(ctx->in_a_val, (nnz + 1) * 8);
+    if (!rc) rc = grow(ctx->zero_block, 64);
+    cudaEventRecord(e1, st);
+    if (rc) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return rc;
+    }
+    auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
+    CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
+    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+        static_cast<double*>(ctx->in_a_val.p), static_cast<const uint32_t*>(ctx->in_a_idx.p),
+        static_cast<const uint32_t*>(ctx->in_b_idx.p), maxes);
+    unsigned long long mx[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(mx, maxes, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // validate (convert.cpp:8-37): every entry inside the matrix
+    if (nnz && (mx[0] >= nmajor || mx[1] >= nminor))
+        return fail(PBG_ERR_ARG, "COO entry out of range (structural_error)");
+    const pbg_csx_view da{nmajor, static_cast<uint32_t>(nnz), nnz,
+                          static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                          static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                          static_cast<const double*>(ctx->in_a_val.p)};
+    const pbg_csx_view db{static_cast<uint32_t>(nnz), nminor, nnz,
+                          static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                          static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                          static_cast<const double*>(ctx->in_b_val.p)};
+    auto* h = new pbg_handle;
+    h->ctx = ctx;
+    h->cfg = cfg;
+    h->t_h2d = ms * 1e-3;
+    if ((rc = run_pipeline(ctx, da, db, cfg, st))) {
+        pbg_release(h);
+        return rc;
+    }
+    if (nnz_out) *nnz_out = ctx->nnz_c;
+    *out = h;
+    return PBG_OK;
+}
+
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
                        pbg_report* rep) {
     if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");

@@ -591,4 +591,34 @@ __global__ void k_zero_u64(uint64_t* p, uint64_t n) {
         p[i] = 0;
 }
 
+// ---------------------------------------------------- COO -> CSR / CSC --
+// The conversion runs as the product A.B with A(major(e), e) = 1 (a CSC with
+// one entry per column) and B(e, minor(e)) = val(e) (a CSR with one entry
+// per row): the expand emits one tuple per entry, the sort+merge sums
+// duplicates and orders minors, the CSR assembly builds the pointer array.
+__global__ void k_coo_views(uint64_t nnz, uint64_t* iota_a, uint64_t* iota_b, double* ones,
+                            const uint32_t* __restrict__ major, const uint32_t* __restrict__ minor,
+                            unsigned long long* maxes) {
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint32_t mj = 0, mn = 0;
+    if (e <= nnz) {
+        iota_a[e] = e;
+        iota_b[e] = e;
+    }
+    if (e < nnz) {
+        ones[e] = 1.0;
+        mj = major[e];
+        mn = minor[e];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mj = max(mj, __shfl_xor_sync(FULL, mj, o));
+        mn = max(mn, __shfl_xor_sync(FULL, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0 && e < nnz + 32) {
+        atomicMax(maxes, static_cast<unsigned long long>(mj));
+        atomicMax(maxes + 1, static_cast<unsigned long long>(mn));
+    }
+}
+
 }  // namespace pbg

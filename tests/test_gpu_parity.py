@@ -454,3 +454,29 @@ def test_empty_rows_and_columns():
     res = gpu(a2, b2)
     check_vs(res, oracle.multiply(a2, b2))
     assert_valid_csr(res.c)
+
+
+def test_coo_conversion_on_gpu():
+    """coo_to_csr / coo_to_csc (convert.cpp:41-98) through the product path:
+    duplicates summed, exact-zero sums kept, minor indices sorted; out-of-range
+    entries rejected; empty input."""
+    rng = np.random.default_rng(9)
+    for (m, n, nnz) in ((300, 500, 20000), (1 << 14, 1 << 14, 300000), (7, 5, 0)):
+        rows = rng.integers(0, m, nnz).astype(np.uint32)
+        cols = rng.integers(0, n, nnz).astype(np.uint32)
+        vals = rng.random(nnz)
+        if nnz:
+            rows[:50], cols[:50] = rows[50:100], cols[50:100]
+            vals[:50] = -vals[50:100]  # cancellations -> exact zeros kept
+        got = api.coo_to_csr(m, n, rows, cols, vals)
+        exp = M.coo_to_csr(m, n, rows, cols, vals)
+        assert_csr_matches(got.rowptr, got.colids, got.values, exp.rowptr, exp.colids, exp.values)
+        gc = api.coo_to_csc(m, n, rows, cols, vals)
+        ec = M.coo_to_csc(m, n, rows, cols, vals)
+        assert_csr_matches(gc.colptr, gc.rowids, gc.values, ec.colptr, ec.rowids, ec.values)
+        if oracle.ref_available() and nnz <= 50000:  # the reference's own convert.cpp
+            rp, ri, rv = oracle.ref_convert(True, m, n, rows, cols, vals)
+            assert_csr_matches(got.rowptr, got.colids, got.values, rp, ri, rv)
+    with pytest.raises(ValueError):
+        api.coo_to_csr(4, 4, np.array([1, 4], np.uint32), np.array([0, 0], np.uint32),
+                       np.ones(2))
