@@ -150,9 +150,21 @@ def dist_env():
     return ws, rank, local
 
 
-def build_inputs(cfg_name: str):
+def build_inputs(cfg_name: str, seed: int = 1):
+    """The config's matrix as (CSC, CSR): generated on the GPU when one is
+    present (pbg_generate_begin, bit-identical to the host build), else on
+    the host."""
     t = time.time()
-    a_csc, a_csr = M.make_config(cfg_name)
+    try:
+        import torch
+        gpu = torch.cuda.is_available()
+    except Exception:
+        gpu = False
+    if gpu:
+        local = int(os.environ.get("PBG_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        a_csc, a_csr = M.make_config_gpu(cfg_name, seed, device=local)
+    else:
+        a_csc, a_csr = M.make_config(cfg_name, seed)
     log(f"[bench] {cfg_name}: n={a_csr.nrows} nnz={a_csr.nnz} inputs built in {time.time() - t:.1f}s")
     return a_csc, a_csr
 
@@ -197,7 +209,10 @@ def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    a_csc, a_csr = build_inputs(args.config)
+    # host-built inputs: nothing of this repository's GPU path touches this arm
+    t = time.time()
+    a_csc, a_csr = M.make_config(args.config)
+    log(f"[bench] {args.config}: n={a_csr.nrows} nnz={a_csr.nnz} host inputs in {time.time() - t:.1f}s")
     nthreads = os.cpu_count() or 1
     os.environ.setdefault("OMP_PLACES", "cores")
     os.environ.setdefault("OMP_PROC_BIND", "close")
@@ -244,7 +259,7 @@ def run_gpu_arm(args):
     if weak:
         # rank r: its own row block A_r of the row-stacked A, times the shared B
         if rank > 0:
-            a_csc = M.make_config(args.config, seed=1 + rank)[0]
+            a_csc = build_inputs(args.config, seed=1 + rank)[0]
         rf = M.row_flop(a_csc, a_csr)
         r0, r1 = 0, n
         a_band = a_csc

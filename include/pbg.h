@@ -130,6 +130,15 @@ int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double
 int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint32_t* rows,
                           const uint32_t* cols, const double* vals, int to_csc,
                           const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_out);
+/* The benchmark inputs of SURVEY.md §8d built on the GPU: gen_er (kind 0,
+ * d = ef distinct rows per column) or gen_rmat (kind 1, Graph500 a,b,c,
+ * duplicates collapsed, self-loops dropped) with the reference's seeded
+ * streams (generate.cpp:20-90), converted like pbg_coo_convert_begin, values
+ * U[0,1) from SplitMix64(split_seed(vseed, row << 32 | col)). to_csc = 0
+ * gives the CSR, 1 the CSC; read with pbg_multiply_fetch, free with
+ * pbg_release. */
+int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t vseed, int to_csc,
+                       const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_out);
 /* The reference SymbolicResult (pb_spgemm.hpp:48-55) on the REFERENCE bin
  * layout: per_column_flop[a.ncols], per_bin_flop[nbins], bin_row_starts
  * [nbins+1]; nbins from pbg_report.nbins. Any pointer may be NULL. */

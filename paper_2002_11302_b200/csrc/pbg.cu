@@ -107,7 +107,7 @@ struct pbg_context {
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
         child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
     DevBuf items[2][8];
-    DevBuf row_pack, tile_pos, tile_item, hv_hist;
+    DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
     DevBuf wb[7];
     size_t zero_bytes = 0;
@@ -133,7 +133,7 @@ struct pbg_context {
         for (auto& set : items)
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
-        for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &va_colptr, &va_rowids, &va_vals,
+        for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &gen_r, &gen_c, &gen_pos, &gen_stat, &va_colptr, &va_rowids, &va_vals,
                           &vcolflop, &bcuts, &vstat})
             b->release();
         if (ev_ok)
@@ -1166,6 +1166,91 @@ int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const ui
         pbg_release(h);
         return rc;
     }
+    if (nnz_out) *nnz_out = ctx->nnz_c;
+    *out = h;
+    return PBG_OK;
+}
+
+int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t vseed, int to_csc,
+                       const pbg_config* cfg_in, pbg_handle** out, uint64_t* nnz_out) {
+    using namespace pbg;
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    *out = nullptr;
+    if ((kind != 0 && kind != 1) || scale < 1 || scale > 30 || ef < 1)
+        return fail(PBG_ERR_ARG, "generator: kind 0 (ER) or 1 (RMAT), scale 1..30, ef >= 1");
+    const uint64_t n = 1ull << scale;
+    if (kind == 0 && ef > n) return fail(PBG_ERR_ARG, "ER: d above n");
+    const uint64_t raw = kind == 0 ? n * ef : static_cast<uint64_t>(ef) << scale;
+    if (raw >= (1ull << 32)) return fail(PBG_ERR_ARG, "generator: 2^32 or more draws");
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    int rc;
+    if ((rc = validate_cfg(cfg))) return rc;
+    if ((rc = set_device(cfg.device))) return rc;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    pbg_context* ctx = pool_get(dev);
+    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
+    cudaStream_t st = nullptr;
+    if ((rc = grow(ctx->in_a_idx, (raw + 1) * 4)) || (rc = grow(ctx->in_b_idx, (raw + 1) * 4)) ||
+        (rc = grow(ctx->in_b_val, (raw + 1) * 8)) || (rc = grow(ctx->in_a_ptr, (raw + 1) * 8)) ||
+        (rc = grow(ctx->in_b_ptr, (raw + 1) * 8)) || (rc = grow(ctx->in_a_val, (raw + 1) * 8)) ||
+        (rc = grow(ctx->zero_block, 64)))
+        return rc;
+    auto* rows = static_cast<uint32_t*>(ctx->in_a_idx.p);
+    auto* cols = static_cast<uint32_t*>(ctx->in_b_idx.p);
+    uint64_t nnz = raw;
+    if (kind == 0) {
+        k_gen_er<<<blocks_for(n, 256), 256, 0, st>>>(scale, ef, seed, rows, cols);
+    } else {
+        // draws, then self-loops dropped by a compaction (duplicates are
+        // collapsed by the conversion below)
+        const uint64_t tiles = (raw + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+        if ((rc = grow(ctx->gen_r, raw * 4)) || (rc = grow(ctx->gen_c, raw * 4)) ||
+            (rc = grow(ctx->gen_pos, (raw + 1) * 8)) || (rc = grow(ctx->gen_stat, (tiles + 16) * 8)))
+            return rc;
+        auto* gr = static_cast<uint32_t*>(ctx->gen_r.p);
+        auto* gc = static_cast<uint32_t*>(ctx->gen_c.p);
+        auto* pos = static_cast<uint64_t*>(ctx->gen_pos.p);
+        auto* gst = static_cast<unsigned long long*>(ctx->gen_stat.p);
+        CUDA_TRY(cudaMemsetAsync(gst, 0, (tiles + 16) * 8, st));
+        k_gen_rmat<<<blocks_for(raw, 256), 256, 0, st>>>(scale, raw, seed, 0.57, 0.19, 0.19, gr, gc);
+        launch_scan(OffDiagIn{gr, gc}, pos, raw, nullptr, raw, gst + 16,
+                    reinterpret_cast<unsigned int*>(gst), nullptr, nullptr, st);
+        k_compact_offdiag<<<blocks_for(raw, 256), 256, 0, st>>>(gr, gc, pos, raw, rows, cols);
+        CUDA_TRY(cudaMemcpyAsync(&nnz, pos + raw, 8, cudaMemcpyDeviceToHost, st));
+    }
+    auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
+    CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const uint32_t* major = to_csc ? cols : rows;
+    const uint32_t* minor = to_csc ? rows : cols;
+    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+        static_cast<double*>(ctx->in_a_val.p), major, minor, maxes);
+    // B's values: 1.0 (duplicates sum to their multiplicity; replaced below)
+    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+        static_cast<double*>(ctx->in_b_val.p), major, minor, maxes);
+    const pbg_csx_view da{static_cast<uint32_t>(n), static_cast<uint32_t>(nnz), nnz,
+                          static_cast<const uint64_t*>(ctx->in_a_ptr.p), major,
+                          static_cast<const double*>(ctx->in_a_val.p)};
+    const pbg_csx_view db{static_cast<uint32_t>(nnz), static_cast<uint32_t>(n), nnz,
+                          static_cast<const uint64_t*>(ctx->in_b_ptr.p), minor,
+                          static_cast<const double*>(ctx->in_b_val.p)};
+    auto* h = new pbg_handle;
+    h->ctx = ctx;
+    h->cfg = cfg;
+    if ((rc = run_pipeline(ctx, da, db, cfg, st))) {
+        pbg_release(h);
+        return rc;
+    }
+    k_fill_values<<<blocks_for(n, 256), 256, 0, st>>>(
+        vseed, n, static_cast<const uint64_t*>(ctx->rowptr.p), static_cast<const uint32_t*>(ctx->ccol.p),
+        static_cast<double*>(ctx->cval.p), to_csc);
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
     if (nnz_out) *nnz_out = ctx->nnz_c;
     *out = h;
     return PBG_OK;

@@ -621,4 +621,90 @@ __global__ void k_coo_views(uint64_t nnz, uint64_t* iota_a, uint64_t* iota_b, do
     }
 }
 
+// ------------------------------------------------ benchmark generators --
+// The reference's generators (generate.hpp:12-40, generate.cpp:20-90) as
+// device streams: SplitMix64 per column (ER, Floyd sampling) or per edge
+// (RMAT quadrant descent), the same seeds giving the same draws.
+struct DSm64 {
+    uint64_t s;
+    __device__ explicit DSm64(uint64_t seed) : s(seed) {}
+    __device__ uint64_t next() {
+        uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    __device__ uint64_t below(uint64_t bound) {
+        const uint64_t limit = bound * (~uint64_t{0} / bound);
+        uint64_t x;
+        do x = next();
+        while (x >= limit);
+        return x % bound;
+    }
+    __device__ double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+__device__ __forceinline__ uint64_t dsplit(uint64_t seed, uint64_t stream) {
+    return DSm64(seed ^ (stream * 0xD6E8FEB86659FD93ULL)).next();
+}
+
+// gen_er: column j holds d distinct rows (Floyd's sampling); entry j*d + f
+__global__ void k_gen_er(int scale, uint32_t d, uint64_t seed, uint32_t* rows, uint32_t* cols) {
+    const uint32_t n = 1u << scale;
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    DSm64 rng(dsplit(seed, j));
+    uint32_t* col = rows + j * d;
+    uint32_t filled = 0;
+    for (uint32_t t = n - d; t < n; ++t) {
+        const uint32_t r = static_cast<uint32_t>(rng.below(static_cast<uint64_t>(t) + 1));
+        bool seen = false;
+        for (uint32_t q = 0; q < filled; ++q) seen |= col[q] == r;
+        cols[j * d + filled] = static_cast<uint32_t>(j);
+        col[filled++] = seen ? t : r;
+    }
+}
+
+// gen_rmat: edge e descends `scale` quadrant levels with cuts a, a+b, a+b+c
+__global__ void k_gen_rmat(int scale, uint64_t nedges, uint64_t seed, double a, double b, double c,
+                           uint32_t* rows, uint32_t* cols) {
+    const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (e >= nedges) return;
+    DSm64 rng(dsplit(seed, e));
+    const double cut_a = a, cut_ab = a + b, cut_abc = a + b + c;
+    uint32_t row = 0, col = 0;
+    for (int level = scale - 1; level >= 0; --level) {
+        const double u = rng.unit();
+        if (u >= cut_ab) row |= 1u << level;
+        if (u >= cut_abc || (u >= cut_a && u < cut_ab)) col |= 1u << level;
+    }
+    rows[e] = row;
+    cols[e] = col;
+}
+
+struct OffDiagIn {  // 1 for an entry off the diagonal (self-loops dropped)
+    const uint32_t* r;
+    const uint32_t* c;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return r[i] != c[i]; }
+};
+__global__ void k_compact_offdiag(const uint32_t* __restrict__ r, const uint32_t* __restrict__ c,
+                                  const uint64_t* __restrict__ pos, uint64_t n, uint32_t* r2,
+                                  uint32_t* c2) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n || r[i] == c[i]) return;
+    r2[pos[i]] = r[i];
+    c2[pos[i]] = c[i];
+}
+
+// U[0,1) value of (row, col): SplitMix64(split_seed(vseed, row << 32 | col))
+// (generate.hpp:35-40), over a compressed matrix (major = row for CSR).
+__global__ void k_fill_values(uint64_t vseed, uint64_t nmajor, const uint64_t* __restrict__ ptr,
+                              const uint32_t* __restrict__ idx, double* vals, int major_is_col) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= nmajor) return;
+    for (uint64_t p = ptr[i]; p < ptr[i + 1]; ++p) {
+        const uint64_t r = major_is_col ? idx[p] : i, c = major_is_col ? i : idx[p];
+        vals[p] = DSm64(dsplit(vseed, (r << 32) | c)).unit();
+    }
+}
+
 }  // namespace pbg

@@ -480,3 +480,15 @@ def test_coo_conversion_on_gpu():
     with pytest.raises(ValueError):
         api.coo_to_csr(4, 4, np.array([1, 4], np.uint32), np.array([0, 0], np.uint32),
                        np.ones(2))
+
+
+@pytest.mark.parametrize("name", ["C1", "R16", "E22"])
+def test_gpu_generators_match_host(name):
+    """pbg_generate_begin: the reference's ER / RMAT draws on the device,
+    converted and valued there, bit-identical to the host build (whose
+    generators are pinned against the reference)."""
+    hc, hr = M.make_config(name)
+    gc, gr = M.make_config_gpu(name)
+    for g, h in ((gc.colptr, hc.colptr), (gc.rowids, hc.rowids), (gc.values, hc.values),
+                 (gr.rowptr, hr.rowptr), (gr.colids, hr.colids), (gr.values, hr.values)):
+        assert np.array_equal(g, h)
