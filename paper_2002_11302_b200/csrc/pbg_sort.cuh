@@ -47,21 +47,38 @@ namespace pbg {
 #ifndef PBG_SM_NT
 #define PBG_SM_NT 512
 #endif
+#ifndef PBG_SM_LAG
+#define PBG_SM_LAG 1
+#endif
+#ifndef PBG_SM_PF
+#define PBG_SM_PF 0
+#endif
 
 constexpr int SM_NT = PBG_SM_NT;
 constexpr int SM_NW = SM_NT / 32;
 constexpr int SM_CAP = PBG_SM_CAP;            // max tuples per smem bin
-constexpr int SM_NB = SM_CAP;                 // buckets of the MSD pass
+constexpr int SM_NB = 2 * SM_CAP;             // buckets of the MSD pass (u16 counters, 2 per word)
 constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
+constexpr int SM_NBW = SM_NB / 2;             // counter words
 #ifndef PBG_SM_BMAX
 #define PBG_SM_BMAX 128
 #endif
 constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
-constexpr int SM_ITEMS = SM_CAP / SM_NT;      // 8 tuples per thread
+constexpr int SM_ITEMS = SM_CAP / SM_NT;      // tuples per thread
 constexpr int SM_PER_WARP = SM_CAP / SM_NW;   // warp-contiguous element layout
-static_assert(SM_ITEMS == 8, "8 tuples per thread");
-static_assert(SM_NB / SM_NT == 8, "8 bucket counters per thread in the scan");
-static_assert(SM_NW * 256 <= SM_NB, "LSD counters fit the bucket counters");
+constexpr int SM_WPT = SM_NBW / SM_NT;        // counter words per thread in the scan
+static_assert(SM_WPT % 4 == 0, "counter words per thread: whole uint4s");
+// LSD fallback digits: per-(warp, digit) counters must fit the counter words
+constexpr int LSD_BITS = SM_NW * 256 <= SM_NBW ? 8 : 7;
+constexpr int LSD_ND = 1 << LSD_BITS;
+static_assert(SM_NW * LSD_ND <= SM_NBW, "LSD counters fit the bucket counter words");
+// Buffer ring: the bin being sorted, LAG sorted bins whose output is still
+// pending (their prefixes need all earlier bins sorted) and PF bins whose TMA
+// copy is in flight.
+constexpr int SM_LAG = PBG_SM_LAG;
+constexpr int SM_PF = PBG_SM_PF;
+constexpr int SM_NBUF = 1 + SM_LAG + SM_PF;
+constexpr int SM_NMETA = SM_NBUF + 1;         // descriptors: pending .. next to fetch
 
 struct SortArgs {
     WorkBins w;
@@ -121,16 +138,17 @@ struct Parked {
 };
 
 struct SortSmem {
-    uint32_t k[2][SM_CAP];
-    double v[2][SM_CAP];
-    uint32_t cnt[SM_NB];  // bucket histogram -> bucket starts; LSD per-warp counters
+    uint32_t k[SM_NBUF][SM_CAP];
+    double v[SM_NBUF][SM_CAP];
+    uint32_t cnt[SM_NBW];  // bucket histogram -> bucket starts (u16 pairs); LSD per-warp counters
     uint32_t s_warp32[SM_NW + 1];
     uint16_t nh_pos[SM_NHMAX];
     uint32_t nh_cnt;
     uint32_t s_dupheavy;  // the previous bin of this CTA was duplicate-heavy
-    unsigned long long mbar;
-    uint64_t s_bin[3];
-    BinMeta meta[3];      // previous / current / next work bin (ring)
+    unsigned long long mbar[SM_NBUF];  // TMA completion, one per buffer
+    uint32_t pend_U[SM_NBUF];          // merged count of the sorted bin in each buffer
+    uint64_t s_bin[SM_NMETA];
+    BinMeta meta[SM_NMETA];            // descriptor ring (CTA-local bin sequence)
     Parked pk[PK_MAX];    // parked bins (ring, oldest first)
     uint64_t pk_P[PK_MAX];
     uint64_t s_pbP;
@@ -211,52 +229,71 @@ __device__ __forceinline__ void issue_tma(const SortArgs& a, SortSmem& sm, int b
     const uint32_t kb = static_cast<uint32_t>((m.n * 4 + 15) & ~15ull);
     const uint32_t vb = static_cast<uint32_t>((m.n * 8 + 15) & ~15ull);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&sm.mbar, kb + vb);
-    bulk_g2s(sm.k[buf], ks + m.off, kb, &sm.mbar);
-    bulk_g2s(sm.v[buf], vs + m.off, vb, &sm.mbar);
+    mbar_expect_tx(&sm.mbar[buf], kb + vb);
+    bulk_g2s(sm.k[buf], ks + m.off, kb, &sm.mbar[buf]);
+    bulk_g2s(sm.v[buf], vs + m.off, vb, &sm.mbar[buf]);
 }
 
 __device__ __forceinline__ uint32_t elem_idx(int it) {
     return (threadIdx.x >> 5) * SM_PER_WARP + it * 32 + (threadIdx.x & 31);
 }
 
-// Exclusive scan of the SM_NB counters in index order (8 per thread).
-// Returns the number of tuples sitting 4th or later in their bucket (~2 % of
-// a bin of distinct uniform keys, most of a duplicate-heavy one).
+// Exclusive scan of the SM_NB u16 counters (two per word, 16 per thread) in
+// index order. Returns the number of tuples sitting 4th or later in their
+// bucket (< 1 % of a bin of distinct uniform keys, most of a duplicate-heavy
+// one).
 __device__ __forceinline__ uint32_t scan_cnt(SortSmem& sm) {
     const int tid = threadIdx.x;
-    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + 2 * tid;
-    const uint4 lo = c4[0], hi = c4[1];
-    const uint32_t c8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    uint32_t s8 = 0, crowd = 0;
+    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + (SM_WPT / 4) * tid;
+    uint32_t w8[SM_WPT];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        s8 += c8[j];
-        crowd += c8[j] > 3 ? c8[j] - 3 : 0;
+    for (int q = 0; q < SM_WPT / 4; ++q) {
+        const uint4 x = c4[q];
+        w8[4 * q] = x.x;
+        w8[4 * q + 1] = x.y;
+        w8[4 * q + 2] = x.z;
+        w8[4 * q + 3] = x.w;
+    }
+    uint32_t s = 0, crowd = 0;
+#pragma unroll
+    for (int j = 0; j < SM_WPT; ++j) {
+        const uint32_t c0 = w8[j] & 0xffffu, c1 = w8[j] >> 16;
+        s += c0 + c1;
+        crowd += (c0 > 3 ? c0 - 3 : 0) + (c1 > 3 ? c1 - 3 : 0);
     }
     uint32_t tot;  // counts <= SM_CAP < 2^16: both sums in one scan
-    uint32_t run = block_exclusive_scan<SM_NT>(crowd << 16 | s8, sm.s_warp32, tot) & 0xffffu;
-    uint32_t o[8];
+    uint32_t run = block_exclusive_scan<SM_NT>(crowd << 16 | s, sm.s_warp32, tot) & 0xffffu;
+    uint32_t o[SM_WPT];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        o[j] = run;
-        run += c8[j];
+    for (int j = 0; j < SM_WPT; ++j) {
+        const uint32_t c0 = w8[j] & 0xffffu, c1 = w8[j] >> 16;
+        o[j] = run | (run + c0) << 16;
+        run += c0 + c1;
     }
-    c4[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    c4[1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+    for (int q = 0; q < SM_WPT / 4; ++q) c4[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
     return tot >> 16;
 }
 
+// u16 counter d of the packed bucket array
+__device__ __forceinline__ uint32_t cnt_get(const SortSmem& sm, uint32_t d) {
+    return (sm.cnt[d >> 1] >> ((d & 1) * 16)) & 0xffffu;
+}
+__device__ __forceinline__ uint32_t cnt_inc(SortSmem& sm, uint32_t d) {
+    const uint32_t sh = (d & 1) * 16;
+    return (atomicAdd(&sm.cnt[d >> 1], 1u << sh) >> sh) & 0xffffu;
+}
+
 __device__ __forceinline__ void zero_cnt(SortSmem& sm) {
-    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + 2 * threadIdx.x;
-    c4[0] = make_uint4(0, 0, 0, 0);
-    c4[1] = make_uint4(0, 0, 0, 0);
+    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + (SM_WPT / 4) * threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < SM_WPT / 4; ++q) c4[q] = make_uint4(0, 0, 0, 0);
 }
 
 // Stable LSD radix sort of K/V[0, n) in place (the tuples are staged in
-// registers, element layout elem_idx) over `bits` key bits, 8-bit digits.
-// Ranks from match.any per warp in element order, per-(warp, digit) counters
-// cnt[w*256+d] scanned digit-major.
+// registers, element layout elem_idx) over `bits` key bits, LSD_BITS-bit
+// digits. Ranks from match.any per warp in element order, per-(warp, digit)
+// counters cnt[w*LSD_ND+d] scanned digit-major.
 __device__ __noinline__ void lsd_sort(SortSmem& sm, uint32_t* K, double* V, uint32_t n, int bits,
                                       uint32_t keylo) {
     const int tid = threadIdx.x, w = tid >> 5;
@@ -270,15 +307,15 @@ __device__ __noinline__ void lsd_sort(SortSmem& sm, uint32_t* K, double* V, uint
         kr[it] = idx < n ? K[idx] : 0u;
         vr[it] = idx < n ? V[idx] : 0.0;
     }
-    for (int shift = 0; shift < bits; shift += 8) {
+    for (int shift = 0; shift < bits; shift += LSD_BITS) {
         zero_cnt(sm);
         __syncthreads();
         uint32_t rd[SM_ITEMS];  // rank << 9 | digit
-        uint32_t* wc = sm.cnt + w * 256;
+        uint32_t* wc = sm.cnt + w * LSD_ND;
 #pragma unroll
         for (int it = 0; it < SM_ITEMS; ++it) {
             const bool valid = elem_idx(it) < n;
-            const uint32_t d = valid ? (((kr[it] - keylo) >> shift) & 0xffu) : 0x100u;
+            const uint32_t d = valid ? (((kr[it] - keylo) >> shift) & (LSD_ND - 1)) : 0x100u;
             const uint32_t peers = __match_any_sync(FULL, d);
             const uint32_t old = valid ? wc[d] : 0;
             rd[it] = (old + __popc(peers & lt)) << 9 | d;
@@ -288,20 +325,20 @@ __device__ __noinline__ void lsd_sort(SortSmem& sm, uint32_t* K, double* V, uint
         }
         __syncthreads();
         {  // digit-major exclusive scan over (digit, warp)
-            constexpr int PER = SM_NW * 256 / SM_NT;  // counters per thread
-            constexpr int TPD = SM_NW / PER;          // threads per digit
+            constexpr int PER = SM_NW * LSD_ND / SM_NT;  // counters per thread
+            constexpr int TPD = SM_NW / PER;             // threads per digit
             const int d = tid / TPD, w0 = (tid % TPD) * PER;
             uint32_t c[PER], s = 0;
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
-                c[j] = sm.cnt[(w0 + j) * 256 + d];
+                c[j] = sm.cnt[(w0 + j) * LSD_ND + d];
                 s += c[j];
             }
             uint32_t tot;
             uint32_t run = block_exclusive_scan<SM_NT>(s, sm.s_warp32, tot);
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
-                sm.cnt[(w0 + j) * 256 + d] = run;
+                sm.cnt[(w0 + j) * LSD_ND + d] = run;
                 run += c[j];
             }
         }
@@ -402,7 +439,7 @@ __device__ __noinline__ uint32_t hash_premerge(SortSmem& sm, uint32_t* K, double
     for (int it = 0; it < SM_ITEMS; ++it) {
         if (elem_idx(it) < n) {
             const uint32_t key = kr[it];
-            uint32_t h = (key * 0x9E3779B1u) >> (32 - SM_NB_BITS);
+            uint32_t h = (key * 0x9E3779B1u) >> (32 - __builtin_ctz(SM_CAP));
             while (true) {
                 const uint32_t old = atomicCAS(&K[h], 0xffffffffu, key);
                 if (old == 0xffffffffu || old == key) {
@@ -449,6 +486,9 @@ struct OutHook {
     uint64_t pb;
     uint64_t pst;   // thread 0: status word of pb (loaded early)
     uint64_t pk0, pk1;  // thread 0: status words of the two oldest parked bins
+    uint32_t tk;        // thread 0: ticket of the CTA's next work bin
+    int mn;             // its descriptor slot
+    bool fetched;       // its descriptor fetch was issued inside the sort
 };
 
 // Thread 0: decide the output phase from the status words. Parked bins whose
@@ -551,10 +591,10 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
 #pragma unroll
     for (int it = 0; it < SM_ITEMS; ++it) {
         slot[it] = 0;
-        if (elem_idx(it) < n) slot[it] = atomicAdd(&sm.cnt[(kr[it] - keylo) >> sh], 1u);
+        if (elem_idx(it) < n) slot[it] = cnt_inc(sm, (kr[it] - keylo) >> sh);
     }
     __syncthreads();
-    uint32_t crowded = scan_cnt(sm);  // cnt[d] = start of bucket d
+    uint32_t crowded = scan_cnt(sm);  // counter d = start of bucket d
     PROF_MARK(1);
     if (crowded * 4 >= n && n >= 256 && !pm) {
         // duplicate-heavy: pre-merge, then start over on the distinct keys
@@ -575,50 +615,44 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
 #pragma unroll
         for (int it = 0; it < SM_ITEMS; ++it) {
             slot[it] = 0;
-            if (elem_idx(it) < n) slot[it] = atomicAdd(&sm.cnt[(kr[it] - keylo) >> sh], 1u);
+            if (elem_idx(it) < n) slot[it] = cnt_inc(sm, (kr[it] - keylo) >> sh);
         }
         __syncthreads();
         scan_cnt(sm);
+    }
+    // values of this thread's tuples (input order) before anything moves
+#pragma unroll
+    for (int it = 0; it < SM_ITEMS; ++it) {
+        const uint32_t idx = elem_idx(it);
+        vr[it] = idx < n ? V[idx] : 0.0;
     }
     __syncthreads();
 #if defined(PBG_DIAG_SORT) && PBG_DIAG_SORT == 2
     return n;
 #endif
-    if (sh == 0) {
-        // a bucket is a single key: bucket order is sorted order, nothing to
-        // rank (duplicate-heavy key ranges, e.g. RMAT heavy-row pieces)
-        bool dz = false;
-#pragma unroll
-        for (int it = 0; it < SM_ITEMS; ++it) {
-            const uint32_t idx = elem_idx(it);
-            vr[it] = idx < n ? V[idx] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < SM_ITEMS; ++it) {
-            if (elem_idx(it) < n) {
-                dz |= slot[it] != 0;
-                const uint32_t p = slot[it] + sm.cnt[kr[it] - keylo];
-                K[p] = kr[it];
-                V[p] = vr[it];
-            }
-        }
-        if (__syncthreads_or(dz)) return merge_dups_inplace(sm, K, V, n);
-        return n;
-    }
-    // ---- 2. keys to their buckets (every tuple is in registers) ----
+    // ---- 2. tuples to their buckets ----
+    bool dz = false;
 #pragma unroll
     for (int it = 0; it < SM_ITEMS; ++it) {
         if (elem_idx(it) < n) {
-            const uint32_t d = (kr[it] - keylo) >> sh;
-            slot[it] += sm.cnt[d];  // now the tuple's position in bucket order
-            K[slot[it]] = kr[it];
+            dz |= slot[it] != 0;
+            const uint32_t p = slot[it] + cnt_get(sm, (kr[it] - keylo) >> sh);
+            K[p] = kr[it];
+            V[p] = vr[it];
         }
+    }
+    if (sh == 0) {
+        // a bucket is a single key: bucket order is sorted order, nothing to
+        // rank (duplicate-heavy key ranges, e.g. RMAT heavy-row pieces)
+        if (__syncthreads_or(dz)) return merge_dups_inplace(sm, K, V, n);
+        return n;
     }
     __syncthreads();
 #if defined(PBG_DIAG_SORT) && PBG_DIAG_SORT == 3
     return n;
 #endif
+    if (tid == 0) meta_fetch(a, sm, hk.mn, hk.tk, *a.nw_dev);  // lands while this bin sorts
+    hk.fetched = true;
     PROF_MARK(2);
     // previous bin's status, fresh (consumed by decide_output below)
     if (tid == 0) {
@@ -627,51 +661,53 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
         if (c > 0) hk.pk0 = ld_relaxed_gpu(&a.status[sm.pk[sm.pk_head].bin]);
         if (c > 1) hk.pk1 = ld_relaxed_gpu(&a.status[sm.pk[(sm.pk_head + 1) % PK_MAX].bin]);
     }
-    // ---- 3. rank inside the bucket -> sorted position ----
-    // slot = f | eqb << 16: f = lo + (smaller keys) + (equal keys earlier in
-    // the bucket) is the sorted position, eqb > 0 marks a duplicate that is
-    // not the first of its key (a "non-head"). Non-heads are rare (C2: one in
+    // ---- 3. rank inside the bucket, by position ----
+    // Thread-owned positions p (bank-conflict free); the bucket of K[p] is a
+    // few positions around p, so the compare loop and the final write stay
+    // near p too. f = lo + (smaller keys) + (equal keys earlier in the
+    // bucket) is the sorted position; eqb > 0 marks a duplicate that is not
+    // the first of its key (a "non-head"). Non-heads are rare (C2: one in
     // ~9000 tuples): their sorted positions go to a short list, every head
     // computes its merged position u = f - (non-heads before f) and each
     // non-head adds its value into its head's slot — the two-pointer merge
-    // (pb_spgemm.hpp:202-216) without a compaction pass.
+    // (pb_spgemm.hpp:202-216) without a compaction pass. A tuple alone in its
+    // bucket (~60 %) is already in place.
     bool big = false;
+    uint32_t moved = 0;  // bit it: tuple it changes position
 #pragma unroll
     for (int it = 0; it < SM_ITEMS; ++it) {
-        if (elem_idx(it) < n) {
-            const uint32_t key = kr[it];
+        const uint32_t p = elem_idx(it);
+        slot[it] = p;
+        if (p < n) {
+            const uint32_t key = K[p];
+            kr[it] = key;
             const uint32_t d = (key - keylo) >> sh;
-            const uint32_t lo = sm.cnt[d];
-            const uint32_t hi = d + 1 < SM_NB ? sm.cnt[d + 1] : n;
-            const uint32_t pos = slot[it];
-            uint32_t lt = 0, eqb = 0;
-            if (hi - lo == 2) {  // ~37 % of tuples (Poisson(1) buckets): no loop
-                const uint32_t j = pos == lo ? lo + 1 : lo;
-                const uint32_t kj = K[j];
-                lt = kj < key;
-                eqb = (kj == key) & (j < pos);
-            } else if (hi - lo > SM_BMAX) {
-                big = true;
-            } else if (hi - lo > 2) {
+            const uint32_t w = sm.cnt[d >> 1];
+            const uint32_t lo = (w >> ((d & 1) * 16)) & 0xffffu;
+            const uint32_t hi = (d & 1) ? (d + 1 < SM_NB ? (sm.cnt[(d + 1) >> 1] & 0xffffu) : n) : (w >> 16);
+            if (hi - lo > 1) {
+                vr[it] = V[p];
+                if (hi - lo > SM_BMAX) {
+                    big = true;
+                } else {
+                    uint32_t lt = 0, eqb = 0;
 #pragma unroll 1
-                for (uint32_t j = lo; j < hi; ++j) {
-                    const uint32_t kj = K[j];
-                    lt += kj < key;
-                    eqb += (kj == key) & (j < pos);
+                    for (uint32_t j = lo; j < hi; ++j) {
+                        const uint32_t kj = K[j];
+                        lt += kj < key;
+                        eqb += (kj == key) & (j < p);
+                    }
+                    const uint32_t f = lo + lt + eqb;
+                    slot[it] = f | eqb << 16;
+                    moved |= (f != p) << it;
+                    if (eqb) {
+                        moved |= 1u << it;
+                        const uint32_t q = atomicAdd(&sm.nh_cnt, 1u);
+                        if (q < SM_NHMAX) sm.nh_pos[q] = static_cast<uint16_t>(f);
+                    }
                 }
             }
-            const uint32_t f = lo + lt + eqb;
-            slot[it] = f | eqb << 16;
-            if (eqb) {
-                const uint32_t q = atomicAdd(&sm.nh_cnt, 1u);
-                if (q < SM_NHMAX) sm.nh_pos[q] = static_cast<uint16_t>(f);
-            }
         }
-    }
-#pragma unroll
-    for (int it = 0; it < SM_ITEMS; ++it) {
-        const uint32_t idx = elem_idx(it);
-        vr[it] = idx < n ? V[idx] : 0.0;
     }
     PROF_MARK(7);
     // the output decision for the previous bin rides on this barrier
@@ -684,10 +720,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
     return n;
 #endif
     if (any_big) {
-        // clustered keys: stable LSD radix sort (keys back in input order)
-#pragma unroll
-        for (int it = 0; it < SM_ITEMS; ++it)
-            if (elem_idx(it) < n) K[elem_idx(it)] = kr[it];
+        // clustered keys: stable LSD radix sort of the bucket-ordered bin
         lsd_sort(sm, K, V, n, bits, keylo);
         if (tid == 0) atomicAdd(a.fallbacks, 1ull);
         bool d2 = false;
@@ -703,14 +736,21 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
     if (nh == 0) {
 #pragma unroll
         for (int it = 0; it < SM_ITEMS; ++it) {
-            if (elem_idx(it) < n) {
+            if ((moved >> it) & 1u) {
                 K[slot[it]] = kr[it];
                 V[slot[it]] = vr[it];
             }
         }
         return n;
     }
+    // tuples that stay in place need their value for the merged write
+#pragma unroll
+    for (int it = 0; it < SM_ITEMS; ++it) {
+        const uint32_t p = elem_idx(it);
+        if (p < n && !((moved >> it) & 1u)) vr[it] = V[p];
+    }
     if (nh > SM_NHMAX) {  // many duplicates: sorted write, then a merge pass
+        __syncthreads();
 #pragma unroll
         for (int it = 0; it < SM_ITEMS; ++it) {
             if (elem_idx(it) < n) {
@@ -722,6 +762,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
         return merge_dups_inplace(sm, K, V, n);
     }
     // heads at their merged positions, then non-heads add into their head
+    __syncthreads();
 #pragma unroll
     for (int it = 0; it < SM_ITEMS; ++it) {
         if (elem_idx(it) < n && (slot[it] >> 16) == 0) {
@@ -758,11 +799,19 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
     double* ovals = a.cval + P;
 #if !(defined(PBG_DIAG_SORT) && PBG_DIAG_SORT == 5)
     for (uint32_t u = tid; u < U; u += SM_NT) {
+#ifdef PBG_PLAIN_ST
+        okeys[u] = K[u] & colmask;
+        ovals[u] = V[u];
+#else
         __stcs(okeys + u, K[u] & colmask);
         __stcs(ovals + u, V[u]);
+#endif
     }
 #endif
     // rowptr[rs + r] = P + first merged entry of local row r (binary search)
+#if defined(PBG_DIAG_SORT) && PBG_DIAG_SORT == 6
+    span = 0;
+#endif
     for (uint32_t r = tid; r < span; r += SM_NT) {
         const uint64_t target = static_cast<uint64_t>(r) << cb;
         uint32_t lo = 0, hi = U;
@@ -938,7 +987,7 @@ __device__ void output_phase(const SortArgs& a, SortSmem& sm, const OutHook& h, 
     }
 }
 
-__global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
+__global__ void __launch_bounds__(SM_NT, SM_NT >= 1024 ? 1 : 1024 / SM_NT) k_sortmerge(SortArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -947,38 +996,42 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         if (tid < 32) status_scanner(a.status, nw);
         return;
     }
-
+    // CTA-local bin sequence j = 0, 1, ...: bin j lives in buffer j % SM_NBUF
+    // and descriptor slot j % SM_NMETA. Iteration i sorts bin i, writes bin
+    // i - SM_LAG and starts the copy of bin i + SM_PF + 1 into the buffer
+    // that frees up.
     if (tid == 0) {
-        mbar_init(&sm.mbar, 1);
+        for (int q = 0; q < SM_NBUF; ++q) mbar_init(&sm.mbar[q], 1);
         sm.s_dupheavy = 0;
         sm.pk_head = 0;
         sm.pk_count = 0;
-        meta_fetch(a, sm, 0, atomicAdd(a.ticket, 1u), nw);
+        for (int j = 0; j <= SM_PF; ++j) meta_fetch(a, sm, j, atomicAdd(a.ticket, 1u), nw);
         cp_async_wait_all();
-        if (sm.s_bin[0] < nw && bin_kind(sm.meta[0]) == 1) issue_tma(a, sm, 0, sm.meta[0]);
+        for (int j = 0; j <= SM_PF; ++j)
+            if (sm.s_bin[j] < nw && bin_kind(sm.meta[j]) == 1) issue_tma(a, sm, j, sm.meta[j]);
     }
     __syncthreads();
-    uint32_t parity = 0;
     long long prof_t = clock64();
     (void)prof_t;
-    int cur = 0;                 // buffer of the current work bin
-    int mp = 2, mc = 0, mn = 1;  // descriptor ring: previous, current, next
-    bool have_prev = false;      // a sorted bin waits in buffer cur ^ 1
-    uint64_t pb = 0;
-    uint32_t pU = 0;
-
-    while (true) {
+    uint32_t phase_bits = 0;  // mbarrier parity per buffer
+    uint32_t i = 0;
+    for (;; ++i) {
+        const int cur = i % SM_NBUF, mc = i % SM_NMETA;
         const uint64_t b = sm.s_bin[mc];
         if (b >= nw) break;
         const BinMeta& M = sm.meta[mc];
         const uint32_t kind = bin_kind(M);
-        // the previous bin's status (its prefix is usually there by now) and
-        // the ticket of the bin after this one, both consumed later
+        const bool have_prev = i >= SM_LAG;
+        const int pbuf = (i + SM_NBUF - SM_LAG) % SM_NBUF;   // buffer of bin i - LAG
+        const int pm = (i + SM_NMETA - SM_LAG) % SM_NMETA;   // its descriptor
+        const uint64_t pb = have_prev ? sm.s_bin[pm] : 0;
+        const uint32_t pU = have_prev ? sm.pend_U[pbuf] : 0;
+        // bin i - LAG's status (its prefix is usually there by now) and the
+        // ticket of bin i + PF + 1, both consumed later
         OutHook hk{have_prev, false, pU, pb,
-                   (have_prev && tid == 0) ? ld_relaxed_gpu(&a.status[pb]) : 0, 0, 0};
-#ifndef PBG_LATE_TICKET
-        const uint32_t tk = tid == 0 ? atomicAdd(a.ticket, 1u) : 0u;
-#endif
+                   (have_prev && tid == 0) ? ld_relaxed_gpu(&a.status[pb]) : 0, 0, 0,
+                   tid == 0 ? atomicAdd(a.ticket, 1u) : 0u, static_cast<int>((i + SM_PF + 1) % SM_NMETA),
+                   false};
         if (tid == 0 && M.n > SM_CAP && !(M.flags & 2u)) atomicOr(a.err, 2u);
         uint32_t U = 0;
         if (kind) {
@@ -986,14 +1039,14 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             zero_cnt(sm);
             if (tid == 0) sm.nh_cnt = 0;
             if (kind == 1) {
-                mbar_wait(&sm.mbar, parity);
-                parity ^= 1;
+                mbar_wait(&sm.mbar[cur], (phase_bits >> cur) & 1u);
+                phase_bits ^= 1u << cur;
             } else {  // unaligned heavy sub-bin: plain coalesced loads
                 const uint32_t* ks = ((M.flags & 1u) ? a.skeys : a.keys) + M.off;
                 const double* vs = ((M.flags & 1u) ? a.svals : a.vals) + M.off;
-                for (uint32_t i = tid; i < n; i += SM_NT) {
-                    sm.k[cur][i] = ks[i];
-                    sm.v[cur][i] = vs[i];
+                for (uint32_t e = tid; e < n; e += SM_NT) {
+                    sm.k[cur][e] = ks[e];
+                    sm.v[cur][e] = vs[e];
                 }
             }
             __syncthreads();
@@ -1008,30 +1061,30 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         }
         PROF_MARK(9);
         if (tid == 0) {
-            // publish this bin's count now; its output goes out one bin later
-            st_release_gpu(&a.status[b], (b == 0 ? ST_INC : ST_AGG) | (U & ST_VAL));
+            // publish this bin's count now (a count needs no ordering with
+            // other memory: relaxed); its output goes out SM_LAG bins later
+            st_relaxed_gpu(&a.status[b], (b == 0 ? ST_INC : ST_AGG) | (U & ST_VAL));
             atomicAdd(a.merged_total, (unsigned long long)U);
-#ifdef PBG_LATE_TICKET
-            const uint32_t tk = atomicAdd(a.ticket, 1u);
-#endif
-            meta_fetch(a, sm, mn, tk, nw);  // the next bin's descriptor
+            sm.pend_U[cur] = U;
+            if (!hk.fetched) meta_fetch(a, sm, hk.mn, hk.tk, nw);
         }
-        output_phase(a, sm, hk, mp, cur ^ 1, nw, false);
+        output_phase(a, sm, hk, pm, pbuf, nw, false);
         PROF_MARK(5);
-        if (tid == 0 && sm.s_bin[mn] < nw && bin_kind(sm.meta[mn]) == 1)
-            issue_tma(a, sm, cur ^ 1, sm.meta[mn]);
-        have_prev = true;
-        pb = b;
-        pU = U;
-        cur ^= 1;
-        const int t = mp;
-        mp = mc;
-        mc = mn;
-        mn = t;
+        // the buffer just written out receives bin i + PF + 1
+        if (tid == 0 && sm.s_bin[hk.mn] < nw && bin_kind(sm.meta[hk.mn]) == 1)
+            issue_tma(a, sm, pbuf, sm.meta[hk.mn]);
     }
-    {
-        OutHook hk{have_prev, false, pU, pb, 0, 0, 0};
-        output_phase(a, sm, hk, mp, cur ^ 1, nw, true);
+    // drain: the last SM_LAG sorted bins, then every parked bin
+    for (int q = SM_LAG; q >= 1; --q) {
+        if (i < static_cast<uint32_t>(q)) continue;
+        const uint32_t j = i - q;
+        const int pbuf = j % SM_NBUF, pm = j % SM_NMETA;
+        OutHook hk{true, false, sm.pend_U[pbuf], sm.s_bin[pm], 0, 0, 0, 0, 0, true};
+        output_phase(a, sm, hk, pm, pbuf, nw, q == 1);
+    }
+    if (i == 0 || SM_LAG == 0) {
+        OutHook hk{false, false, 0, 0, 0, 0, 0, 0, 0, true};
+        output_phase(a, sm, hk, 0, 0, nw, true);
     }
 }
 
