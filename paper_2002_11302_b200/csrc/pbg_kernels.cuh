@@ -333,19 +333,17 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ void st_tuple_key(uint32_t* p, uint32_t v) {
+__device__ __forceinline__ void st_tuple_key(uint32_t* p, uint32_t v, uint64_t pol) {
 #if PBG_EXP_EVICT_LAST
-    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v),
-                 "l"(l2_evict_last_policy())
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol)
                  : "memory");
 #else
     *p = v;
 #endif
 }
-__device__ __forceinline__ void st_tuple_val(double* p, double v) {
+__device__ __forceinline__ void st_tuple_val(double* p, double v, uint64_t pol) {
 #if PBG_EXP_EVICT_LAST
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v),
-                 "l"(l2_evict_last_policy())
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
                  : "memory");
 #else
     *p = v;
@@ -378,6 +376,7 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t lt = lanemask_lt();
     const int cb = a.col_bits;
+    const uint64_t pol = l2_evict_last_policy();
 
     for (uint64_t c = gw; c < a.nchunks; c += nw) {
         uint64_t p = a.chunk_p0[c];
@@ -480,8 +479,8 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
                     if (ok[u])
 #endif
                     {
-                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u]);
-                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u]);
+                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u], pol);
+                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u], pol);
                     }
                 }
             }

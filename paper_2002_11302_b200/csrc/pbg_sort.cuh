@@ -64,6 +64,12 @@ constexpr int SM_NBW = SM_NB / 2;             // counter words
 #define PBG_SM_BMAX 128
 #endif
 constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
+#ifndef PBG_SM_BMAX_PM
+#define PBG_SM_BMAX_PM 128
+#endif
+// after a hash pre-merge the distinct keys of banded rows cluster in a few
+// buckets (stencil: 25 columns within +-258 of each other): LSD radix instead
+constexpr int SM_BMAX_PM = PBG_SM_BMAX_PM;
 constexpr int SM_ITEMS = SM_CAP / SM_NT;      // tuples per thread
 constexpr int SM_PER_WARP = SM_CAP / SM_NW;   // warp-contiguous element layout
 constexpr int SM_WPT = SM_NBW / SM_NT;        // counter words per thread in the scan
@@ -599,6 +605,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
     if (crowded * 4 >= n && n >= 256 && !pm) {
         // duplicate-heavy: pre-merge, then start over on the distinct keys
         __syncthreads();
+        pm = true;
         const uint32_t u = hash_premerge(sm, K, V, n);
         if (tid == 0) {
             atomicAdd(a.premerged, 1ull);
@@ -687,7 +694,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int buf, uin
             const uint32_t hi = (d & 1) ? (d + 1 < SM_NB ? (sm.cnt[(d + 1) >> 1] & 0xffffu) : n) : (w >> 16);
             if (hi - lo > 1) {
                 vr[it] = V[p];
-                if (hi - lo > SM_BMAX) {
+                if (hi - lo > (pm ? SM_BMAX_PM : SM_BMAX)) {
                     big = true;
                 } else {
                     uint32_t lt = 0, eqb = 0;
@@ -987,7 +994,10 @@ __device__ void output_phase(const SortArgs& a, SortSmem& sm, const OutHook& h, 
     }
 }
 
-__global__ void __launch_bounds__(SM_NT, SM_NT >= 1024 ? 1 : 1024 / SM_NT) k_sortmerge(SortArgs a) {
+#ifndef PBG_SM_MINB
+#define PBG_SM_MINB (SM_NT >= 1024 ? 1 : 1024 / SM_NT)
+#endif
+__global__ void __launch_bounds__(SM_NT, PBG_SM_MINB) k_sortmerge(SortArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x;
