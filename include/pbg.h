@@ -75,15 +75,13 @@ typedef struct pbg_config {
     /* reserved[0]: cap on tuples per round of the host path (0 = from free
      * HBM); when flop exceeds it, pbg_multiply_begin runs flop-balanced row
      * bands one after another and assembles C on the host.
-     * reserved[1]: force the number of expand row bands (0 = auto).
-     * reserved[2]: test hook, 1 = the sort kernel parks every sorted bin it
-     * can (exercises the deferred-output path deterministically). */
+     * reserved[1]: force the number of expand row bands (0 = auto). */
     uint64_t reserved[4];
 } pbg_config;
 
 /* spgemm::PhaseReport times (report.hpp:26-33) measured with CUDA events,
  * plus the acceptance counters (acceptance.cpp:46-58). t_sort covers the
- * work-bin list (with the heavy-row split) and the fused sort+merge+CSR
+ * per-bin distinct count, the offset scan and the fused sort+merge+CSR
  * kernel; t_compress and t_convert are 0 (fused). */
 typedef struct pbg_report {
     double t_symbolic, t_expand, t_sort, t_compress, t_convert, t_total; /* seconds */
@@ -98,8 +96,8 @@ typedef struct pbg_report {
     uint64_t tuple_bytes;      /* bytes of tuple storage (12 B per tuple + pad)   */
     uint64_t sort_fallbacks;   /* bins sorted by the LSD fallback (clustered keys) */
     uint32_t expand_bands;     /* row bands the expand ran in (L2 write frontier) */
-    uint32_t premerged_bins;   /* duplicate-heavy bins pre-merged in the sort's hash */
-    double t_count;            /* work-bin list + heavy-row split (in t_sort)     */
+    uint32_t pad0;
+    double t_count;            /* per-bin distinct-key count + offset scan (in t_sort) */
     double t_sortmerge_kernel; /* the sort+merge+CSR kernel alone (in t_sort)     */
 } pbg_report;
 

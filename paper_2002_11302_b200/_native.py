@@ -49,7 +49,7 @@ class Report(C.Structure):
                 ("tuples_into_sort", u64), ("merged_total", u64),
                 ("nbins", u32), ("gpu_bins", u32), ("heavy_bins", u32), ("bin_cap", u32),
                 ("tuple_bytes", u64), ("sort_fallbacks", u64),
-                ("expand_bands", u32), ("premerged_bins", u32),
+                ("expand_bands", u32), ("pad0", u32),
                 ("t_count", f64), ("t_sortmerge_kernel", f64)]
 
     def as_dict(self) -> dict:

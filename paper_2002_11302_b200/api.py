@@ -56,7 +56,6 @@ class PbConfig:
     bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
     max_round_tuples: int = 0  # host path: tuples per bounded-memory round (0 = from free HBM)
     expand_bands: int = 0  # row bands of the expand (0 or 1 = one pass, the default)
-    force_park: bool = False  # test hook: the sort kernel defers every bin's output it can
 
     def to_c(self) -> _native.Config:
         c = _native.Config()
@@ -66,7 +65,6 @@ class PbConfig:
         c.device, c.bin_cap = self.device, self.bin_cap
         c.reserved[0] = self.max_round_tuples
         c.reserved[1] = self.expand_bands
-        c.reserved[2] = int(self.force_park)
         return c
 
 

@@ -85,8 +85,7 @@ enum Scalar : int {
     S_MERGED_TOTAL,    // sum of merged counts
     S_ERR,             // error bits (u32 in low word)
     S_FALLBACKS,       // bins sorted by the LSD fallback
-    S_PREMERGED,       // bins pre-merged in the sort kernel's hash
-    S_PARKED,          // sorted bins parked before their output offset was known
+    S_NNZ,             // nnz(C) from the distinct-count scan
     S_TILES,           // split tiles of the current heavy level
     S_HEAVY_PAD,       // padded tuples of heavy rows (scratch size)
     S_ITEMS,           // heavy-row items after a split pass
@@ -106,7 +105,7 @@ struct pbg_context {
         in_a_val, in_b_ptr, in_b_idx, in_b_val;
     // heavy rows + work bins
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
-        child_pos, hstat, wcnt, wpos, wb_status;
+        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
     DevBuf items[2][8];
     DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
@@ -129,7 +128,7 @@ struct pbg_context {
                           &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
                           &in_b_idx, &in_b_val, &heavy_excl, &hpad_excl, &bin_hidx, &hbin, &hoff,
                           &hhead, &hcount, &skeys, &svals, &child_cnt, &child_pos, &hstat, &wcnt,
-                          &wpos, &wb_status})
+                          &wpos, &wb_nnz, &wb_out})
             b->release();
         for (auto& set : items)
             for (auto& b : set) b.release();
@@ -358,13 +357,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         if ((rc = grow(ctx->vals, tcap * 8))) return rc;
         // C arrays sized to the flop upper bound (nnz(C) <= flop): no sync
         // for nnz(C) before the sort kernel
-#ifdef PBG_DIAG_NOWAIT
-        if ((rc = grow(ctx->ccol, tcap * 4 + 64))) return rc;
-        if ((rc = grow(ctx->cval, tcap * 8 + 64))) return rc;
-#else
         if ((rc = grow(ctx->ccol, flop * 4))) return rc;
         if ((rc = grow(ctx->cval, flop * 8))) return rc;
-#endif
         CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
         auto* keys = static_cast<uint32_t*>(ctx->keys.p);
         auto* vals = static_cast<double*>(ctx->vals.p);
@@ -446,7 +440,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             k_expand<uint64_t><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         }
         L += 2;
-#if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE)
+#if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE) || defined(PBG_DIAG_REGION)
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(PBG_ERR_INTERNAL, "diagnostic build: stopped after the expand");
 #endif
@@ -573,7 +567,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         const uint64_t wcap = m + 1 + nitems;
         if ((rc = grow(ctx->wcnt, (m + 1) * 8))) return rc;
         if ((rc = grow(ctx->wpos, (m + 2) * 8))) return rc;
-        if ((rc = grow(ctx->wb_status, (wcap + 1) * 8))) return rc;
+        if ((rc = grow(ctx->wb_nnz, (wcap + 1) * 8))) return rc;
+        if ((rc = grow(ctx->wb_out, (wcap + 2) * 8))) return rc;
         {
             const size_t wsz[7] = {8, 8, 4, 4, 4, 4, 4};
             for (int f = 0; f < 7; ++f)
@@ -585,8 +580,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                    static_cast<uint32_t*>(ctx->wb[6].p)};
         auto* wcnt = static_cast<uint64_t*>(ctx->wcnt.p);
         auto* wpos = static_cast<uint64_t*>(ctx->wpos.p);
-        auto* wb_status = static_cast<unsigned long long*>(ctx->wb_status.p);
-        CUDA_TRY(cudaMemsetAsync(wb_status, 0, (wcap + 1) * 8, st));
+        auto* wb_nnz = static_cast<uint64_t*>(ctx->wb_nnz.p);
+        auto* wb_out = static_cast<uint64_t*>(ctx->wb_out.p);
         k_work_count<<<blocks_for(m + 1, 256), 256, 0, st>>>(
             nb_dev, bin_hidx, hcount, cursor, bin_off, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
             reinterpret_cast<unsigned int*>(sc + S_ERR));
@@ -603,6 +598,33 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         }
         const uint64_t* nw_dev = reinterpret_cast<const uint64_t*>(sc + S_NWORK);
 
+        // ---- distinct keys per work bin -> output offset of every work bin ----
+        static bool cnt_attr[64] = {};
+        const size_t cnt_smem = CNT_SLOTS * 4;
+        if (!cnt_attr[ctx->device & 63]) {
+            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(cnt_smem)));
+            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          100));
+            cnt_attr[ctx->device & 63] = true;
+        }
+        int cnt_per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cnt_per_sm, k_bincount, CNT_NT, cnt_smem);
+        if (const char* e = getenv("PBG_CNT_PER_SM")) cnt_per_sm = atoi(e);  // tuning hook
+        k_bincount<<<static_cast<unsigned>(std::min<uint64_t>(
+                         wcap, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
+                     CNT_NT, cnt_smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
+        ++L;
+        // wcap can exceed the m-sized status pool: give this scan its own words
+        {
+            const uint64_t tiles = (wcap + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+            if ((rc = grow(ctx->hstat, tiles * 8 + 64))) return rc;
+            auto* hst = static_cast<unsigned long long*>(ctx->hstat.p);
+            CUDA_TRY(cudaMemsetAsync(hst, 0, tiles * 8 + 64, st));
+            launch_scan(ArrayIn{wb_nnz}, wb_out, 0, nw_dev, wcap, hst + 8,
+                        reinterpret_cast<unsigned int*>(hst), sc + S_NNZ, nullptr, st);
+        }
+        ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
         static bool attr_set[64] = {};
@@ -616,7 +638,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         SortArgs sa{};
         sa.w = w;
         sa.nw_dev = nw_dev;
-        sa.status = wb_status;
+        sa.wb_out = wb_out;
+        sa.wb_nnz = wb_nnz;
         sa.ticket = tickets + 4;
         sa.keys = keys;
         sa.vals = vals;
@@ -630,18 +653,11 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         sa.merged_total = sc + S_MERGED_TOTAL;
         sa.err = reinterpret_cast<unsigned int*>(sc + S_ERR);
         sa.fallbacks = sc + S_FALLBACKS;
-        sa.premerged = sc + S_PREMERGED;
-        sa.parked = sc + S_PARKED;
-        sa.force_park = static_cast<int>(cfg.reserved[2] & 1);
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge, SM_NT, sizeof(SortSmem));
         if (const char* e = getenv("PBG_SORT_PER_SM")) per_sm = atoi(e);  // tuning hook
-        // every CTA must be resident (the last one runs the work-bin scan)
-        const unsigned sm_blocks = static_cast<unsigned>(std::max<uint64_t>(
-            2, std::min<uint64_t>(wcap + 1, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms)));
-        if (getenv("PBG_VERBOSE"))
-            fprintf(stderr, "[pbg] k_sortmerge: %d CTAs/SM, %u CTAs, %zu B smem\n", per_sm, sm_blocks,
-                    sizeof(SortSmem));
+        const unsigned sm_blocks = static_cast<unsigned>(
+            std::min<uint64_t>(wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
 #ifdef PBG_SORT_PROF
         static unsigned long long* prof = nullptr;
         if (!prof) CUDA_TRY(cudaMalloc(&prof, 16 * 8));
@@ -655,13 +671,12 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             unsigned long long hp[16];
             CUDA_TRY(cudaMemcpyAsync(hp, prof, sizeof hp, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
-            const char* names[10] = {"wait_data", "hist_scan", "key_scatter", "rank_barrier",
-                                     "final_write", "flush_write", "tma_sync", "rank_work",
-                                     "prefix_wait", "premerge_mark"};
+            const char* names[7] = {"wait_data", "hist_scan", "scatter", "rank", "dupcheck_merge",
+                                    "write", "end_sync"};
             fprintf(stderr, "[sortprof] us per CTA:");
             double tot = 0;
-            for (int i = 0; i < 10; ++i) {
-                const double us = hp[i] / double(sm_blocks - 1) / 1965.0;
+            for (int i = 0; i < 7; ++i) {
+                const double us = hp[i] / double(sm_blocks) / 1965.0;
                 tot += us;
                 fprintf(stderr, " %s=%.1f", names[i], us);
             }
@@ -678,10 +693,10 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ctx->rep.tuples_into_sort = hs[S_TUPLES_TOTAL];
         ctx->rep.merged_total = hs[S_MERGED_TOTAL];
         ctx->rep.sort_fallbacks = hs[S_FALLBACKS];
-        ctx->rep.premerged_bins = static_cast<uint32_t>(hs[S_PREMERGED]);
-        if (getenv("PBG_VERBOSE")) fprintf(stderr, "[pbg] parked bins: %llu\n", hs[S_PARKED]);
         const unsigned err = static_cast<unsigned>(hs[S_ERR]);
         if (err & 2u) return fail(PBG_ERR_INTERNAL, "a work bin exceeds the shared-memory capacity");
+        if (err & 4u || hs[S_NNZ] != nnz)
+            return fail(PBG_ERR_INTERNAL, "merged counts disagree with the distinct-key counts");
         if (err & 1u || hs[S_TUPLES_TOTAL] != flop)
             return fail(PBG_ERR_INTERNAL, "tuple conservation broken: expanded " +
                                               std::to_string(hs[S_TUPLES_TOTAL]) + " of " +
@@ -898,7 +913,6 @@ int multiply_in_rounds(pbg_handle* h, const pbg_csx_view& a, const pbg_csx_view&
         tot.gpu_bins += r.gpu_bins;
         tot.heavy_bins += r.heavy_bins;
         tot.sort_fallbacks += r.sort_fallbacks;
-        tot.premerged_bins += r.premerged_bins;
         tot.tuple_bytes = std::max(tot.tuple_bytes, r.tuple_bytes);
         tot.bin_cap = r.bin_cap;
     }

@@ -544,4 +544,102 @@ __global__ void k_work_fill_items(const uint64_t* __restrict__ wpos,
     w.flags[q] = (fin.buf[it] ? 1u : 0u) | (fin.kind[it] == IT_MERGED ? 2u : 0u) | 4u;
 }
 
+// ------------------------------------------------------ work-bin counts --
+// Distinct keys per work bin = its merged count (its share of nnz(C)),
+// counted from the keys alone with a shared-memory hash set (load <= 1/8 for
+// a full bin, so probe chains stay short and warps rarely diverge). A scan of
+// these counts gives every work bin its output offset before the sort+merge
+// kernel runs, so bins never wait on each other. Uniform-key items count 1.
+#ifndef PBG_CNT_NT
+#define PBG_CNT_NT 512
+#endif
+constexpr int CNT_NT = PBG_CNT_NT;
+#ifndef PBG_CNT_SLOTS_LOG
+#define PBG_CNT_SLOTS_LOG 14
+#endif
+constexpr int CNT_SLOTS_LOG = PBG_CNT_SLOTS_LOG;
+constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
+constexpr uint32_t CNT_EMPTY = 0xffffffffu;
+constexpr int CNT_PER = 4096 / CNT_NT;  // keys per thread: bins of up to CNT_NT*CNT_PER = 4096 tuples
+
+__device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
+                                         const uint32_t* __restrict__ skeys, const WorkBins& w,
+                                         uint64_t b, uint64_t nw, uint64_t cap, uint32_t (&kk)[CNT_PER],
+                                         uint32_t& n) {
+    n = 0;
+    if (b >= nw) return;
+    const uint32_t fl = w.flags[b];
+    const uint64_t nn = w.n[b];
+    if ((fl & 2u) || nn > cap) return;
+    n = static_cast<uint32_t>(nn);
+    const uint32_t* kb = ((fl & 1u) ? skeys : keys) + w.off[b];
+#pragma unroll
+    for (int j = 0; j < CNT_PER; ++j) {
+        const uint32_t i = threadIdx.x + j * CNT_NT;
+        kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
+    }
+}
+
+__global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict__ keys,
+                                                   const uint32_t* __restrict__ skeys,
+                                                   WorkBins w, const uint64_t* nw_dev,
+                                                   uint64_t cap, uint64_t* wb_nnz) {
+    extern __shared__ __align__(16) uint32_t table[];  // CNT_SLOTS
+    __shared__ uint32_t s_red[2][CNT_NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const uint64_t nw = *nw_dev;
+    for (int i = tid; i < CNT_SLOTS / 4; i += CNT_NT)
+        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
+    __syncthreads();
+    int par = 0;
+    uint32_t kk[CNT_PER], n;
+    uint64_t b = blockIdx.x;
+    cnt_load(keys, skeys, w, b, nw, cap, kk, n);  // software pipeline: keys of bin b
+    for (; b < nw; b += gridDim.x) {
+        uint32_t cur[CNT_PER];
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j) cur[j] = kk[j];
+        const uint32_t ncur = n;
+        const uint32_t fl = w.flags[b];
+        cnt_load(keys, skeys, w, b + gridDim.x, nw, cap, kk, n);  // next bin's keys in flight
+        uint32_t slot[CNT_PER];
+        uint32_t fresh = 0;
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j) {
+            slot[j] = CNT_SLOTS;  // none
+            if (tid + j * CNT_NT < ncur) {
+                const uint32_t key = cur[j];
+                uint32_t h = (key * 0x9E3779B1u) >> (32 - CNT_SLOTS_LOG);
+                while (true) {
+                    const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
+                    if (old == CNT_EMPTY) {
+                        ++fresh;
+                        slot[j] = h;
+                        break;
+                    }
+                    if (old == key) break;
+                    h = (h + 1) & (CNT_SLOTS - 1);
+                }
+            }
+        }
+        fresh = warp_sum(fresh);
+        if (lane == 0) s_red[par][wp] = fresh;
+        __syncthreads();
+        // reset only the slots this thread claimed: the table is clean for the
+        // next bin without a full clear
+#pragma unroll
+        for (int j = 0; j < CNT_PER; ++j)
+            if (slot[j] < CNT_SLOTS) table[slot[j]] = CNT_EMPTY;
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int i = 0; i < CNT_NT / 32; ++i) t += s_red[par][i];
+            // merged items are already distinct; a valid list has no other
+            // bin above the capacity
+            wb_nnz[b] = (fl & 2u) ? w.n[b] : t;
+        }
+        par ^= 1;
+        __syncthreads();
+    }
+}
+
 }  // namespace pbg

@@ -466,6 +466,8 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
                     avv[u] = s_av[w][ri];
 #ifdef PBG_DIAG_SEQSTORE
                     dv[u] = (tpos + t) % (1ull << 28);
+#elif defined(PBG_DIAG_REGION)  // timing experiment: the same scatter folded into 2^R tuples
+                    dv[u] = (s_dst[w][ri] + q) & ((1ull << PBG_DIAG_REGION) - 1);
 #else
                     dv[u] = s_dst[w][ri] + q;
 #endif

@@ -14,6 +14,6 @@ done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_C2.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
 # full sections of the three top kernels (second multiply)
-ncu --set full --clock-control none --import-source on -k regex:"k_expand|k_sortmerge" \
+ncu --set full --clock-control none --import-source on -k regex:"k_expand|k_bincount|k_sortmerge" \
   -s 3 -c 3 -o $O/full_C2 python scripts/profile_step.py --config C2 --steps 1 > /dev/null 2>&1
 echo done

@@ -41,7 +41,7 @@ def test_kernels_are_sm100a_with_tma():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(so)],
                          capture_output=True, text=True, check=True).stdout
     assert "sm_100a" in out
-    for k in ("k_expand", "k_sortmerge", "k_scan"):
+    for k in ("k_expand", "k_sortmerge", "k_bincount", "k_scan"):
         assert k in out, k
     assert "UBLKCP" in out
 

@@ -90,23 +90,6 @@ def test_random_sweep_vs_oracle(seed):
     assert_valid_csr(res.c)
 
 
-@pytest.mark.parametrize("seed", range(12))
-def test_parked_output_path(seed):
-    """Bins whose output offset is not yet known when their buffer is needed
-    are parked in their own tuple range and written later (pbg_sort.cuh
-    output_phase); the test hook parks every bin it can, including heavy-row
-    pieces (small bin caps) and merged heavy sub-bins."""
-    rng = np.random.default_rng(77 + seed)
-    scale = int(rng.integers(6, 12))
-    kind = ["er", "rmat"][seed % 2]
-    csr = M.make_matrix(kind, scale, int(rng.integers(3, 17)), seed=seed)
-    a = M.csr_to_csc(csr)
-    cap = [0, 256, 1024][seed % 3]
-    res = gpu(a, csr, bin_cap=cap, force_park=True)
-    check_vs(res, oracle.multiply(a, csr))
-    assert_valid_csr(res.c)
-
-
 def test_rectangular():
     r, c = M.gen_er(9, 4, 5)
     a = M.coo_to_csr(512, 512, r, c)
