@@ -411,7 +411,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         // short runs (ER, stencil): the scattered run stores bound the kernel
         // and 2 CTAs per SM issue them best (measured 3-6 % faster than 8);
         // long runs (RMAT) stream B and want every warp
-        unsigned exp_blocks = (flop < 64 * nnz_a ? 2u : 8u) * ctx->num_sms;
+        const bool long_runs = flop >= 64 * nnz_a;
+        unsigned exp_blocks = (long_runs ? 8u : 2u) * ctx->num_sms;
         if (const char* e = getenv("PBG_EXP_BLOCKS")) exp_blocks = static_cast<unsigned>(atoi(e));  // tuning hook
         const uint64_t warps = static_cast<uint64_t>(exp_blocks) * EXP_NW;
         uint64_t ch = 256;
@@ -433,11 +434,13 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         if (pack32) {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
                                                          static_cast<uint32_t*>(ctx->row_pack.p));
-            k_expand<uint32_t><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            if (long_runs) k_expand<uint32_t, 4><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            else k_expand<uint32_t, PBG_EXP_MINB><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         } else {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
                                                          static_cast<uint64_t*>(ctx->row_pack.p));
-            k_expand<uint64_t><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            if (long_runs) k_expand<uint64_t, 4><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            else k_expand<uint64_t, PBG_EXP_MINB><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         }
         L += 2;
 #if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE) || defined(PBG_DIAG_REGION)

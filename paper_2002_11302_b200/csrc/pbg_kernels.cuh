@@ -362,10 +362,13 @@ constexpr int EXP_NW = EXP_NT / 32;
 // role of the reference's thread-private local bins: each bin's write
 // frontier stays resident until its lines are full.
 #ifndef PBG_EXP_MINB
-#define PBG_EXP_MINB 4
+#define PBG_EXP_MINB 2
 #endif
-template <typename P>
-__global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
+// MINB: resident CTAs per SM the register budget is sized for — 2 for short
+// runs (ER, stencil: 128 registers, deeper batch pipeline), 4 for long runs
+// (RMAT: more warps streaming B rows).
+template <typename P, int MINB>
+__global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
     __shared__ uint64_t s_dst[EXP_NW][32];
     __shared__ uint64_t s_bst[EXP_NW][32];
     __shared__ double s_av[EXP_NW][32];
@@ -386,44 +389,78 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
         const uint64_t pend = a.chunk_p0[c + 1];
         if (p >= pend) continue;
         uint64_t kcur = warp_last_le(a.a_colptr, 0, a.a_ncols, p);
+        // Software pipeline over batches of 32 runs: batch t+1's loads (row
+        // id, value, column window, then packed bin and B row bounds) are
+        // issued while batch t's tuples stream out, so only the bin-cursor
+        // atomic's round trip remains exposed per batch.
+        double av_n = 0.0;
+        uint32_t rid_n = 0;
+        uint64_t bnd_n;
+        {
+            const uint64_t pl = p + lane;
+            if (pl < pend) {
+                av_n = a.a_vals[pl];
+                rid_n = a.a_rowids[pl];
+            }
+            const uint64_t bi = kcur + 1 + lane;
+            bnd_n = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
+        }
+        P pack_n = 0;
+        uint64_t kl_n = 0, bst_n = 0, bend_n = 0;
+        bool staged = false;  // pack_n / kl_n / bst_n hold the batch at p
         while (p < pend) {
             const uint64_t pl = p + lane;
             const bool valid = pl < pend;
-            // the run's row, value and packed bin are independent of its
-            // column: issued first so their latency overlaps the search
-            P pack = 0;
-            double av = 0.0;
-            if (valid) {
-                av = a.a_vals[pl];
-                pack = static_cast<const P*>(a.row_pack)[a.a_rowids[pl]];
-            }
-            // column of run pl: kcur + #{j : colptr[kcur+1+j] <= pl}
-            const uint64_t bi = kcur + 1 + lane;
-            const uint64_t bnd = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
-            int cnt = 0;
+            // ---- stage 2 of this batch (unless done during the last tuple loop)
+            if (!staged) {
+                if (valid) pack_n = static_cast<const P*>(a.row_pack)[rid_n];
+                int cnt = 0;
 #pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-                const uint64_t v = __shfl_sync(FULL, bnd, cnt + s - 1);
-                if (v <= pl) cnt += s;
+                for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                    const uint64_t v = __shfl_sync(FULL, bnd_n, cnt + s2 - 1);
+                    if (v <= pl) cnt += s2;
+                }
+                {
+                    const uint64_t v = __shfl_sync(FULL, bnd_n, cnt & 31);
+                    if (cnt == 31 && v <= pl) cnt = 32;
+                }
+                kl_n = kcur + cnt;
+                if (valid && cnt == 32) kl_n = last_le(a.a_colptr, kcur, a.a_ncols, pl);
+                if (valid) {
+                    const uint64_t bj = kl_n < a.b_rows ? kl_n : kl_n % a.b_rows;
+                    bst_n = a.b_rowptr[bj];
+                    bend_n = a.b_rowptr[bj + 1];
+                }
             }
-            {
-                const uint64_t v = __shfl_sync(FULL, bnd, cnt & 31);
-                if (cnt == 31 && v <= pl) cnt = 32;
-            }
-            uint64_t kl = kcur + cnt;
-            if (valid && cnt == 32) kl = last_le(a.a_colptr, kcur, a.a_ncols, pl);
+            const double av = av_n;
+            const P pack = pack_n;
+            const uint64_t kl = kl_n;
             uint64_t lb = 0, bst = 0, dst = 0;
             uint32_t rp = 0;
             if (valid) {
-                const uint64_t bj = kl < a.b_rows ? kl : kl % a.b_rows;
-                bst = a.b_rowptr[bj];
-                lb = a.b_rowptr[bj + 1] - bst;
+                bst = bst_n;
+                lb = bend_n - bst;
                 if (lb) {
                     const P bin = pack >> a.lbits;
                     dst = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
                     rp = static_cast<uint32_t>(pack & ((P(1) << a.lbits) - 1)) << cb;
                 }
             }
+            // ---- stage 1 of the next batch
+            const int last = (pend - p) < 32 ? static_cast<int>(pend - p) - 1 : 31;
+            const uint64_t knext = __shfl_sync(FULL, kl, last);
+            const uint64_t pn = p + 32;
+            const bool has_next = pn < pend;
+            if (has_next) {
+                const uint64_t pln = pn + lane;
+                if (pln < pend) {
+                    av_n = a.a_vals[pln];
+                    rid_n = a.a_rowids[pln];
+                }
+                const uint64_t bi = knext + 1 + lane;
+                bnd_n = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
+            }
+            staged = false;
             const bool ne = lb != 0;
             const uint32_t nemask = __ballot_sync(FULL, ne);
             const int rank = __popc(nemask & lt);
@@ -485,11 +522,34 @@ __global__ void __launch_bounds__(EXP_NT, PBG_EXP_MINB) k_expand(ExpandArgs a) {
                         st_tuple_val(a.vals + dv[u], avv[u] * bv[u], pol);
                     }
                 }
+                // ---- stage 2 of the next batch, once its stage-1 loads landed
+                if (s0 == 0 && has_next) {
+                    const uint64_t pln = pn + lane;
+                    const bool vn = pln < pend;
+                    if (vn) pack_n = static_cast<const P*>(a.row_pack)[rid_n];
+                    int cnt = 0;
+#pragma unroll
+                    for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                        const uint64_t v = __shfl_sync(FULL, bnd_n, cnt + s2 - 1);
+                        if (v <= pln) cnt += s2;
+                    }
+                    {
+                        const uint64_t v = __shfl_sync(FULL, bnd_n, cnt & 31);
+                        if (cnt == 31 && v <= pln) cnt = 32;
+                    }
+                    kl_n = knext + cnt;
+                    if (vn && cnt == 32) kl_n = last_le(a.a_colptr, knext, a.a_ncols, pln);
+                    if (vn) {
+                        const uint64_t bj = kl_n < a.b_rows ? kl_n : kl_n % a.b_rows;
+                        bst_n = a.b_rowptr[bj];
+                        bend_n = a.b_rowptr[bj + 1];
+                    }
+                    staged = true;
+                }
             }
             __syncwarp();
-            const int last = (pend - p) < 32 ? static_cast<int>(pend - p) - 1 : 31;
-            kcur = __shfl_sync(FULL, kl, last);
-            p += 32;
+            kcur = knext;
+            p = pn;
 #ifdef PBG_DIAG_SEQSTORE
             tpos += total;
 #endif
