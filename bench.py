@@ -150,11 +150,32 @@ def dist_env():
     return ws, rank, local
 
 
+MATRIX_PATH = None  # --matrix: a Matrix Market file squared instead of a config
+
+
+def data_desc() -> str:
+    if MATRIX_PATH:
+        return f"Matrix Market file {Path(MATRIX_PATH).name}"
+    return "synthetic (seeded, SURVEY.md §8d generators)"
+
+
+def workload_name(cfg_name: str) -> str:
+    if MATRIX_PATH:
+        return f"matrix {Path(MATRIX_PATH).name}: C = A*A (mm_read, duplicates summed)"
+    return f"{cfg_name}: {M.CONFIG_NAMES[cfg_name]}"
+
+
 def build_inputs(cfg_name: str, seed: int = 1):
     """The config's matrix as (CSC, CSR): generated on the GPU when one is
     present (pbg_generate_begin, bit-identical to the host build), else on
-    the host."""
+    the host. With --matrix, the file's matrix (the reference bench's
+    --matrix squaring path, spgemm_bench.cpp:55-58)."""
     t = time.time()
+    if MATRIX_PATH:
+        a_csr = M.matrix_from_mtx(MATRIX_PATH)
+        log(f"[bench] {MATRIX_PATH}: {a_csr.nrows}x{a_csr.ncols} nnz={a_csr.nnz} read in "
+            f"{time.time() - t:.1f}s")
+        return M.csr_to_csc(a_csr), a_csr
     try:
         import torch
         gpu = torch.cuda.is_available()
@@ -211,7 +232,11 @@ def run_reference_arm(args):
         return 0
     # host-built inputs: nothing of this repository's GPU path touches this arm
     t = time.time()
-    a_csc, a_csr = M.make_config(args.config)
+    if MATRIX_PATH:
+        a_csr = M.matrix_from_mtx(MATRIX_PATH)
+        a_csc = M.csr_to_csc(a_csr)
+    else:
+        a_csc, a_csr = M.make_config(args.config)
     log(f"[bench] {args.config}: n={a_csr.nrows} nnz={a_csr.nnz} host inputs in {time.time() - t:.1f}s")
     nthreads = os.cpu_count() or 1
     os.environ.setdefault("OMP_PLACES", "cores")
@@ -222,8 +247,8 @@ def run_reference_arm(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
         "scaling": args.scaling if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded, SURVEY.md §8d generators)",
-        "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}"},
+        "data": data_desc(),
+        "config": {"workload": workload_name(args.config)},
         "impl": "reference",
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "mult/s", "h2d_bytes_per_step": 0,
@@ -457,8 +482,8 @@ def run_gpu_arm(args):
         "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong" if (ws > 1 and not weak) else "weak", "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded generators of SURVEY.md §8d; no dataset)",
-        "config": {"workload": f"{args.config}: {M.CONFIG_NAMES[args.config]}",
+        "data": data_desc(),
+        "config": {"workload": workload_name(args.config),
                    "n": n, "nnz_a": nnz_a, "flop": flop, "nnz_c": nnz_c,
                    "model_bytes": b_tot, "model_GBps": b_tot / t_step / 1e9,
                    "model_frac_of_peak_per_gpu": b_tot / t_step / 1e9 / (peak * ws),
@@ -488,6 +513,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(M.CONFIGS))
+    ap.add_argument("--matrix", default=None,
+                    help="Matrix Market file: square it (C = A*A) instead of a synthetic config")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
@@ -498,6 +525,9 @@ def main():
     ap.add_argument("--max-round-tuples", type=int, default=0,
                     help="force bounded-memory rounds of at most this many mults")
     args = ap.parse_args()
+    if args.matrix:
+        global MATRIX_PATH
+        MATRIX_PATH = args.matrix
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu_arm(args)

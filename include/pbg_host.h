@@ -65,6 +65,25 @@ int pbgh_row_flop(uint32_t nrows, uint32_t ncols, const uint64_t* a_colptr,
 /* Flop-balanced cuts of [0, nrows) into g bands: cuts[0]=0, cuts[g]=nrows. */
 int pbgh_band_cuts(uint32_t nrows, const uint64_t* row_flop, uint32_t g, uint32_t* cuts);
 
+/* ---- Matrix Market I/O (mm_read / mm_write, proj/src/mmio.cpp:33-130) ----
+ * Coordinate format; real/integer/pattern fields, general/symmetric
+ * symmetry. Symmetric storage is expanded to both triangles (diagonal kept
+ * single, the mirror entry right after its source); pattern entries get 1.0;
+ * 1-based indices leave 0-based; entries keep file order. Malformed input
+ * fails with the reference's parse_error message ("name:line: what"),
+ * available from pbgh_last_error(). Two calls: open parses the file into a
+ * handle and reports dims and entry count, fetch copies the entries out. */
+typedef struct pbgh_mm pbgh_mm;
+int pbgh_mm_open(const char* path, pbgh_mm** out, uint32_t* nrows, uint32_t* ncols,
+                 uint64_t* nnz);
+int pbgh_mm_fetch(const pbgh_mm* h, uint32_t* rows, uint32_t* cols, double* vals);
+void pbgh_mm_free(pbgh_mm* h);
+/* coordinate real general, values printed round-trip exact (%.17g). */
+int pbgh_mm_write(const char* path, uint32_t nrows, uint32_t ncols, uint64_t nnz,
+                  const uint32_t* rows, const uint32_t* cols, const double* vals);
+/* Message of the last non-zero return on this thread. */
+const char* pbgh_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

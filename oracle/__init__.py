@@ -104,6 +104,8 @@ def ref_lib():
         lib.ref_choose_nbins.argtypes = [u64, u32, u64, u32]
         lib.ref_dense_multiply.argtypes = [u32, u32, u32, u64, vp, vp, vp, u64, vp, vp, vp,
                                            C.POINTER(vp)]
+        lib.ref_mm_read.argtypes = [C.c_char_p, C.POINTER(vp), C.POINTER(u32), C.POINTER(u32)]
+        lib.ref_mm_write.argtypes = [C.c_char_p, u32, u32, u64, vp, vp, vp]
         _libs["ref"] = lib
     return _libs["ref"]
 
@@ -112,6 +114,7 @@ class OracleError(Exception):
     def __init__(self, code: int, msg: str = ""):
         super().__init__(f"oracle error {code}: {msg}")
         self.code = code  # 1 parameter_error, 2 internal_error, 3 other
+        self.msg = msg
 
 
 @dataclass
@@ -198,6 +201,35 @@ def ref_generate(kind: str, scale: int, ef: int, seed: int):
     lib.ref_coo_get(h, _ptr(r), _ptr(c), _ptr(v))
     lib.ref_coo_free(h)
     return r, c, v
+
+
+def ref_mm_read(path):
+    """The reference's mm_read (mmio.cpp:33-105): (nrows, ncols, rows, cols,
+    vals) in entry order; a parse_error becomes OracleError(3, message)."""
+    lib = ref_lib()
+    h = vp()
+    nr, nc = u32(), u32()
+    rc = lib.ref_mm_read(str(path).encode(), C.byref(h), C.byref(nr), C.byref(nc))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
+    n = lib.ref_coo_nnz(h)
+    r = np.empty(n, np.uint32)
+    c = np.empty(n, np.uint32)
+    v = np.empty(n, np.float64)
+    lib.ref_coo_get(h, _ptr(r), _ptr(c), _ptr(v))
+    lib.ref_coo_free(h)
+    return nr.value, nc.value, r, c, v
+
+
+def ref_mm_write(path, nrows: int, ncols: int, rows, cols, vals) -> None:
+    """The reference's mm_write (mmio.cpp:107-117)."""
+    lib = ref_lib()
+    r = np.ascontiguousarray(rows, np.uint32)
+    c = np.ascontiguousarray(cols, np.uint32)
+    v = np.ascontiguousarray(vals, np.float64)
+    rc = lib.ref_mm_write(str(path).encode(), nrows, ncols, r.size, _ptr(r), _ptr(c), _ptr(v))
+    if rc:
+        raise OracleError(rc, lib.ref_last_error().decode())
 
 
 def ref_convert(to_csr: bool, nrows: int, ncols: int, rows, cols, vals):

@@ -10,6 +10,7 @@
 //   spgemm::gen_er / gen_rmat     proj/include/spgemm/generate.hpp:65-69
 //   spgemm::coo_to_csc/coo_to_csr proj/include/spgemm/convert.hpp:8-9
 //   spgemm::reference_multiply    proj/include/spgemm/reference.hpp:12
+//   spgemm::mm_read / mm_write    proj/include/spgemm/mmio.hpp:15-21
 // Exceptions are turned into return codes: 1 parameter_error, 2 internal_error,
 // 3 anything else; the message goes to ref_last_error().
 
@@ -20,6 +21,7 @@
 
 #include "spgemm/convert.hpp"
 #include "spgemm/generate.hpp"
+#include "spgemm/mmio.hpp"
 #include "spgemm/pb_spgemm.hpp"
 #include "spgemm/reference.hpp"
 
@@ -109,6 +111,26 @@ void ref_coo_get(void* h, uint32_t* rows, uint32_t* cols, double* vals) {
 }
 
 void ref_coo_free(void* h) { delete static_cast<CooMatrix*>(h); }
+
+// ---- Matrix Market: mm_read into a COO handle (ref_coo_*), mm_write ----
+int ref_mm_read(const char* path, void** out, uint32_t* nrows, uint32_t* ncols) {
+    return guarded([&] {
+        auto* m = new CooMatrix(mm_read(std::string(path)));
+        *nrows = m->dims.nrows;
+        *ncols = m->dims.ncols;
+        *out = m;
+    });
+}
+
+int ref_mm_write(const char* path, uint32_t nrows, uint32_t ncols, uint64_t nnz,
+                 const uint32_t* rows, const uint32_t* cols, const double* vals) {
+    return guarded([&] {
+        CooMatrix m;
+        m.dims = {nrows, ncols};
+        for (uint64_t i = 0; i < nnz; ++i) m.entries.push_back({rows[i], cols[i], vals[i]});
+        mm_write(m, std::string(path));
+    });
+}
 
 // ---- conversion: COO -> CSC (major=col) or CSR (major=row) ----
 // Caller gives ptr of size nmajor+1 and idx/val of size nnz (upper bound);

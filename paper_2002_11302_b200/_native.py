@@ -88,6 +88,11 @@ HOST_EXPORTS = {
     "pbgh_csc_row_band": (C.c_int, [u32, u32, vp, vp, vp, u32, u32, vp, vp, vp, P(u64)]),
     "pbgh_row_flop": (C.c_int, [u32, u32, vp, vp, vp, vp]),
     "pbgh_band_cuts": (C.c_int, [u32, vp, u32, vp]),
+    "pbgh_mm_open": (C.c_int, [C.c_char_p, P(vp), P(u32), P(u32), P(u64)]),
+    "pbgh_mm_fetch": (C.c_int, [vp, vp, vp, vp]),
+    "pbgh_mm_free": (None, [vp]),
+    "pbgh_mm_write": (C.c_int, [C.c_char_p, u32, u32, u64, vp, vp, vp]),
+    "pbgh_last_error": (C.c_char_p, []),
 }
 
 _libs: dict = {}

@@ -8,8 +8,14 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cctype>
+#include <cerrno>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <vector>
 
 namespace {
@@ -43,9 +49,224 @@ void prefix(const std::vector<uint64_t>& counts, uint64_t* ptr) {
     for (size_t i = 0; i < counts.size(); ++i) ptr[i + 1] = ptr[i] + counts[i];
 }
 
+thread_local std::string g_host_err;
+
+int host_fail(const std::string& msg) {
+    g_host_err = msg;
+    return 1;
+}
+
+// ---- Matrix Market (semantics of mm_read, proj/src/mmio.cpp:33-105) ----
+struct MmParse {
+    std::string err;
+};
+
+std::string lower(std::string s) {
+    for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    return s;
+}
+
+bool blank_or_comment(const char* b, const char* e) {
+    for (const char* p = b; p < e; ++p) {
+        if (*p == '%') return true;
+        if (!std::isspace(static_cast<unsigned char>(*p))) return false;
+    }
+    return true;
+}
+
+// One whitespace-separated unsigned integer token like `istream >> uint64`
+// (a leading '+' or '-' is accepted by istream; '-' wraps, as there).
+bool take_u64(const char*& p, const char* e, uint64_t& v) {
+    while (p < e && std::isspace(static_cast<unsigned char>(*p))) ++p;
+    if (p >= e) return false;
+    char buf[64];
+    size_t n = 0;
+    while (p < e && !std::isspace(static_cast<unsigned char>(*p)) && n < sizeof buf - 1) buf[n++] = *p++;
+    buf[n] = 0;
+    char* end = nullptr;
+    errno = 0;
+    const unsigned long long x = std::strtoull(buf, &end, 10);
+    if (end == buf || errno) return false;
+    v = x;
+    p -= (buf + n) - end;  // give back an unparsed tail (e.g. "12abc")
+    return true;
+}
+
+bool take_f64(const char*& p, const char* e, double& v) {
+    while (p < e && std::isspace(static_cast<unsigned char>(*p))) ++p;
+    if (p >= e) return false;
+    char buf[128];
+    size_t n = 0;
+    while (p < e && !std::isspace(static_cast<unsigned char>(*p)) && n < sizeof buf - 1) buf[n++] = *p++;
+    buf[n] = 0;
+    // istream >> double (libstdc++ num_get) takes decimal numbers only and
+    // fails on overflow; strtod would also take inf/nan/hex spellings
+    const char* d = buf + (buf[0] == '+' || buf[0] == '-');
+    if (!(std::isdigit(static_cast<unsigned char>(*d)) || *d == '.')) return false;
+    if (d[0] == '0' && (d[1] == 'x' || d[1] == 'X')) {
+        v = 0.0;  // num_get reads the "0" and stops at 'x'
+        p -= (buf + n) - (d + 1);
+        return true;
+    }
+    char* end = nullptr;
+    errno = 0;
+    const double x = std::strtod(buf, &end);
+    if (end == buf || (errno == ERANGE && std::isinf(x))) return false;
+    v = x;
+    p -= (buf + n) - end;
+    return true;
+}
+
+}  // namespace
+
+struct pbgh_mm {
+    uint32_t nrows = 0, ncols = 0;
+    std::vector<uint32_t> rows, cols;
+    std::vector<double> vals;
+};
+
+namespace {
+
+int mm_parse(const std::string& name, const std::string& text, pbgh_mm& out) {
+    const char* p = text.data();
+    const char* end = p + text.size();
+    uint64_t lineno = 0;
+    auto next_line = [&](const char*& b, const char*& e) -> bool {
+        if (p >= end) return false;
+        b = p;
+        const char* nl = static_cast<const char*>(std::memchr(p, '\n', end - p));
+        e = nl ? nl : end;
+        p = nl ? nl + 1 : end;
+        if (e > b && e[-1] == '\r') --e;
+        ++lineno;
+        return true;
+    };
+    auto fail = [&](uint64_t ln, const std::string& msg) {
+        return host_fail(name + ":" + std::to_string(ln) + ": " + msg);
+    };
+    const char *b, *e;
+    if (!next_line(b, e)) return fail(1, "empty file");
+    std::string tok[5];
+    {
+        const char* q = b;
+        for (auto& t : tok) {
+            while (q < e && std::isspace(static_cast<unsigned char>(*q))) ++q;
+            while (q < e && !std::isspace(static_cast<unsigned char>(*q))) t += *q++;
+        }
+    }
+    if (lower(tok[0]) != "%%matrixmarket") return fail(lineno, "missing %%MatrixMarket banner");
+    if (lower(tok[1]) != "matrix") return fail(lineno, "unsupported object '" + tok[1] + "'");
+    if (lower(tok[2]) != "coordinate") return fail(lineno, "unsupported format '" + tok[2] + "'");
+    const std::string field = lower(tok[3]), symmetry = lower(tok[4]);
+    if (field != "real" && field != "integer" && field != "pattern")
+        return fail(lineno, "unsupported field '" + field + "'");
+    if (symmetry != "general" && symmetry != "symmetric")
+        return fail(lineno, "unsupported symmetry '" + symmetry + "'");
+    const bool pattern = field == "pattern";
+    const bool symmetric = symmetry == "symmetric";
+
+    uint64_t nrows = 0, ncols = 0, nnz_decl = 0;
+    for (;;) {
+        if (!next_line(b, e)) return fail(lineno + 1, "missing size line");
+        if (blank_or_comment(b, e)) continue;
+        const char* q = b;
+        if (!take_u64(q, e, nrows) || !take_u64(q, e, ncols) || !take_u64(q, e, nnz_decl))
+            return fail(lineno, "malformed size line");
+        break;
+    }
+    if (nrows < 1 || ncols < 1) return fail(lineno, "matrix dims must be at least 1x1");
+    if (nrows > (uint64_t{1} << 31) || ncols > (uint64_t{1} << 31))
+        return fail(lineno, "dims exceed 2^31 cap");
+    out.nrows = static_cast<uint32_t>(nrows);
+    out.ncols = static_cast<uint32_t>(ncols);
+    const uint64_t cap = symmetric ? 2 * nnz_decl : nnz_decl;
+    out.rows.reserve(cap);
+    out.cols.reserve(cap);
+    out.vals.reserve(cap);
+    uint64_t seen = 0;
+    while (seen < nnz_decl) {
+        if (!next_line(b, e))
+            return fail(lineno + 1, "expected " + std::to_string(nnz_decl) + " entries, got " +
+                                        std::to_string(seen));
+        if (blank_or_comment(b, e)) continue;
+        const char* q = b;
+        uint64_t r = 0, c = 0;
+        double v = 1.0;
+        if (!take_u64(q, e, r) || !take_u64(q, e, c)) return fail(lineno, "malformed entry");
+        if (!pattern && !take_f64(q, e, v)) return fail(lineno, "entry missing value");
+        if (r < 1 || r > nrows || c < 1 || c > ncols)
+            return fail(lineno, "index (" + std::to_string(r) + "," + std::to_string(c) +
+                                    ") outside declared " + std::to_string(nrows) + "x" +
+                                    std::to_string(ncols));
+        if (std::isnan(v)) return fail(lineno, "NaN value");
+        const uint32_t row = static_cast<uint32_t>(r - 1), col = static_cast<uint32_t>(c - 1);
+        out.rows.push_back(row);
+        out.cols.push_back(col);
+        out.vals.push_back(v);
+        if (symmetric && row != col) {
+            out.rows.push_back(col);
+            out.cols.push_back(row);
+            out.vals.push_back(v);
+        }
+        ++seen;
+    }
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
+
+const char* pbgh_last_error(void) { return g_host_err.c_str(); }
+
+int pbgh_mm_open(const char* path, pbgh_mm** out, uint32_t* nrows, uint32_t* ncols,
+                 uint64_t* nnz) {
+    if (!path || !out) return host_fail("null argument");
+    *out = nullptr;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return host_fail(std::string(path) + ": cannot open");
+    std::string text;
+    char buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) text.append(buf, n);
+    std::fclose(f);
+    auto* h = new pbgh_mm;
+    if (int rc = mm_parse(path, text, *h)) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    if (nrows) *nrows = h->nrows;
+    if (ncols) *ncols = h->ncols;
+    if (nnz) *nnz = h->rows.size();
+    return 0;
+}
+
+int pbgh_mm_fetch(const pbgh_mm* h, uint32_t* rows, uint32_t* cols, double* vals) {
+    if (!h) return host_fail("null handle");
+    if (rows) std::memcpy(rows, h->rows.data(), h->rows.size() * 4);
+    if (cols) std::memcpy(cols, h->cols.data(), h->cols.size() * 4);
+    if (vals) std::memcpy(vals, h->vals.data(), h->vals.size() * 8);
+    return 0;
+}
+
+void pbgh_mm_free(pbgh_mm* h) { delete h; }
+
+int pbgh_mm_write(const char* path, uint32_t nrows, uint32_t ncols, uint64_t nnz,
+                  const uint32_t* rows, const uint32_t* cols, const double* vals) {
+    for (uint64_t i = 0; i < nnz; ++i)  // validate (convert.cpp:8-37): indices in range
+        if (rows[i] >= nrows || cols[i] >= ncols)
+            return host_fail("entry " + std::to_string(i) + " outside " + std::to_string(nrows) +
+                             "x" + std::to_string(ncols));
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return host_fail(std::string(path) + ": cannot open for writing");
+    std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n%u %u %llu\n", nrows, ncols,
+                 static_cast<unsigned long long>(nnz));
+    for (uint64_t i = 0; i < nnz; ++i)
+        std::fprintf(f, "%u %u %.17g\n", rows[i] + 1, cols[i] + 1, vals ? vals[i] : 1.0);
+    return std::fclose(f) == 0 ? 0 : host_fail(std::string(path) + ": write failed");
+}
+
 
 uint64_t pbgh_split_seed(uint64_t seed, uint64_t stream) { return split(seed, stream); }
 

@@ -212,6 +212,46 @@ CONFIG_NAMES = {
 }
 
 
+class ParseError(ValueError):
+    """spgemm::parse_error (types.hpp:84): malformed Matrix Market input."""
+
+
+def read_mtx(path):
+    """Matrix Market coordinate file -> (nrows, ncols, rows, cols, vals), the
+    semantics of mm_read (mmio.cpp:33-105): real/integer/pattern, general/
+    symmetric (expanded, mirror right after its source), pattern -> 1.0,
+    0-based, file order. Parsed by the native host library."""
+    lib = _native.host()
+    h = C.c_void_p()
+    nr, nc, nnz = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    rc = lib.pbgh_mm_open(str(path).encode(), C.byref(h), C.byref(nr), C.byref(nc), C.byref(nnz))
+    if rc:
+        raise ParseError(lib.pbgh_last_error().decode())
+    n = nnz.value
+    rows = np.empty(n, np.uint32)
+    cols = np.empty(n, np.uint32)
+    vals = np.empty(n, np.float64)
+    lib.pbgh_mm_fetch(h, _p(rows), _p(cols), _p(vals))
+    lib.pbgh_mm_free(h)
+    return nr.value, nc.value, rows, cols, vals
+
+
+def write_mtx(path, nrows: int, ncols: int, rows, cols, vals=None) -> None:
+    """mm_write (mmio.cpp:107-117): coordinate real general, %.17g values."""
+    r = np.ascontiguousarray(rows, np.uint32)
+    c = np.ascontiguousarray(cols, np.uint32)
+    v = np.ascontiguousarray(np.ones(r.size) if vals is None else vals, np.float64)
+    _check(_native.host().pbgh_mm_write(str(path).encode(), nrows, ncols, r.size, _p(r), _p(c),
+                                        _p(v)), "pbgh_mm_write")
+
+
+def matrix_from_mtx(path) -> CsrMatrix:
+    """A Matrix Market file as CSR (duplicates summed, coo_to_csr), the
+    reference bench's --matrix input (spgemm_bench.cpp:55-58)."""
+    nr, nc, r, c, v = read_mtx(path)
+    return coo_to_csr(nr, nc, r, c, v)
+
+
 def make_matrix(kind: str, scale: int, ef: int | None, seed: int = 1) -> CsrMatrix:
     """One square input matrix in CSR (values included)."""
     vseed = seed ^ VALUE_SEED_XOR

@@ -90,6 +90,24 @@ def test_random_sweep_vs_oracle(seed):
     assert_valid_csr(res.c)
 
 
+def test_matrix_market_squaring(tmp_path):
+    """The reference bench's --matrix path (spgemm_bench.cpp:55-58): a Matrix
+    Market file (symmetric storage, mm_read semantics) squared on the GPU."""
+    s = M.stencil27(6)
+    rows = np.repeat(np.arange(s.nrows, dtype=np.uint32), np.diff(s.rowptr).astype(np.int64))
+    lower = rows >= s.colids
+    p = tmp_path / "st6_sym.mtx"
+    with open(p, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real symmetric\n")
+        f.write(f"{s.nrows} {s.ncols} {int(lower.sum())}\n")
+        for r, c, v in zip(rows[lower], s.colids[lower], s.values[lower]):
+            f.write(f"{r + 1} {c + 1} {v:.17g}\n")
+    a = M.matrix_from_mtx(p)
+    assert np.array_equal(a.rowptr, s.rowptr) and np.array_equal(a.colids, s.colids)
+    res = gpu(M.csr_to_csc(a), a)
+    check_vs(res, oracle.multiply(M.csr_to_csc(a), a))
+
+
 def test_rectangular():
     r, c = M.gen_er(9, 4, 5)
     a = M.coo_to_csr(512, 512, r, c)
