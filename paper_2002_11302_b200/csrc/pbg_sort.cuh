@@ -381,6 +381,7 @@ __device__ uint32_t hash_premerge(SortSmem& sm, int in, int scr, uint32_t n) {
 // merged count; *res gets the buffer holding the merged output.
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
                                    int bits, uint32_t keylo, uint32_t distinct, int* res,
+                                   int* rshift,
                                    int next_slot, uint64_t next_bin, long long& prof_t) {
     const int tid = threadIdx.x;
     if (distinct * 2 <= n && n >= 64) {
@@ -423,10 +424,12 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         // rank (duplicate-heavy keys, e.g. RMAT heavy-row pieces)
         __syncthreads();
         *res = scr;
+        *rshift = 0;  // row starts from the bucket ends if nothing merges
         bool dupz = false;
         for (uint32_t i = tid + 1; i < n; i += SM_NT) dupz |= sm.k[scr][i] == sm.k[scr][i - 1];
         if (__syncthreads_or(dupz)) {
             *res = in;
+            *rshift = -1;
             return merge_dups(sm, scr, in, n);
         }
         return n;
@@ -468,13 +471,14 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         return merge_dups(sm, sorted, other, n);
     }
     *res = sorted;
+    *rshift = any_big ? -1 : sh;  // sorted positions = bucket ends: row starts from them
     return n;
 }
 
 // Write a work bin: colids / values at P, rowptr of the rows it starts.
 __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm, int buf,
                                           uint64_t b, uint64_t nw, uint32_t rs, uint32_t span,
-                                          uint32_t U, uint64_t P) {
+                                          uint32_t U, uint64_t P, int rshift) {
     const int tid = threadIdx.x;
     const int cb = a.col_bits;
     const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
@@ -485,6 +489,16 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
     for (uint32_t u = tid; u < U; u += SM_NT) {
         __stcs(okeys + u, K[u] & colmask);
         __stcs(ovals + u, V[u]);
+    }
+    if (rshift >= 0 && rshift <= cb) {
+        // nothing merged: row r starts where its first MSD bucket starts
+        // (cnt[d] holds the end of bucket d after the scatter)
+        for (uint32_t r = tid; r < span; r += SM_NT) {
+            const uint32_t d = (r << cb) >> rshift;
+            a.rowptr[rs + r] = P + (d ? sm.cnt[d - 1] : 0u);
+        }
+        if (tid == 0 && b == nw - 1) a.rowptr[a.m] = P + U;
+        return;
     }
     // rowptr[rs + r] = P + first merged entry of local row r (binary search)
     for (uint32_t r = tid; r < span; r += SM_NT) {
@@ -547,6 +561,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         const uint32_t tk = tid == 0 ? atomicAdd(a.ticket, 1u) : 0u;
         if (tid == 0 && M.n > SM_CAP && !(M.flags & 2u)) atomicOr(a.err, 2u);
         int res = inb;
+        int rshift = -1;
         uint32_t U = 0;
         bool merged = false, fetched = false;
         if (loaded) {
@@ -566,7 +581,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             __syncthreads();
             PROF_MARK(0);
             U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(M.keybits), M.keylo,
-                               static_cast<uint32_t>(M.nnz), &res, mc ^ 1, tk, prof_t);
+                               static_cast<uint32_t>(M.nnz), &res, &rshift, mc ^ 1, tk, prof_t);
             fetched = true;
 #ifdef PBG_SORT_PROF
             __syncthreads();
@@ -587,7 +602,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         if (tid == 0 && sm.s_bin[mc ^ 1] < nw && bin_kind(sm.meta[mc ^ 1]) == 1)
             issue_tma(a, sm, res ^ 1, sm.meta[mc ^ 1]);
         if (merged) write_merged(a, M, b, nw, M.out, U);
-        else write_bin(a, sm, res, b, nw, M.rs, M.span, U, M.out);
+        else write_bin(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift);
         PROF_MARK(5);
         inb = res ^ 1;
         mc ^= 1;
