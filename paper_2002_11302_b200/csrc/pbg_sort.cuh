@@ -46,7 +46,11 @@ namespace pbg {
 constexpr int SM_NT = PBG_SM_NT;
 constexpr int SM_NW = SM_NT / 32;
 constexpr int SM_CAP = PBG_SM_CAP;            // max tuples per smem bin
-constexpr int SM_NB = SM_CAP;                 // buckets of the MSD pass
+#ifndef PBG_SM_NB
+#define PBG_SM_NB PBG_SM_CAP
+#endif
+constexpr int SM_NB = PBG_SM_NB;              // buckets of the MSD pass (u16 counters)
+constexpr int SM_CQ = SM_NB * 2 / 16 / SM_NT; // uint4s of counters per thread
 constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
 #ifndef PBG_SM_BMAX
 #define PBG_SM_BMAX 128
@@ -56,7 +60,7 @@ constexpr int SM_ITEMS = SM_CAP / SM_NT;      // 8
 constexpr int SM_PER_WARP = SM_CAP / SM_NW;
 constexpr int SM_NBUF = 2;                    // ping, pong
 static_assert(SM_ITEMS == 8, "one uint4 of u16 counters per thread");
-static_assert(SM_NB * 2 / 16 == SM_NT, "counter scan layout");
+static_assert(SM_CQ >= 1 && SM_CQ * 16 * SM_NT == SM_NB * 2, "counter scan layout");
 
 struct SortArgs {
     WorkBins w;
@@ -194,28 +198,38 @@ __device__ __forceinline__ void issue_tma(const SortArgs& a, SortSmem& sm, int b
 // Exclusive scan of the SM_NB u16 counters in index order (8 per thread).
 __device__ __forceinline__ void scan_cnt(SortSmem& sm) {
     const int tid = threadIdx.x;
-    const uint4 raw = reinterpret_cast<const uint4*>(sm.cnt)[tid];
-    const uint32_t rw[4] = {raw.x, raw.y, raw.z, raw.w};
-    uint32_t c8[8];
+    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + SM_CQ * tid;
+    uint32_t rw[4 * SM_CQ];
+#pragma unroll
+    for (int q = 0; q < SM_CQ; ++q) {
+        const uint4 raw = c4[q];
+        rw[4 * q] = raw.x;
+        rw[4 * q + 1] = raw.y;
+        rw[4 * q + 2] = raw.z;
+        rw[4 * q + 3] = raw.w;
+    }
     uint32_t s8 = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        c8[2 * j] = rw[j] & 0xffffu;
-        c8[2 * j + 1] = rw[j] >> 16;
-        s8 += c8[2 * j] + c8[2 * j + 1];
-    }
+    for (int j = 0; j < 4 * SM_CQ; ++j) s8 += (rw[j] & 0xffffu) + (rw[j] >> 16);
     uint32_t tot;
     uint32_t run = block_exclusive_scan<SM_NT>(s8, sm.s_warp32, tot);
-    uint32_t ow[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 4 * SM_CQ; ++j) {
         const uint32_t lo = run;
-        run += c8[2 * j];
+        run += rw[j] & 0xffffu;
         const uint32_t hi = run;
-        run += c8[2 * j + 1];
-        ow[j] = lo | (hi << 16);
+        run += rw[j] >> 16;
+        rw[j] = lo | (hi << 16);
     }
-    reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+#pragma unroll
+    for (int q = 0; q < SM_CQ; ++q)
+        c4[q] = make_uint4(rw[4 * q], rw[4 * q + 1], rw[4 * q + 2], rw[4 * q + 3]);
+}
+
+__device__ __forceinline__ void zero_cnt(SortSmem& sm) {
+    uint4* c4 = reinterpret_cast<uint4*>(sm.cnt) + SM_CQ * threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < SM_CQ; ++q) c4[q] = make_uint4(0, 0, 0, 0);
 }
 
 // Stable LSD radix sort of buffer `x` (n <= SM_CAP) over `bits` key bits,
@@ -234,7 +248,7 @@ __device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits, uint32
         kr[it] = idx < n ? sm.k[cur][idx] : 0u;
     }
     for (int shift = 0; shift < bits; shift += 8) {
-        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+        zero_cnt(sm);
         __syncthreads();
         uint16_t rank[SM_ITEMS];
         uint32_t dig[SM_ITEMS];
@@ -386,7 +400,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     const int tid = threadIdx.x;
     if (distinct * 2 <= n && n >= 64) {
         n = hash_premerge(sm, in, scr, n);  // now n distinct keys, no duplicates
-        reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+        zero_cnt(sm);
         __syncthreads();
     }
     uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);
@@ -566,7 +580,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         bool merged = false, fetched = false;
         if (loaded) {
             const uint32_t n = static_cast<uint32_t>(M.n);
-            reinterpret_cast<uint4*>(sm.cnt)[tid] = make_uint4(0, 0, 0, 0);
+            zero_cnt(sm);
             if (loaded == 1) {
                 mbar_wait(&sm.mbar, parity);
                 parity ^= 1;
