@@ -139,6 +139,17 @@ int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const ui
  * pbg_release. */
 int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t vseed, int to_csc,
                        const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_out);
+/* spgemm::hash_multiply (baseline.hpp:21-24, baseline.cpp:141-200) on the
+ * GPU: C = A.B with A, B and C in CSC (column Gustavson SpGEMM, one shared-
+ * memory hash table per output column, sized bit_ceil(2 f_j) like the
+ * reference's). Same errors as pbg_multiply_begin (PBG_ERR_DIM,
+ * PBG_ERR_FLOP_OVERFLOW); a column of more than 4096 products returns
+ * PBG_ERR_UNIMPLEMENTED (use pbg_multiply_begin). Read with
+ * pbg_multiply_fetch (rowptr = colptr[b.ncols+1], colids = row ids), free
+ * with pbg_release. pbg_report: flop, nnz_c, t_symbolic (column flop +
+ * scan), t_sort (hash + sort + compaction), t_total. */
+int pbg_hash_multiply_begin(const pbg_csx_view* a_csc, const pbg_csx_view* b_csc,
+                            const pbg_config* cfg, pbg_handle** out, uint64_t* nnz_c);
 /* The reference SymbolicResult (pb_spgemm.hpp:48-55) on the REFERENCE bin
  * layout: per_column_flop[a.ncols], per_bin_flop[nbins], bin_row_starts
  * [nbins+1]; nbins from pbg_report.nbins. Any pointer may be NULL. */

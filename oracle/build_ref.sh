@@ -14,7 +14,7 @@ if [ ! -d "$REF/src" ]; then
   exit 0
 fi
 mkdir -p "$OUT"
-SRCS="$REF/src/convert.cpp $REF/src/generate.cpp $REF/src/mmio.cpp $REF/src/pb_spgemm.cpp $REF/src/reference.cpp"
+SRCS="$REF/src/baseline.cpp $REF/src/convert.cpp $REF/src/generate.cpp $REF/src/mmio.cpp $REF/src/pb_spgemm.cpp $REF/src/reference.cpp"
 # -march=x86-64-v3: portable to the GPU box's host (AVX2), the container's
 # native target may differ.
 g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -I "$REF/include" \

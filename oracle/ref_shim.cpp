@@ -11,6 +11,7 @@
 //   spgemm::coo_to_csc/coo_to_csr proj/include/spgemm/convert.hpp:8-9
 //   spgemm::reference_multiply    proj/include/spgemm/reference.hpp:12
 //   spgemm::mm_read / mm_write    proj/include/spgemm/mmio.hpp:15-21
+//   spgemm::hash_multiply         proj/include/spgemm/baseline.hpp:21-24
 // Exceptions are turned into return codes: 1 parameter_error, 2 internal_error,
 // 3 anything else; the message goes to ref_last_error().
 
@@ -19,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "spgemm/baseline.hpp"
 #include "spgemm/convert.hpp"
 #include "spgemm/generate.hpp"
 #include "spgemm/mmio.hpp"
@@ -111,6 +113,33 @@ void ref_coo_get(void* h, uint32_t* rows, uint32_t* cols, double* vals) {
 }
 
 void ref_coo_free(void* h) { delete static_cast<CooMatrix*>(h); }
+
+// ---- column hash SpGEMM (CSC x CSC -> CSC) ----
+int ref_hash_multiply(uint32_t a_nrows, uint32_t a_ncols, uint64_t a_nnz, const uint64_t* a_colptr,
+                      const uint32_t* a_rowids, const double* a_vals, uint32_t b_nrows,
+                      uint32_t b_ncols, uint64_t b_nnz, const uint64_t* b_colptr,
+                      const uint32_t* b_rowids, const double* b_vals, int nthreads, void** out) {
+    return guarded([&] {
+        CscMatrix a, b;
+        a.dims = {a_nrows, a_ncols};
+        a.colptr.assign(a_colptr, a_colptr + a_ncols + 1);
+        a.rowids.assign(a_rowids, a_rowids + a_nnz);
+        a.values.assign(a_vals, a_vals + a_nnz);
+        b.dims = {b_nrows, b_ncols};
+        b.colptr.assign(b_colptr, b_colptr + b_ncols + 1);
+        b.rowids.assign(b_rowids, b_rowids + b_nnz);
+        b.values.assign(b_vals, b_vals + b_nnz);
+        *out = new CscMatrix(hash_multiply(a, b, nthreads));
+    });
+}
+uint64_t ref_csc_nnz(void* h) { return static_cast<CscMatrix*>(h)->rowids.size(); }
+void ref_csc_get(void* h, uint64_t* colptr, uint32_t* rowids, double* vals) {
+    auto* m = static_cast<CscMatrix*>(h);
+    std::memcpy(colptr, m->colptr.data(), m->colptr.size() * 8);
+    std::memcpy(rowids, m->rowids.data(), m->rowids.size() * 4);
+    std::memcpy(vals, m->values.data(), m->values.size() * 8);
+}
+void ref_csc_free(void* h) { delete static_cast<CscMatrix*>(h); }
 
 // ---- Matrix Market: mm_read into a COO handle (ref_coo_*), mm_write ----
 int ref_mm_read(const char* path, void** out, uint32_t* nrows, uint32_t* ncols) {

@@ -64,6 +64,7 @@ PBG_EXPORTS = {
     "pbg_multiply_fetch": (C.c_int, [vp, vp, vp, vp, P(Report)]),
     "pbg_generate_begin": (C.c_int, [C.c_int, C.c_int, u32, u64, u64, C.c_int, P(Config), P(vp),
                                      P(u64)]),
+    "pbg_hash_multiply_begin": (C.c_int, [P(CsxView), P(CsxView), P(Config), P(vp), P(u64)]),
     "pbg_coo_convert_begin": (C.c_int, [u32, u32, u64, vp, vp, vp, C.c_int, P(Config), P(vp),
                                         P(u64)]),
     "pbg_symbolic_fetch": (C.c_int, [vp, vp, vp, vp]),

@@ -160,6 +160,51 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
     return PbResult(c, sym, phases, rep.tuples_into_sort, rep.merged_total, r)
 
 
+@dataclass
+class HashResult:
+    c: CscMatrix
+    flop: int
+    phases: dict
+
+
+def hash_multiply(a: CscMatrix, b: CscMatrix, cfg: PbConfig | None = None) -> HashResult:
+    """spgemm::hash_multiply (baseline.hpp:21-24, baseline.cpp:141-200) on the
+    GPU: C = A·B, A, B and C in CSC — the column hash SpGEMM the paper finds
+    faster than PB-SpGEMM above a compression factor of ~4 (SURVEY.md §8f
+    f3). Columns of more than 4096 products raise NotImplementedError (use
+    pb_multiply)."""
+    cfg = cfg or PbConfig()
+    lib = _native.pbg()
+    ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))
+    bp, bi, bv = (np.ascontiguousarray(x) for x in _host_arrays(b))
+    if not isinstance(b, CscMatrix):
+        raise TypeError("hash_multiply takes B in CSC")
+    va = _view(a.nrows, a.ncols, ap, ai, av)
+    vb = _view(b.nrows, b.ncols, bp, bi, bv)
+    c_cfg = cfg.to_c()
+    h = C.c_void_p()
+    nnz = C.c_uint64(0)
+    rc = lib.pbg_hash_multiply_begin(C.byref(va), C.byref(vb), C.byref(c_cfg), C.byref(h),
+                                     C.byref(nnz))
+    if rc:
+        _raise(rc)
+    try:
+        k = nnz.value
+        colptr = np.empty(b.ncols + 1, np.uint64)
+        rowids = np.empty(max(k, 1), np.uint32)
+        values = np.empty(max(k, 1), np.float64)
+        rep = _native.Report()
+        rc = lib.pbg_multiply_fetch(h, colptr.ctypes.data, rowids.ctypes.data,
+                                    values.ctypes.data, C.byref(rep))
+        if rc:
+            _raise(rc)
+    finally:
+        lib.pbg_release(h)
+    r = rep.as_dict()
+    phases = {key: r[key] for key in ("t_symbolic", "t_sort", "t_total", "t_h2d", "t_d2h")}
+    return HashResult(CscMatrix(a.nrows, b.ncols, colptr, rowids[:k], values[:k]), rep.flop, phases)
+
+
 def _coo_convert(nrows, ncols, rows, cols, vals, to_csc, cfg):
     cfg = cfg or PbConfig()
     lib = _native.pbg()

@@ -16,6 +16,7 @@
 #include "pbg_kernels.cuh"
 #include "pbg_heavy.cuh"
 #include "pbg_sort.cuh"
+#include "pbg_hash.cuh"
 
 namespace {
 
@@ -105,7 +106,7 @@ struct pbg_context {
         in_a_val, in_b_ptr, in_b_idx, in_b_val;
     // heavy rows + work bins
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
-        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out;
+        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out, hflop, hbound, hcolcnt, hzero;
     DevBuf items[2][8];
     DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
@@ -128,7 +129,7 @@ struct pbg_context {
                           &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
                           &in_b_idx, &in_b_val, &heavy_excl, &hpad_excl, &bin_hidx, &hbin, &hoff,
                           &hhead, &hcount, &skeys, &svals, &child_cnt, &child_pos, &hstat, &wcnt,
-                          &wpos, &wb_nnz, &wb_out})
+                          &wpos, &wb_nnz, &wb_out, &hflop, &hbound, &hcolcnt, &hzero})
             b->release();
         for (auto& set : items)
             for (auto& b : set) b.release();
@@ -1193,6 +1194,169 @@ int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const ui
         return rc;
     }
     if (nnz_out) *nnz_out = ctx->nnz_c;
+    *out = h;
+    return PBG_OK;
+}
+
+int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
+                            pbg_handle** out, uint64_t* nnz_c) {
+    using namespace pbg;
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    *out = nullptr;
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    if (a->ncols != b->nrows)  // require_multipliable (types.hpp:97-102)
+        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
+                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
+                                     "x" + std::to_string(b->ncols));
+    if ((rc = set_device(cfg.device))) return rc;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    pbg_context* ctx = pool_get(dev);
+    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
+    auto* h = new pbg_handle;
+    h->ctx = ctx;
+    h->cfg = cfg;
+    cudaStream_t st = nullptr;
+    auto bail = [&](int code) {
+        pbg_release(h);
+        return code;
+    };
+    const uint64_t na = uint64_t(a->ncols) + 1, nbc = uint64_t(b->ncols);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    rc = copy_in(ctx->in_a_ptr, a->ptr, na * 8, st);
+    if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (nbc + 1) * 8, st);
+    if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
+    if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
+    cudaEventRecord(e1, st);
+    if (rc) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return bail(rc);
+    }
+    const auto* a_ptr = static_cast<const uint64_t*>(ctx->in_a_ptr.p);
+    const auto* b_ptr = static_cast<const uint64_t*>(ctx->in_b_ptr.p);
+    // scan status words + tickets + scalars for the two scans (zeroed)
+    const uint64_t tiles = (nbc + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    const size_t zbytes = (2 * tiles + 16) * 8;
+    if ((rc = grow(ctx->hzero, zbytes)) || (rc = grow(ctx->hflop, (nbc + 1) * 8)) ||
+        (rc = grow(ctx->hbound, (nbc + 2) * 8)) || (rc = grow(ctx->hcolcnt, (nbc + 1) * 8)) ||
+        (rc = grow(ctx->rowptr, (nbc + 2) * 8)))
+        return bail(rc);
+    auto* zb = static_cast<unsigned long long*>(ctx->hzero.p);
+    unsigned int* tk = reinterpret_cast<unsigned int*>(zb);           // 2 tickets
+    unsigned long long* sc = zb + 2;                                   // flop, max flop, err
+    unsigned long long* stat = zb + 16;
+    auto* flop = static_cast<uint64_t*>(ctx->hflop.p);
+    auto* bound = static_cast<uint64_t*>(ctx->hbound.p);
+    auto* count = static_cast<uint64_t*>(ctx->hcolcnt.p);
+    auto* colptr = static_cast<uint64_t*>(ctx->rowptr.p);
+    cudaEvent_t ev[4];
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[0], st);
+    CUDA_TRY(cudaMemsetAsync(zb, 0, zbytes, st));
+    if (nbc) k_hash_colflop<<<blocks_for(nbc, 256), 256, 0, st>>>(a_ptr, b_ptr,
+                                                                  static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                                                                  nbc, flop);
+    launch_scan(ArrayIn{flop}, bound, nbc, nullptr, nbc, stat, tk, sc + 0, sc + 1, st);
+    cudaEventRecord(ev[1], st);
+    unsigned long long hs[3];
+    CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    // the exact 64-bit overflow test of column_symbolic (baseline.cpp:81-83)
+    {
+        std::vector<uint64_t> hf(nbc);
+        if (nbc) CUDA_TRY(cudaMemcpy(hf.data(), flop, nbc * 8, cudaMemcpyDeviceToHost));
+        uint64_t tot = 0;
+        for (uint64_t x : hf)
+            if (__builtin_add_overflow(tot, x, &tot)) {
+                for (auto& e : ev) cudaEventDestroy(e);
+                return bail(fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits"));
+            }
+    }
+    const uint64_t total = hs[0], maxf = hs[1];
+    if (maxf > HASH_BIG_F) {
+        for (auto& e : ev) cudaEventDestroy(e);
+        return bail(fail(PBG_ERR_UNIMPLEMENTED,
+                         "a column of " + std::to_string(maxf) + " products exceeds the hash path's " +
+                             std::to_string(HASH_BIG_F) + " (use pbg_multiply_begin)"));
+    }
+    if ((rc = grow(ctx->keys, total * 4 + 16)) || (rc = grow(ctx->vals, total * 8 + 16)) ||
+        (rc = grow(ctx->ccol, total * 4 + 16)) || (rc = grow(ctx->cval, total * 8 + 16))) {
+        for (auto& e : ev) cudaEventDestroy(e);
+        return bail(rc);
+    }
+    HashArgs ha{a_ptr, static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                static_cast<const double*>(ctx->in_a_val.p), b_ptr,
+                static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                static_cast<const double*>(ctx->in_b_val.p), nbc, flop, bound,
+                static_cast<uint32_t*>(ctx->keys.p), static_cast<double*>(ctx->vals.p), count,
+                reinterpret_cast<unsigned int*>(sc + 2)};
+    CUDA_TRY(cudaMemsetAsync(count, 0, (nbc + 1) * 8, st));
+    using Small = HashSmem<128, 2048, 1024>;
+    using Big = HashSmem<512, 8192, 4096>;
+    static bool attr[64] = {};
+    if (!attr[ctx->device & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_hash_cols<128, 2048, 1024>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Small)));
+        CUDA_TRY(cudaFuncSetAttribute(k_hash_cols<512, 8192, 4096>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Big)));
+        attr[ctx->device & 63] = true;
+    }
+    if (nbc && total) {
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_cols<128, 2048, 1024>, 128,
+                                                      sizeof(Small));
+        const unsigned g1 = static_cast<unsigned>(
+            std::min<uint64_t>(nbc, uint64_t(std::max(per_sm, 1)) * ctx->num_sms));
+        k_hash_cols<128, 2048, 1024><<<g1, 128, sizeof(Small), st>>>(ha, 0, HASH_SMALL_F);
+        if (maxf > HASH_SMALL_F)
+            k_hash_cols<512, 8192, 4096><<<ctx->num_sms, 512, sizeof(Big), st>>>(ha, HASH_SMALL_F,
+                                                                                 HASH_BIG_F);
+    }
+    launch_scan(ArrayIn{count}, colptr, nbc, nullptr, nbc, stat + tiles, tk + 1, nullptr, nullptr, st);
+    if (nbc)
+        k_hash_compact<<<blocks_for(nbc * 32, 256), 256, 0, st>>>(
+            bound, colptr, nbc, static_cast<const uint32_t*>(ctx->keys.p),
+            static_cast<const double*>(ctx->vals.p), static_cast<uint32_t*>(ctx->ccol.p),
+            static_cast<double*>(ctx->cval.p));
+    cudaEventRecord(ev[2], st);
+    uint64_t nnz = 0;
+    CUDA_TRY(cudaMemcpyAsync(&nnz, colptr + nbc, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    float t_sym = 0, t_num = 0, t_h2d = 0;
+    cudaEventElapsedTime(&t_sym, ev[0], ev[1]);
+    cudaEventElapsedTime(&t_num, ev[1], ev[2]);
+    cudaEventElapsedTime(&t_h2d, e0, e1);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ctx->m = nbc;  // the "rows" of the fetched pointer array are C's columns
+    ctx->k = a->ncols;
+    ctx->n = a->nrows;
+    ctx->nnz_c = nnz;
+    ctx->flop = total;
+    ctx->rep = pbg_report{};
+    ctx->rep.flop = total;
+    ctx->rep.nnz_c = nnz;
+    ctx->rep.nnz_a = a->nnz;
+    ctx->rep.nnz_b = b->nnz;
+    ctx->rep.t_symbolic = t_sym * 1e-3;
+    ctx->rep.t_sort = t_num * 1e-3;
+    ctx->rep.t_total = (t_sym + t_num) * 1e-3;
+    ctx->rep.merged_total = nnz;
+    ctx->have_result = true;
+    h->t_h2d = t_h2d * 1e-3;
+    if (nnz_c) *nnz_c = nnz;
     *out = h;
     return PBG_OK;
 }

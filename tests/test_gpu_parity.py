@@ -510,3 +510,61 @@ def test_gpu_generators_match_host(name):
     for g, h in ((gc.colptr, hc.colptr), (gc.rowids, hc.rowids), (gc.values, hc.values),
                  (gr.rowptr, hr.rowptr), (gr.colids, hr.colids), (gr.values, hr.values)):
         assert np.array_equal(g, h)
+
+
+# ---- column hash SpGEMM: spgemm::hash_multiply ----------
+def _hash_vs_reference(a, b):
+    res = api.hash_multiply(a, b, api.PbConfig(device=0))
+    if oracle.ref_available():
+        cp, ri, v = oracle.ref_hash_multiply(a, b)
+    else:  # CSC of C = (CSR of C^T): the oracle product of the transposes
+        ref = oracle.multiply(M.csr_to_csc(_transpose(b)), _transpose(a))
+        cp, ri, v = ref.rowptr, ref.colids, ref.values
+    assert_csr_matches(res.c.colptr, res.c.rowids, res.c.values, cp, ri, v)
+    return res
+
+
+def _transpose(m):
+    """CSC m as the CSR of its transpose (same arrays)."""
+    return M.CsrMatrix(m.ncols, m.nrows, m.colptr, m.rowids, m.values)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_hash_multiply_random_vs_reference(seed):
+    rng = np.random.default_rng(500 + seed)
+    scale = int(rng.integers(4, 11))
+    mats = [M.make_matrix("er" if rng.integers(2) else "rmat", scale,
+                          int(min(rng.integers(2, 12), 1 << scale)), seed=seed * 7 + k)
+            for k in range(2)]
+    a, b = M.csr_to_csc(mats[0]), M.csr_to_csc(mats[1])
+    try:
+        _hash_vs_reference(a, b)
+    except NotImplementedError:  # an RMAT hub column above the hash capacity
+        assert max(np.diff(b.colptr)) > 0
+
+
+def test_hash_multiply_stencil_and_edges():
+    s = M.stencil27(12)   # cf ~5.8: the hash path's regime; exact integer values
+    a = M.csr_to_csc(s)
+    res = _hash_vs_reference(a, a)
+    assert np.all(res.c.values == np.round(res.c.values))
+    # big-table kernel: columns of 1025..4096 products
+    r, c = M.gen_er(10, 40, 3)
+    big = M.coo_to_csc(1 << 10, 1 << 10, r, c, np.linspace(0.5, 1.5, r.size))
+    _hash_vs_reference(big, big)
+    # empty columns, exact-zero cancellation kept
+    x = M.coo_to_csc(2, 2, [0, 0], [0, 1], [1.0, -1.0])
+    y = M.coo_to_csc(2, 2, [0, 1], [1, 1], [1.0, 1.0])
+    z = api.hash_multiply(x, y, api.PbConfig(device=0)).c
+    assert list(z.colptr) == [0, 0, 1] and z.values[0] == 0.0
+    with pytest.raises(api.ParameterError):
+        api.hash_multiply(M.coo_to_csc(2, 3, [0], [0]), x, api.PbConfig(device=0))
+
+
+def test_hash_multiply_refuses_hub_columns():
+    # one B column of 8000 products: above the shared-memory table
+    k = 8000
+    a = M.coo_to_csc(k, 1, np.arange(k), np.zeros(k, int), np.ones(k))
+    b = M.coo_to_csc(1, 1, [0], [0], [2.0])
+    with pytest.raises(NotImplementedError):
+        api.hash_multiply(a, b, api.PbConfig(device=0))
