@@ -9,7 +9,7 @@
 // 73-85, gives its product count f_j and its scratch range):
 //   * the products A(:, i)·B(i, j) for every B(i, j) are accumulated in a
 //     shared-memory open-addressing table keyed by row id (linear probing,
-//     table = bit_ceil(2 f_j) slots like the reference's, exact zeros kept);
+//     bit_ceil(f_j + 1) slots, exact zeros kept);
 //   * the occupied slots are compacted, sorted by row id (rank counting for
 //     short columns, a bitonic network otherwise) and written to the column's
 //     scratch range at bound_start[j] (ScratchOutput, baseline.cpp:16-50);
@@ -80,15 +80,15 @@ __global__ void __launch_bounds__(NT) k_hash_cols(HashArgs a, uint64_t lo_f, uin
     for (uint64_t j = blockIdx.x; j < a.ncols; j += gridDim.x) {
         const uint64_t f = a.flop[j];
         if (f <= lo_f || f > hi_f) continue;
-        // bit_ceil(2 f) slots as the reference sizes its table; HASH_LOAD1
-        // builds size it to the product count (load <= 1: the distinct row
-        // ids never exceed f) to halve the clear and compaction scans
-#ifdef PBG_HASH_LOAD1
-        uint32_t T = 32;
-        while (T < f + 1) T <<= 1;
-#else
+        // bit_ceil(f + 1) slots: the distinct row ids never exceed f, so the
+        // table cannot fill; half the reference's bit_ceil(2 f) halves the
+        // clear and compaction scans (C4 42 -> 34 ms; C2 22 -> 24 ms)
+#ifdef PBG_HASH_LOAD2
         uint32_t T = 32;
         while (T < 2 * f) T <<= 1;
+#else
+        uint32_t T = 32;
+        while (T < f + 1) T <<= 1;
 #endif
         for (uint32_t s = tid; s < T; s += NT) {
             sm.key[s] = HASH_EMPTY;
