@@ -1311,13 +1311,36 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Big)));
         attr[ctx->device & 63] = true;
     }
+    using W512 = HashWarpSmem<512, 8>;
+    using W1K = HashWarpSmem<1024, 8>;
+    static bool wattr[64] = {};
+    if (!wattr[ctx->device & 63]) {
+        CUDA_TRY(cudaFuncSetAttribute(k_hash_warp<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(W512)));
+        CUDA_TRY(cudaFuncSetAttribute(k_hash_warp<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sizeof(W1K)));
+        wattr[ctx->device & 63] = true;
+    }
     if (nbc && total) {
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hash_cols<128, 2048, 1024>, 128,
-                                                      sizeof(Small));
-        const unsigned g1 = static_cast<unsigned>(
-            std::min<uint64_t>(nbc, uint64_t(std::max(per_sm, 1)) * ctx->num_sms));
-        k_hash_cols<128, 2048, 1024><<<g1, 128, sizeof(Small), st>>>(ha, 0, HASH_SMALL_F);
+        // columns of up to 1023 products: a warp each; up to 4096: a CTA each
+        auto grid_for = [&](auto kern, int nt, size_t smem, uint64_t units) {
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem);
+            return static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>(units, uint64_t(std::max(per_sm, 1)) * ctx->num_sms)));
+        };
+        // (a warp per column of 512..1023 products measured slower than a CTA
+        // per column on the stencil: 37 vs 34 ms; k_hash_warp<1024, 8> kept
+        // for tuning via PBG_HASH_WARP1K)
+        const uint64_t wmax = getenv("PBG_HASH_WARP1K") ? 1023 : 511;
+        k_hash_warp<512, 8><<<grid_for(k_hash_warp<512, 8>, 256, sizeof(W512), (nbc + 7) / 8), 256,
+                              sizeof(W512), st>>>(ha, 0, 511);
+        if (maxf > 511 && wmax > 511)
+            k_hash_warp<1024, 8><<<grid_for(k_hash_warp<1024, 8>, 256, sizeof(W1K), (nbc + 7) / 8),
+                                   256, sizeof(W1K), st>>>(ha, 511, 1023);
+        if (maxf > wmax)
+            k_hash_cols<128, 2048, 1024><<<grid_for(k_hash_cols<128, 2048, 1024>, 128, sizeof(Small), nbc),
+                                           128, sizeof(Small), st>>>(ha, wmax, HASH_SMALL_F);
         if (maxf > HASH_SMALL_F)
             k_hash_cols<512, 8192, 4096><<<ctx->num_sms, 512, sizeof(Big), st>>>(ha, HASH_SMALL_F,
                                                                                  HASH_BIG_F);

@@ -191,6 +191,135 @@ __global__ void __launch_bounds__(NT) k_hash_cols(HashArgs a, uint64_t lo_f, uin
     (void)lane;
 }
 
+// Short columns, one WARP per column (no block barriers): a TW-slot table
+// per warp in shared memory; products flattened over the warp (a B chunk's
+// A-column lengths are scanned across lanes, each lane finds its product's
+// B entry by a shuffle search); in-place compaction of the occupied slots
+// in slot order (a warp's chunk is read before any write lands at or below
+// it); a bitonic network in the table's front; then the scratch range.
+template <int TW, int NWARP>
+struct HashWarpSmem {
+    uint32_t key[NWARP][TW];
+    double val[NWARP][TW];
+};
+
+template <int TW, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32) k_hash_warp(HashArgs a, uint64_t lo_f, uint64_t hi_f) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    auto& sm = *reinterpret_cast<HashWarpSmem<TW, NWARP>*>(smem_raw);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* K = sm.key[w];
+    double* V = sm.val[w];
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * NWARP + w;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * NWARP;
+    for (uint64_t j = gw; j < a.ncols; j += nwarps) {
+        const uint64_t f = a.flop[j];
+        if (f <= lo_f || f > hi_f) continue;
+        uint32_t T = 32;
+        while (T < f + 1) T <<= 1;
+        for (uint32_t s2 = lane; s2 < T; s2 += 32) {
+            K[s2] = HASH_EMPTY;
+            V[s2] = 0.0;
+        }
+        __syncwarp();
+        // ---- products, 32 B entries per chunk, flattened over the lanes
+        const uint64_t b0 = a.b_colptr[j], b1 = a.b_colptr[j + 1];
+        for (uint64_t c0 = b0; c0 < b1; c0 += 32) {
+            const uint64_t p = c0 + lane;
+            uint64_t qs = 0;
+            uint32_t len = 0;
+            double bv = 0.0;
+            if (p < b1) {
+                const uint32_t i = a.b_rowids[p];
+                bv = a.b_vals[p];
+                qs = a.a_colptr[i];
+                len = static_cast<uint32_t>(a.a_colptr[i + 1] - qs);
+            }
+            const uint32_t incl = warp_inclusive_scan(len);
+            const uint32_t tot = __shfl_sync(FULL, incl, 31);
+            const uint32_t excl = incl - len;
+            for (uint32_t t0 = 0; t0 < tot; t0 += 32) {
+                const uint32_t t = t0 + lane;
+                // owner: the number of lanes whose inclusive prefix is <= t
+                int lo = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const uint32_t v = __shfl_sync(FULL, incl, lo + st - 1);
+                    if (v <= t) lo += st;
+                }
+                const uint64_t oqs = __shfl_sync(FULL, qs, lo);
+                const double obv = __shfl_sync(FULL, bv, lo);
+                const uint32_t oex = __shfl_sync(FULL, excl, lo);
+                if (t < tot) {
+                    const uint64_t q = oqs + (t - oex);
+                    const uint32_t r = a.a_rowids[q];
+                    const double v = a.a_vals[q] * obv;
+                    uint32_t h = static_cast<uint32_t>((r * 0x9E3779B97F4A7C15ull) >> 32) & (T - 1);
+                    while (true) {
+                        const uint32_t old = atomicCAS(&K[h], HASH_EMPTY, r);
+                        if (old == HASH_EMPTY || old == r) {
+                            atomicAdd(&V[h], v);
+                            break;
+                        }
+                        h = (h + 1) & (T - 1);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // ---- in-place compaction in slot order
+        uint32_t m = 0;
+        for (uint32_t s0 = 0; s0 < T; s0 += 32) {
+            const uint32_t s2 = s0 + lane;
+            const uint32_t k = K[s2];
+            const double v = V[s2];
+            const bool occ = k != HASH_EMPTY;
+            const uint32_t bal = __ballot_sync(FULL, occ);
+            __syncwarp();
+            if (occ) {
+                const uint32_t o = m + __popc(bal & lanemask_lt());
+                K[o] = k;
+                V[o] = v;
+            }
+            m += __popc(bal);
+            __syncwarp();
+        }
+        // ---- bitonic sort of K/V[0, P), P = bit_ceil(m), padded with EMPTY
+        uint32_t P = 1;
+        while (P < m) P <<= 1;
+        for (uint32_t e = m + lane; e < P; e += 32) K[e] = HASH_EMPTY;
+        __syncwarp();
+        for (uint32_t k2 = 2; k2 <= P; k2 <<= 1) {
+            for (uint32_t jj = k2 >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t e0 = 0; e0 < P / 2; e0 += 32) {
+                    const uint32_t c = e0 + lane;  // compare-exchange index
+                    if (c < P / 2) {
+                        const uint32_t e = 2 * c - (c & (jj - 1));  // lower element of the pair
+                        const uint32_t x = e + jj;
+                        const bool up = (e & k2) == 0;
+                        const uint32_t ke = K[e], kx = K[x];
+                        if ((ke > kx) == up) {
+                            K[e] = kx;
+                            K[x] = ke;
+                            const double t2 = V[e];
+                            V[e] = V[x];
+                            V[x] = t2;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        const uint64_t base = a.bound[j];
+        for (uint32_t e = lane; e < m; e += 32) {
+            a.s_rows[base + e] = K[e];
+            a.s_vals[base + e] = V[e];
+        }
+        if (lane == 0) a.count[j] = m;
+        __syncwarp();
+    }
+}
+
 // Columns above the large-table capacity: flag them (the host reports
 // PBG_ERR_UNIMPLEMENTED).
 __global__ void k_hash_check(const uint64_t* __restrict__ flop, uint64_t ncols, uint64_t hi_f,

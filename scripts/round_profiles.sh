@@ -16,4 +16,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 # full sections of the three top kernels (second multiply)
 ncu --set full --clock-control none --import-source on -k regex:"k_expand|k_bincount|k_sortmerge" \
   -s 3 -c 3 -o $O/full_C2 python scripts/profile_step.py --config C2 --steps 1 > /dev/null 2>&1
+timeout 600 python scripts/bench_hash.py C1 C2 C4 C5a > $O/bench_hash.jsonl 2> $O/bench_hash.err
+timeout 900 python -m pytest tests -m gpu -q > $O/gputests.log 2>&1
 echo done
