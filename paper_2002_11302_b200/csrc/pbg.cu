@@ -444,7 +444,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             else k_expand<uint64_t, PBG_EXP_MINB><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         }
         L += 2;
-#if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE) || defined(PBG_DIAG_REGION)
+#if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE) || defined(PBG_DIAG_REGION) || \
+    defined(PBG_DIAG_NOBLOAD) || defined(PBG_DIAG_NOKEYST) || defined(PBG_DIAG_NOVALST)
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(PBG_ERR_INTERNAL, "diagnostic build: stopped after the expand");
 #endif

@@ -497,8 +497,13 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                     ri = ok[u] ? ri : 0;
                     const uint64_t q = t - s_st[w][ri];
                     const uint64_t src = s_bst[w][ri] + q;
+#ifdef PBG_DIAG_NOBLOAD  // timing experiment: no B gathers (wrong output)
+                    kv[u] = static_cast<uint32_t>(src) & 0xfffffu;
+                    bv[u] = 1.0;
+#else
                     kv[u] = ok[u] ? __ldg(a.b_colids + src) : 0u;
                     bv[u] = ok[u] ? __ldg(a.b_vals + src) : 0.0;
+#endif
                     rpv[u] = s_rp[w][ri];
                     avv[u] = s_av[w][ri];
 #ifdef PBG_DIAG_SEQSTORE
@@ -518,8 +523,12 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                     if (ok[u])
 #endif
                     {
+#ifndef PBG_DIAG_NOKEYST
                         st_tuple_key(a.keys + dv[u], rpv[u] | kv[u], pol);
+#endif
+#ifndef PBG_DIAG_NOVALST
                         st_tuple_val(a.vals + dv[u], avv[u] * bv[u], pol);
+#endif
                     }
                 }
                 // ---- stage 2 of the next batch, once its stage-1 loads landed
