@@ -445,7 +445,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         }
         L += 2;
 #if defined(PBG_DIAG_SEQSTORE) || defined(PBG_DIAG_NOSTORE) || defined(PBG_DIAG_REGION) || \
-    defined(PBG_DIAG_NOBLOAD) || defined(PBG_DIAG_NOKEYST) || defined(PBG_DIAG_NOVALST)
+    defined(PBG_DIAG_NOBLOAD) || defined(PBG_DIAG_NOKEYST) || defined(PBG_DIAG_NOVALST) || \
+    defined(PBG_DIAG_AOS12) || defined(PBG_DIAG_AOS16)
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(PBG_ERR_INTERNAL, "diagnostic build: stopped after the expand");
 #endif

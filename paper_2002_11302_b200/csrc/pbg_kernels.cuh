@@ -349,6 +349,14 @@ __device__ __forceinline__ void st_tuple_val(double* p, double v, uint64_t pol) 
     *p = v;
 #endif
 }
+__device__ __forceinline__ void st_tuple_key2(uint32_t* p, uint32_t v0, uint32_t v1, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v0), "r"(v1), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_tuple_val2(double* p, double v0, double v1, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v0), "d"(v1), "l"(pol)
+                 : "memory");
+}
 constexpr int EXP_NW = EXP_NT / 32;
 
 // Outer-product expansion (expand_impl, pb_spgemm.cpp:180-246). One warp per
@@ -374,6 +382,9 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
     __shared__ double s_av[EXP_NW][32];
     __shared__ uint64_t s_st[EXP_NW][32];
     __shared__ uint32_t s_rp[EXP_NW][32];
+#ifdef PBG_EXP_PAIRS
+    __shared__ uint32_t s_lb[EXP_NW][32];
+#endif
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -464,8 +475,16 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
             const bool ne = lb != 0;
             const uint32_t nemask = __ballot_sync(FULL, ne);
             const int rank = __popc(nemask & lt);
-            uint64_t incl = warp_inclusive_scan(lb);
-            const uint64_t start = incl - lb;
+#ifdef PBG_EXP_PAIRS
+            // a run is cut into pieces of 2 tuples at even slots (one 8-byte
+            // key store + one 16-byte value store each) plus an odd head/tail
+            const uint64_t hd = lb ? (dst & 1u) : 0u;
+            const uint64_t units = hd + (lb - hd + 1) / 2;
+#else
+            const uint64_t units = lb;
+#endif
+            uint64_t incl = warp_inclusive_scan(units);
+            const uint64_t start = incl - units;
             const uint64_t total = __shfl_sync(FULL, incl, 31);
             if (ne) {
                 s_dst[w][rank] = dst;
@@ -473,11 +492,59 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                 s_av[w][rank] = av;
                 s_st[w][rank] = start;
                 s_rp[w][rank] = rp;
+#ifdef PBG_EXP_PAIRS
+                s_lb[w][rank] = static_cast<uint32_t>(lb);
+#endif
             }
             __syncwarp();
             // tuples, EXP_U steps of 32 per iteration: all B loads of the
             // group are issued before any store so their latencies overlap
             uint32_t before = 0;
+#ifdef PBG_EXP_PAIRS
+            for (uint64_t s0 = 0; s0 < total; s0 += 32 * EXP_U) {
+                uint32_t kv[EXP_U], kv1[EXP_U];
+                double bv[EXP_U], bv1[EXP_U], avv[EXP_U];
+                uint32_t rpv[EXP_U];
+                uint64_t dv[EXP_U];
+                int cntv[EXP_U];
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+                    const uint64_t s = s0 + 32 * u;
+                    const uint32_t bit =
+                        (ne && start >= s && start < s + 32) ? (1u << (start - s)) : 0u;
+                    const uint32_t mk = __reduce_or_sync(FULL, bit);
+                    const uint64_t t = s + lane;
+                    const bool ok = t < total;
+                    const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+                    int ri = static_cast<int>(before + __popc(mk & upto)) - 1;
+                    ri = ok ? ri : 0;
+                    const uint64_t q = t - s_st[w][ri];  // piece of the run
+                    const uint64_t d0 = s_dst[w][ri];
+                    const uint32_t h = static_cast<uint32_t>(d0 & 1u);
+                    const uint32_t off = q == 0 ? 0u : static_cast<uint32_t>(2 * q - h);
+                    const uint32_t L = s_lb[w][ri];
+                    cntv[u] = !ok ? 0 : ((h && q == 0) || off + 1 >= L) ? 1 : 2;
+                    const uint64_t src = s_bst[w][ri] + off;
+                    kv[u] = cntv[u] ? __ldg(a.b_colids + src) : 0u;
+                    bv[u] = cntv[u] ? __ldg(a.b_vals + src) : 0.0;
+                    kv1[u] = cntv[u] == 2 ? __ldg(a.b_colids + src + 1) : 0u;
+                    bv1[u] = cntv[u] == 2 ? __ldg(a.b_vals + src + 1) : 0.0;
+                    rpv[u] = s_rp[w][ri];
+                    avv[u] = s_av[w][ri];
+                    dv[u] = d0 + off;
+                    before += __popc(mk);
+                }
+#pragma unroll
+                for (int u = 0; u < EXP_U; ++u) {
+                    if (cntv[u] == 2) {
+                        st_tuple_key2(a.keys + dv[u], rpv[u] | kv[u], rpv[u] | kv1[u], pol);
+                        st_tuple_val2(a.vals + dv[u], avv[u] * bv[u], avv[u] * bv1[u], pol);
+                    } else if (cntv[u] == 1) {
+                        st_tuple_key(a.keys + dv[u], rpv[u] | kv[u], pol);
+                        st_tuple_val(a.vals + dv[u], avv[u] * bv[u], pol);
+                    }
+                }
+#else
             for (uint64_t s0 = 0; s0 < total; s0 += 32 * EXP_U) {
                 uint32_t kv[EXP_U];
                 double bv[EXP_U], avv[EXP_U];
@@ -523,6 +590,29 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                     if (ok[u])
 #endif
                     {
+#ifdef PBG_DIAG_AOS16  // timing experiment: 16-byte AoS tuples, one vector store each
+                        {
+                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + ((dv[u] * 4) & ((1ull << 29) - 1));
+                            const double vv = avv[u] * bv[u];
+                            const unsigned long long bits = __double_as_longlong(vv);
+                            asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(T),
+                                         "r"(rpv[u] | kv[u]), "r"(0u), "r"(static_cast<uint32_t>(bits)),
+                                         "r"(static_cast<uint32_t>(bits >> 32)), "l"(pol)
+                                         : "memory");
+                        }
+                        continue;
+#endif
+#ifdef PBG_DIAG_AOS12  // timing experiment: 12-byte AoS tuples (one store segment per run)
+                        {
+                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + ((dv[u] * 3) & ((1ull << 29) - 1));
+                            const double vv = avv[u] * bv[u];
+                            const unsigned long long bits = __double_as_longlong(vv);
+                            st_tuple_key(T, rpv[u] | kv[u], pol);
+                            st_tuple_key(T + 1, static_cast<uint32_t>(bits), pol);
+                            st_tuple_key(T + 2, static_cast<uint32_t>(bits >> 32), pol);
+                        }
+                        continue;
+#endif
 #ifndef PBG_DIAG_NOKEYST
                         st_tuple_key(a.keys + dv[u], rpv[u] | kv[u], pol);
 #endif
@@ -531,6 +621,7 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
 #endif
                     }
                 }
+#endif  // PBG_EXP_PAIRS
                 // ---- stage 2 of the next batch, once its stage-1 loads landed
                 if (s0 == 0 && has_next) {
                     const uint64_t pln = pn + lane;
