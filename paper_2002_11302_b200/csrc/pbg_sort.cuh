@@ -440,8 +440,9 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         *res = scr;
         *rshift = 0;  // row starts from the bucket ends if nothing merges
         bool dupz = false;
-        for (uint32_t i = tid + 1; i < n; i += SM_NT) dupz |= sm.k[scr][i] == sm.k[scr][i - 1];
-        if (__syncthreads_or(dupz)) {
+        if (distinct < n)
+            for (uint32_t i = tid + 1; i < n; i += SM_NT) dupz |= sm.k[scr][i] == sm.k[scr][i - 1];
+        if (distinct < n && __syncthreads_or(dupz)) {
             *res = in;
             *rshift = -1;
             return merge_dups(sm, scr, in, n);
@@ -457,10 +458,15 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
             continue;
         }
         uint32_t r = 0;
+        if (distinct < n) {
 #pragma unroll 1
-        for (uint32_t j = lo; j < hi; ++j) {
-            const uint32_t kj = sm.k[scr][j];
-            r += (kj < key) | ((kj == key) & (j < i));
+            for (uint32_t j = lo; j < hi; ++j) {
+                const uint32_t kj = sm.k[scr][j];
+                r += (kj < key) | ((kj == key) & (j < i));
+            }
+        } else {  // all keys distinct
+#pragma unroll 1
+            for (uint32_t j = lo; j < hi; ++j) r += sm.k[scr][j] < key;
         }
         sm.k[in][lo + r] = key;
         sm.v[in][lo + r] = sm.v[scr][i];
@@ -477,10 +483,11 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         sorted = in;
         other = scr;
     }
+    // ---- 3. merge duplicates (none when the count kernel saw n distinct keys)
     bool dup = false;
-    for (uint32_t i = tid + 1; i < n; i += SM_NT) dup |= sm.k[sorted][i] == sm.k[sorted][i - 1];
-    // ---- 3. merge duplicates ----
-    if (__syncthreads_or(dup)) {
+    if (distinct < n)
+        for (uint32_t i = tid + 1; i < n; i += SM_NT) dup |= sm.k[sorted][i] == sm.k[sorted][i - 1];
+    if (distinct < n && __syncthreads_or(dup)) {
         *res = other;
         return merge_dups(sm, sorted, other, n);
     }
