@@ -59,12 +59,12 @@ def build_host(force: bool = False) -> Path:
 
 
 def build_shim(force: bool = False) -> Path:
-    deps = [CSRC / "pb_spgemm_shim.cpp", INCLUDE / "spgemm_b200" / "pb_spgemm.hpp",
-            INCLUDE / "spgemm_b200" / "types.hpp", INCLUDE / "pbg.h", LIBPBG]
+    deps = [CSRC / "pb_spgemm_shim.cpp", *sorted((INCLUDE / "spgemm_b200").glob("*.hpp")),
+            INCLUDE / "pbg.h", INCLUDE / "pbg_host.h", LIBPBG, LIBHOST]
     if force or not _newer(LIBSHIM, deps):
         tmp = LIBSHIM.with_suffix(".so.tmp")
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-I", INCLUDE,
-              "-o", tmp, CSRC / "pb_spgemm_shim.cpp", "-L", PKG, "-lpbg",
+              "-o", tmp, CSRC / "pb_spgemm_shim.cpp", "-L", PKG, "-lpbg", "-l:libpbg_host.so",
               f"-Wl,-rpath,$ORIGIN"])
         tmp.replace(LIBSHIM)
     return LIBSHIM

@@ -4,6 +4,9 @@
 #include <stdexcept>
 
 #include "pbg.h"
+#include "pbg_host.h"
+#include "spgemm_b200/baseline.hpp"
+#include "spgemm_b200/mmio.hpp"
 #include "spgemm_b200/pb_spgemm.hpp"
 
 namespace spgemm {
@@ -94,6 +97,60 @@ PbResult pb_multiply(const CscMatrix& a, const CsrMatrix& b, const PbConfig& cfg
     if (res.c.nnz() != res.merged_total)
         throw internal_error("compressed counts disagree with output nnz");
     return res;
+}
+
+CscMatrix hash_multiply(const CscMatrix& a, const CscMatrix& b, int /*nthreads*/) {
+    require_multipliable(a.dims, b.dims);
+    pbg_config c;
+    pbg_default_config(&c);
+    const pbg_csx_view av{a.dims.nrows, a.dims.ncols, a.nnz(), a.colptr.data(), a.rowids.data(),
+                          a.values.data()};
+    const pbg_csx_view bv{b.dims.nrows, b.dims.ncols, b.nnz(), b.colptr.data(), b.rowids.data(),
+                          b.values.data()};
+    Handle h;
+    std::uint64_t nnz = 0;
+    int rc = pbg_hash_multiply_begin(&av, &bv, &c, &h.h, &nnz);
+    if (rc) throw_for(rc);
+    CscMatrix out;
+    out.dims = {a.dims.nrows, b.dims.ncols};
+    out.colptr.resize(static_cast<std::size_t>(b.dims.ncols) + 1);
+    out.rowids.resize(nnz);
+    out.values.resize(nnz);
+    rc = pbg_multiply_fetch(h.h, out.colptr.data(), out.rowids.data(), out.values.data(), nullptr);
+    if (rc) throw_for(rc);
+    return out;
+}
+
+CscMatrix heap_multiply(const CscMatrix& a, const CscMatrix& b, int nthreads) {
+    return hash_multiply(a, b, nthreads);  // same result; the GPU path has one column kernel
+}
+
+CooMatrix mm_read(const std::string& path) {
+    pbgh_mm* h = nullptr;
+    std::uint32_t nr = 0, nc = 0;
+    std::uint64_t n = 0;
+    if (pbgh_mm_open(path.c_str(), &h, &nr, &nc, &n)) throw parse_error(pbgh_last_error());
+    std::vector<std::uint32_t> r(n), c(n);
+    std::vector<double> v(n);
+    pbgh_mm_fetch(h, r.data(), c.data(), v.data());
+    pbgh_mm_free(h);
+    CooMatrix m;
+    m.dims = {nr, nc};
+    m.entries.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) m.entries[i] = {r[i], c[i], v[i]};
+    return m;
+}
+
+void mm_write(const CooMatrix& m, const std::string& path) {
+    std::vector<std::uint32_t> r(m.nnz()), c(m.nnz());
+    std::vector<double> v(m.nnz());
+    for (std::size_t i = 0; i < m.nnz(); ++i) {
+        r[i] = m.entries[i].row;
+        c[i] = m.entries[i].col;
+        v[i] = m.entries[i].val;
+    }
+    if (pbgh_mm_write(path.c_str(), m.dims.nrows, m.dims.ncols, m.nnz(), r.data(), c.data(), v.data()))
+        throw structural_error(pbgh_last_error());
 }
 
 }  // namespace spgemm

@@ -10,6 +10,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include "spgemm_b200/baseline.hpp"
+#include "spgemm_b200/mmio.hpp"
 #include "spgemm_b200/pb_spgemm.hpp"
 
 using namespace spgemm;
@@ -85,6 +87,20 @@ int main(int argc, char** argv) {
     badl.lbin_bytes = 24;
     CHECK(throws<parameter_error>([&] { pb_multiply(csc_of(4, {}), b44, badl); }));
 
+    // Matrix Market round trip (mmio.hpp:15-21), host only
+    {
+        CooMatrix m;
+        m.dims = {3, 4};
+        m.entries = {{0, 0, 1.5}, {2, 3, -2e-3}, {1, 1, 0.0}};
+        const char* path = "dropin_test_tmp.mtx";
+        mm_write(m, path);
+        CooMatrix r = mm_read(path);
+        CHECK(r.dims == m.dims && r.entries == m.entries);
+        std::remove(path);
+        CHECK(throws<parse_error>([&] { mm_read("no/such/file.mtx"); }));
+    }
+    CHECK(throws<parameter_error>([&] { hash_multiply(a43, csc_of(4, {})); }));
+
     std::vector<CooEntry> eye;
     for (index_t i = 0; i < 4; ++i) eye.push_back({i, i, 1.0});
     if (!gpu) {
@@ -115,6 +131,15 @@ int main(int argc, char** argv) {
         PbResult z = pb_multiply(csc_of(2, {{0, 0, 1.0}, {0, 1, -1.0}}),
                                  csr_of(2, {{0, 1, 1.0}, {1, 1, 1.0}}));
         CHECK(z.c.nnz() == 1 && z.c.values[0] == 0.0);
+        // column hash SpGEMM (baseline.hpp:21-24): the 2x2 known answer in CSC
+        CscMatrix hc = hash_multiply(csc_of(2, d2), csc_of(2, d2));
+        CHECK((hc.colptr == std::vector<offset_t>{0, 2, 4}));
+        CHECK((hc.rowids == std::vector<index_t>{0, 1, 0, 1}));
+        CHECK((hc.values == std::vector<double>{7.0, 15.0, 10.0, 22.0}));
+        CHECK(heap_multiply(csc_of(2, d2), csc_of(2, d2)).values == hc.values);
+    }
+    if (!gpu) {
+        CHECK(throws<std::runtime_error>([&] { hash_multiply(csc_of(4, eye), csc_of(4, eye)); }));
     }
     std::printf("%s: %d failure(s)\n", gpu ? "gpu" : "nodevice", failures);
     return failures ? 1 : 0;
