@@ -106,8 +106,10 @@ struct BinMeta {
 };
 
 struct SortSmem {
-    uint32_t k[SM_NBUF][SM_CAP];
-    double v[SM_NBUF][SM_CAP];
+    // +4 / +2 slack: a duplicate-free bin is written sorted at an offset that
+    // aligns it with its 16-byte-aligned place in C (TMA bulk store)
+    uint32_t k[SM_NBUF][SM_CAP + 4];
+    double v[SM_NBUF][SM_CAP + 2];
     uint16_t cnt[SM_NB];  // bucket histogram -> bucket ends; LSD per-warp counters
     uint32_t s_warp32[SM_NW + 1];
     unsigned long long mbar;
@@ -136,6 +138,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_addr(bar))
         : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_addr(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the bulk stores issued so far have finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -395,10 +412,14 @@ __device__ uint32_t hash_premerge(SortSmem& sm, int in, int scr, uint32_t n) {
 // merged count; *res gets the buffer holding the merged output.
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
                                    int bits, uint32_t keylo, uint32_t distinct, int* res,
-                                   int* rshift,
+                                   int* rshift, uint64_t P, int* bulk,
                                    int next_slot, uint64_t next_bin, long long& prof_t) {
     const int tid = threadIdx.x;
+    *bulk = 0;
+    // the previous bin's bulk store reads buffer `scr`: done before it is written
+    if (tid == 0) bulk_wait_read();
     if (distinct * 2 <= n && n >= 64) {
+        __syncthreads();  // thread 0's bulk_wait_read before anyone writes `scr`
         n = hash_premerge(sm, in, scr, n);  // now n distinct keys, no duplicates
         zero_cnt(sm);
         __syncthreads();
@@ -449,6 +470,9 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         }
         return n;
     }
+    const bool nodup = distinct >= n;
+    const uint32_t shK = static_cast<uint32_t>(P & 3), shV = static_cast<uint32_t>(P & 1);
+    const uint32_t colmask = a.col_bits >= 32 ? 0xffffffffu : ((1u << a.col_bits) - 1u);
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[scr][i];
         const uint32_t d = (key - keylo) >> sh;
@@ -468,8 +492,13 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
 #pragma unroll 1
             for (uint32_t j = lo; j < hi; ++j) r += sm.k[scr][j] < key;
         }
-        sm.k[in][lo + r] = key;
-        sm.v[in][lo + r] = sm.v[scr][i];
+        if (nodup) {  // final form: masked column ids, C-aligned offsets
+            sm.k[in][lo + r + shK] = key & colmask;
+            sm.v[in][lo + r + shV] = sm.v[scr][i];
+        } else {
+            sm.k[in][lo + r] = key;
+            sm.v[in][lo + r] = sm.v[scr][i];
+        }
     }
     const bool any_big = __syncthreads_or(big);
     PROF_MARK(3);
@@ -493,6 +522,8 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     }
     *res = sorted;
     *rshift = any_big ? -1 : sh;  // sorted positions = bucket ends: row starts from them
+    *bulk = !any_big && nodup && sh <= a.col_bits;
+    if (*bulk) fence_proxy_async_smem();  // this thread's smem writes -> the TMA store
     return n;
 }
 
@@ -531,6 +562,41 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
             else hi = mid;
         }
         a.rowptr[rs + r] = P + lo;
+    }
+    if (tid == 0 && b == nw - 1) a.rowptr[a.m] = P + U;
+}
+
+// Output of a duplicate-free bin sorted in final form (masked column ids at
+// smem index u + (P & 3), values at u + (P & 1), so smem and C agree modulo
+// 16 bytes): thread 0 hands the 16-byte-aligned middles to the TMA engine
+// (cp.async.bulk shared -> global, one bulk group) and a few threads store
+// the unaligned head/tail elements; row starts come from the bucket ends.
+// The buffer may be overwritten only after bulk_wait_read().
+__device__ __forceinline__ void write_bin_bulk(const SortArgs& a, SortSmem& sm, int buf, uint64_t b,
+                                               uint64_t nw, uint32_t rs, uint32_t span, uint32_t U,
+                                               uint64_t P, int rshift) {
+    const int tid = threadIdx.x;
+    const uint32_t shK = static_cast<uint32_t>(P & 3), shV = static_cast<uint32_t>(P & 1);
+    const uint32_t* K = sm.k[buf] + shK;
+    const double* V = sm.v[buf] + shV;
+    uint32_t ka = (4u - shK) & 3u, va = shV;
+    if (ka > U) ka = U;
+    if (va > U) va = U;
+    const uint32_t kb = ka + ((U - ka) & ~3u), vb = va + ((U - va) & ~1u);
+    if (tid < ka) a.ccol[P + tid] = K[tid];
+    if (tid < U - kb) a.ccol[P + kb + tid] = K[kb + tid];
+    if (tid < va) a.cval[P + tid] = V[tid];
+    if (tid < U - vb) a.cval[P + vb + tid] = V[vb + tid];
+    if (tid == 0) {
+        fence_proxy_async_smem();  // the whole CTA's smem writes (barrier before) to the async proxy
+        if (kb > ka) bulk_s2g(a.ccol + P + ka, K + ka, (kb - ka) * 4);
+        if (vb > va) bulk_s2g(a.cval + P + va, V + va, (vb - va) * 8);
+        bulk_commit();
+    }
+    const int cb = a.col_bits;
+    for (uint32_t r = tid; r < span; r += SM_NT) {
+        const uint32_t d = (r << cb) >> rshift;
+        a.rowptr[rs + r] = P + (d ? sm.cnt[d - 1] : 0u);
     }
     if (tid == 0 && b == nw - 1) a.rowptr[a.m] = P + U;
 }
@@ -582,7 +648,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         const uint32_t tk = tid == 0 ? atomicAdd(a.ticket, 1u) : 0u;
         if (tid == 0 && M.n > SM_CAP && !(M.flags & 2u)) atomicOr(a.err, 2u);
         int res = inb;
-        int rshift = -1;
+        int rshift = -1, bulk = 0;
         uint32_t U = 0;
         bool merged = false, fetched = false;
         if (loaded) {
@@ -602,7 +668,8 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             __syncthreads();
             PROF_MARK(0);
             U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(M.keybits), M.keylo,
-                               static_cast<uint32_t>(M.nnz), &res, &rshift, mc ^ 1, tk, prof_t);
+                               static_cast<uint32_t>(M.nnz), &res, &rshift, M.out, &bulk, mc ^ 1,
+                               tk, prof_t);
             fetched = true;
 #ifdef PBG_SORT_PROF
             __syncthreads();
@@ -620,9 +687,12 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         }
         __syncthreads();
         // next work bin's copy into the free buffer overlaps this one's output
-        if (tid == 0 && sm.s_bin[mc ^ 1] < nw && bin_kind(sm.meta[mc ^ 1]) == 1)
+        if (tid == 0 && sm.s_bin[mc ^ 1] < nw && bin_kind(sm.meta[mc ^ 1]) == 1) {
+            bulk_wait_read();  // a previous bulk store may still read that buffer
             issue_tma(a, sm, res ^ 1, sm.meta[mc ^ 1]);
+        }
         if (merged) write_merged(a, M, b, nw, M.out, U);
+        else if (bulk) write_bin_bulk(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift);
         else write_bin(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift);
         PROF_MARK(5);
         inb = res ^ 1;
@@ -630,6 +700,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         __syncthreads();
         PROF_MARK(6);
     }
+    if (tid == 0) bulk_wait_all();  // the last bins' C stores are complete
 }
 
 }  // namespace pbg
