@@ -58,8 +58,9 @@ __device__ __forceinline__ T warp_sum(T x) {
 
 // Block-wide exclusive scan of one value per thread. s_warp needs NT/32+1
 // slots. Returns the exclusive prefix and the block total. Ends with a
-// __syncthreads so s_warp can be reused immediately.
-template <int NT, typename T>
+// __syncthreads so s_warp can be reused immediately (TRAIL = false: the
+// caller guarantees a barrier before s_warp's next use).
+template <int NT, typename T, bool TRAIL = true>
 __device__ __forceinline__ T block_exclusive_scan(T v, T* s_warp, T& total) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -75,7 +76,7 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* s_warp, T& total) {
     __syncthreads();
     T excl = s_warp[w] + x - v;
     total = s_warp[NW];
-    __syncthreads();
+    if (TRAIL) __syncthreads();
     return excl;
 }
 

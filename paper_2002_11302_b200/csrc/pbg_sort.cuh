@@ -229,7 +229,8 @@ __device__ __forceinline__ void scan_cnt(SortSmem& sm) {
 #pragma unroll
     for (int j = 0; j < 4 * SM_CQ; ++j) s8 += (rw[j] & 0xffffu) + (rw[j] >> 16);
     uint32_t tot;
-    uint32_t run = block_exclusive_scan<SM_NT>(s8, sm.s_warp32, tot);
+    // (the caller's barrier after scan_cnt protects s_warp32)
+    uint32_t run = block_exclusive_scan<SM_NT, uint32_t, false>(s8, sm.s_warp32, tot);
 #pragma unroll
     for (int j = 0; j < 4 * SM_CQ; ++j) {
         const uint32_t lo = run;
