@@ -26,7 +26,13 @@
 //      independent: no look-back chain, no waiting on slower neighbours.
 //      (A single-pass decoupled look-back over U_b was measured 2-3x slower:
 //      per-bin work is long and uneven, so every CTA ended up waiting on the
-//      slowest in-flight predecessor.)
+//      slowest in-flight predecessor; a one-bin-lagged variant tied.)
+//      A bin the count found duplicate-free skips the duplicate check, is
+//      ranked in final form (masked column ids at a shared-memory offset
+//      congruent to its place in C modulo 16 B) and leaves through TMA bulk
+//      stores (cp.async.bulk shared -> global); its row starts come from
+//      the MSD bucket ends. Work-bin descriptors are staged by cp.async one
+//      bin ahead.
 #pragma once
 
 #include <cstdint>
