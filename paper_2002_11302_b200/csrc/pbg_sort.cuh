@@ -62,6 +62,18 @@ constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
 #define PBG_SM_BMAX 128
 #endif
 constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
+#ifndef PBG_RANK_UNROLL
+#define PBG_RANK_UNROLL 1
+#endif
+#ifndef PBG_HIST_UNROLL
+#define PBG_HIST_UNROLL 1
+#endif
+#ifndef PBG_SCAT_UNROLL
+#define PBG_SCAT_UNROLL 1
+#endif
+constexpr int RANK_UNROLL = PBG_RANK_UNROLL;  // tuning hooks (A/B)
+constexpr int SCAT_UNROLL = PBG_SCAT_UNROLL;
+constexpr int HIST_UNROLL = PBG_HIST_UNROLL;
 constexpr int SM_ITEMS = SM_CAP / SM_NT;      // 8
 constexpr int SM_PER_WARP = SM_CAP / SM_NW;
 constexpr int SM_NBUF = 2;                    // ping, pong
@@ -436,6 +448,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     // ---- 1. bucket histogram / scan / scatter in -> scr ----
     // (keeping the histogram's returned slot in registers to save the second
     // atomic was measured slower: register pressure at 64 regs spills)
+#pragma unroll HIST_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t d = (sm.k[in][i] - keylo) >> sh;
         atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
@@ -446,6 +459,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     PROF_MARK(1);
     // the next bin's descriptor (its ticket was taken at the loop top)
     if (threadIdx.x == 0) meta_fetch(a, sm, next_slot, next_bin, *a.nw_dev);
+#pragma unroll SCAT_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[in][i];
         const uint32_t d = (key - keylo) >> sh;
@@ -480,6 +494,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     const bool nodup = distinct >= n;
     const uint32_t shK = static_cast<uint32_t>(P & 3), shV = static_cast<uint32_t>(P & 1);
     const uint32_t colmask = a.col_bits >= 32 ? 0xffffffffu : ((1u << a.col_bits) - 1u);
+#pragma unroll RANK_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t key = sm.k[scr][i];
         const uint32_t d = (key - keylo) >> sh;
