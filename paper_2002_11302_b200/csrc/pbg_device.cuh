@@ -123,101 +123,6 @@ __device__ __forceinline__ uint64_t lookback_warp(unsigned long long* status, ui
     return prefix;
 }
 
-// Second half of a deferred decoupled look-back: the tile published its
-// aggregate earlier (ST_AGG, or ST_INC for tile 0); now walk predecessors,
-// LB_W per step (LB_T per lane), publish the inclusive prefix and return the
-// exclusive one. The walker also "helps": every predecessor it summed in the
-// window that held the inclusive prefix gets its own inclusive value
-// published, so later walks stop close by. Called by one full warp.
-#ifndef PBG_LB_T
-#define PBG_LB_T 8
-#endif
-#ifndef PBG_LB_HELP
-#define PBG_LB_HELP 1
-#endif
-constexpr int LB_T = PBG_LB_T;
-constexpr int LB_W = 32 * LB_T;
-
-__device__ __forceinline__ uint64_t lookback_resolve(unsigned long long* status, uint64_t tile,
-                                                     uint64_t aggregate) {
-    const int lane = threadIdx.x & 31;
-    if (tile == 0) return 0;
-    uint64_t prefix = 0;
-    int64_t top = static_cast<int64_t>(tile) - 1;
-    while (true) {
-        uint64_t s[LB_T];
-#pragma unroll
-        for (int t = 0; t < LB_T; ++t) {
-            const int64_t j = top - LB_T * lane - t;
-            s[t] = j >= 0 ? ld_relaxed_gpu(&status[j]) : ST_INC;
-        }
-        int tinc;
-        int first;
-        while (true) {
-            tinc = LB_T;
-#pragma unroll
-            for (int t = LB_T - 1; t >= 0; --t)
-                if ((s[t] >> 62) == 2) tinc = t;
-            const uint32_t incm = __ballot_sync(FULL, tinc < LB_T);
-            first = incm ? __ffs(incm) - 1 : 32;
-            bool bad = false;
-#pragma unroll
-            for (int t = 0; t < LB_T; ++t) {
-                const bool used = lane < first || (lane == first && t <= tinc);
-                bad |= used && (s[t] >> 62) == 0;
-            }
-            if (!__any_sync(FULL, bad)) break;
-            __nanosleep(32);
-#pragma unroll
-            for (int t = 0; t < LB_T; ++t)
-                if ((s[t] >> 62) == 0) s[t] = ld_relaxed_gpu(&status[top - LB_T * lane - t]);
-        }
-        // sum of the entries strictly more recent than the inclusive one, and
-        // the inclusive value itself
-        uint64_t agg = 0, incv = 0;
-#pragma unroll
-        for (int t = 0; t < LB_T; ++t) {
-            if (lane < first || (lane == first && t < tinc)) agg += s[t] & ST_VAL;
-            if (lane == first && t == tinc) incv = s[t] & ST_VAL;
-        }
-        const uint64_t wagg = warp_sum(agg);
-        if (first < 32) {
-            incv = __shfl_sync(FULL, incv, first);
-            prefix += wagg + incv;
-            if (!PBG_LB_HELP) break;
-            // help: inclusive value of every AGG entry in this window
-            // incl(entry) = incv + sum of AGG values from that entry down to
-            // (excluding) the inclusive one = incv + (lanes after me) + my tail
-            uint64_t after = 0;  // sum of agg over lanes > lane (<= first)
-            {
-                uint64_t x = agg;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint64_t y = __shfl_down_sync(FULL, x, o);
-                    if (lane + o < 32) x += y;
-                }
-                after = x - agg;
-            }
-            uint64_t run = incv + after;
-#pragma unroll
-            for (int t = LB_T - 1; t >= 0; --t) {
-                if (lane < first || (lane == first && t < tinc)) {
-                    run += s[t] & ST_VAL;
-                    if ((s[t] >> 62) == 1) {
-                        const int64_t j = top - LB_T * lane - t;
-                        st_relaxed_gpu(&status[j], ST_INC | (run & ST_VAL));
-                    }
-                }
-            }
-            break;
-        }
-        prefix += wagg;
-        top -= LB_W;
-    }
-    if (lane == 0) st_release_gpu(&status[tile], ST_INC | ((prefix + aggregate) & ST_VAL));
-    return prefix;
-}
-
 // Largest i in [lo, hi) with a[i] <= x, assuming a[lo] <= x and a nondecreasing.
 __device__ __forceinline__ uint64_t last_le(const uint64_t* __restrict__ a, uint64_t lo,
                                             uint64_t hi, uint64_t x) {
