@@ -355,7 +355,11 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ctx->nnz_c = 0;
     } else {
         if ((rc = grow(ctx->keys, tcap * 4))) return rc;
+#if defined(PBG_DIAG_AOS12) || defined(PBG_DIAG_AOS16)
+        if ((rc = grow(ctx->vals, tcap * 16))) return rc;  // timing experiment: AoS tuples
+#else
         if ((rc = grow(ctx->vals, tcap * 8))) return rc;
+#endif
         // C arrays sized to the flop upper bound (nnz(C) <= flop): no sync
         // for nnz(C) before the sort kernel
         if ((rc = grow(ctx->ccol, flop * 4))) return rc;

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                     {
 #ifdef PBG_DIAG_AOS16  // timing experiment: 16-byte AoS tuples, one vector store each
                         {
-                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + ((dv[u] * 4) & ((1ull << 29) - 1));
+                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + dv[u] * 4;
                             const double vv = avv[u] * bv[u];
                             const unsigned long long bits = __double_as_longlong(vv);
                             asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(T),
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
 #endif
 #ifdef PBG_DIAG_AOS12  // timing experiment: 12-byte AoS tuples (one store segment per run)
                         {
-                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + ((dv[u] * 3) & ((1ull << 29) - 1));
+                            uint32_t* T = reinterpret_cast<uint32_t*>(a.vals) + dv[u] * 3;
                             const double vv = avv[u] * bv[u];
                             const unsigned long long bits = __double_as_longlong(vv);
                             st_tuple_key(T, rpv[u] | kv[u], pol);
