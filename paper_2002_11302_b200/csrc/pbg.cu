@@ -609,21 +609,32 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         const uint64_t* nw_dev = reinterpret_cast<const uint64_t*>(sc + S_NWORK);
 
         // ---- distinct keys per work bin -> output offset of every work bin ----
-        static bool cnt_attr[64] = {};
-        const size_t cnt_smem = CNT_SLOTS * 4;
-        if (!cnt_attr[ctx->device & 63]) {
-            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(cnt_smem)));
-            CUDA_TRY(cudaFuncSetAttribute(k_bincount, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          100));
-            cnt_attr[ctx->device & 63] = true;
+        // count-kernel shape: the large table pays on distinct-key bins; long
+        // rows (the stencil, > 512 products per output row on average) and
+        // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
+        const bool big_table = H == 0 && flop <= 512 * m;
+        auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
+            static bool attr_set[2][64] = {};  // [shape][device]
+            if (!attr_set[big_table][ctx->device & 63]) {
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem)));
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              100));
+                attr_set[big_table][ctx->device & 63] = true;
+            }
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem);
+            if (const char* e = getenv("PBG_CNT_PER_SM")) per_sm = atoi(e);  // tuning hook
+            kern<<<static_cast<unsigned>(std::min<uint64_t>(
+                       wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms)),
+                   nt, smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
+            return PBG_OK;
+        };
+        if (big_table) {
+            if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
+        } else {
+            if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
         }
-        int cnt_per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cnt_per_sm, k_bincount, CNT_NT, cnt_smem);
-        if (const char* e = getenv("PBG_CNT_PER_SM")) cnt_per_sm = atoi(e);  // tuning hook
-        k_bincount<<<static_cast<unsigned>(std::min<uint64_t>(
-                         wcap, static_cast<uint64_t>(std::max(cnt_per_sm, 1)) * ctx->num_sms)),
-                     CNT_NT, cnt_smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
         ++L;
         // wcap can exceed the m-sized status pool: give this scan its own words
         {

@@ -550,22 +550,20 @@ __global__ void k_work_fill_items(const uint64_t* __restrict__ wpos,
 // a full bin, so probe chains stay short and warps rarely diverge). A scan of
 // these counts gives every work bin its output offset before the sort+merge
 // kernel runs, so bins never wait on each other. Uniform-key items count 1.
-#ifndef PBG_CNT_NT
-#define PBG_CNT_NT 512
-#endif
-constexpr int CNT_NT = PBG_CNT_NT;
-#ifndef PBG_CNT_SLOTS_LOG
-#define PBG_CNT_SLOTS_LOG 14
-#endif
-constexpr int CNT_SLOTS_LOG = PBG_CNT_SLOTS_LOG;
-constexpr int CNT_SLOTS = 1 << CNT_SLOTS_LOG;
+// Two shapes (template): 512 threads with a 16 K-slot table (3 CTAs/SM) and
+// 1024 threads with a 27 K-slot table (2 CTAs/SM, 64 warps). The large table
+// (load ~1/7) cuts the probe chains of distinct-key bins (C2 count 1.30 ->
+// 1.15 ms, C5a 5.4 -> 4.9 ms); duplicate-heavy inputs (the stencil, RMAT)
+// gain nothing from it and lose the third CTA per SM (C4 3.4 -> 4.2 ms), so
+// the host picks the shape from the bin statistics (CountShape below).
 constexpr uint32_t CNT_EMPTY = 0xffffffffu;
-constexpr int CNT_PER = 4096 / CNT_NT;  // keys per thread: bins of up to CNT_NT*CNT_PER = 4096 tuples
 
+template <int NT>
 __device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
                                          const uint32_t* __restrict__ skeys, const WorkBins& w,
-                                         uint64_t b, uint64_t nw, uint64_t cap, uint32_t (&kk)[CNT_PER],
-                                         uint32_t& n) {
+                                         uint64_t b, uint64_t nw, uint64_t cap,
+                                         uint32_t (&kk)[4096 / NT], uint32_t& n) {
+    constexpr int PER = 4096 / NT;  // keys per thread: bins of up to 4096 tuples
     n = 0;
     if (b >= nw) return;
     const uint32_t fl = w.flags[b];
@@ -574,42 +572,47 @@ __device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
     n = static_cast<uint32_t>(nn);
     const uint32_t* kb = ((fl & 1u) ? skeys : keys) + w.off[b];
 #pragma unroll
-    for (int j = 0; j < CNT_PER; ++j) {
-        const uint32_t i = threadIdx.x + j * CNT_NT;
+    for (int j = 0; j < PER; ++j) {
+        const uint32_t i = threadIdx.x + j * NT;
         kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
     }
 }
 
-__global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict__ keys,
-                                                   const uint32_t* __restrict__ skeys,
-                                                   WorkBins w, const uint64_t* nw_dev,
-                                                   uint64_t cap, uint64_t* wb_nnz) {
-    extern __shared__ __align__(16) uint32_t table[];  // CNT_SLOTS
-    __shared__ uint32_t s_red[2][CNT_NT / 32];
+template <int NT, int SLOTS>
+__global__ void __launch_bounds__(NT) k_bincount(const uint32_t* __restrict__ keys,
+                                                 const uint32_t* __restrict__ skeys, WorkBins w,
+                                                 const uint64_t* nw_dev, uint64_t cap,
+                                                 uint64_t* wb_nnz) {
+    constexpr int PER = 4096 / NT;
+    static_assert(SLOTS % 4 == 0, "table cleared in uint4s");
+    extern __shared__ __align__(16) uint32_t table[];  // SLOTS
+    __shared__ uint32_t s_red[2][NT / 32];
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const uint64_t nw = *nw_dev;
-    for (int i = tid; i < CNT_SLOTS / 4; i += CNT_NT)
+    for (int i = tid; i < SLOTS / 4; i += NT)
         reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
     __syncthreads();
     int par = 0;
-    uint32_t kk[CNT_PER], n;
+    uint32_t kk[PER], n;
     uint64_t b = blockIdx.x;
-    cnt_load(keys, skeys, w, b, nw, cap, kk, n);  // software pipeline: keys of bin b
+    cnt_load<NT>(keys, skeys, w, b, nw, cap, kk, n);  // software pipeline: keys of bin b
     for (; b < nw; b += gridDim.x) {
-        uint32_t cur[CNT_PER];
+        uint32_t cur[PER];
 #pragma unroll
-        for (int j = 0; j < CNT_PER; ++j) cur[j] = kk[j];
+        for (int j = 0; j < PER; ++j) cur[j] = kk[j];
         const uint32_t ncur = n;
         const uint32_t fl = w.flags[b];
-        cnt_load(keys, skeys, w, b + gridDim.x, nw, cap, kk, n);  // next bin's keys in flight
-        uint32_t slot[CNT_PER];
+        cnt_load<NT>(keys, skeys, w, b + gridDim.x, nw, cap, kk, n);  // next bin's keys in flight
+        uint32_t slot[PER];
         uint32_t fresh = 0;
 #pragma unroll
-        for (int j = 0; j < CNT_PER; ++j) {
-            slot[j] = CNT_SLOTS;  // none
-            if (tid + j * CNT_NT < ncur) {
+        for (int j = 0; j < PER; ++j) {
+            slot[j] = SLOTS;  // none
+            if (tid + j * NT < ncur) {
                 const uint32_t key = cur[j];
-                uint32_t h = (key * 0x9E3779B1u) >> (32 - CNT_SLOTS_LOG);
+                // multiply-shift onto [0, SLOTS) (any table size)
+                uint32_t h = static_cast<uint32_t>(
+                    (static_cast<uint64_t>(key * 0x9E3779B1u) * SLOTS) >> 32);
                 while (true) {
                     const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
                     if (old == CNT_EMPTY) {
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict_
                         break;
                     }
                     if (old == key) break;
-                    h = (h + 1) & (CNT_SLOTS - 1);
+                    h = h + 1 == SLOTS ? 0u : h + 1;
                 }
             }
         }
@@ -628,11 +631,11 @@ __global__ void __launch_bounds__(CNT_NT) k_bincount(const uint32_t* __restrict_
         // reset only the slots this thread claimed: the table is clean for the
         // next bin without a full clear
 #pragma unroll
-        for (int j = 0; j < CNT_PER; ++j)
-            if (slot[j] < CNT_SLOTS) table[slot[j]] = CNT_EMPTY;
+        for (int j = 0; j < PER; ++j)
+            if (slot[j] < SLOTS) table[slot[j]] = CNT_EMPTY;
         if (tid == 0) {
             uint32_t t = 0;
-            for (int i = 0; i < CNT_NT / 32; ++i) t += s_red[par][i];
+            for (int i = 0; i < NT / 32; ++i) t += s_red[par][i];
             // merged items are already distinct; a valid list has no other
             // bin above the capacity
             wb_nnz[b] = (fl & 2u) ? w.n[b] : t;
