@@ -692,11 +692,12 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             unsigned long long hp[16];
             CUDA_TRY(cudaMemcpyAsync(hp, prof, sizeof hp, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
-            const char* names[7] = {"wait_data", "hist_scan", "scatter", "rank", "dupcheck_merge",
-                                    "write", "end_sync"};
+            const char* names[12] = {"wait_data", "hist_scan", "scatter", "rank", "dupcheck_merge",
+                                     "write", "end_sync", "pm_sum", "pm_clear", "pm_insert",
+                                     "pm_scan", "pm_scatter"};
             fprintf(stderr, "[sortprof] us per CTA:");
             double tot = 0;
-            for (int i = 0; i < 7; ++i) {
+            for (int i = 0; i < 12; ++i) {
                 const double us = hp[i] / double(sm_blocks) / 1965.0;
                 tot += us;
                 fprintf(stderr, " %s=%.1f", names[i], us);

@@ -382,49 +382,96 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
 }
 
 // Duplicate-heavy bin (its distinct count from k_bincount is <= n/2, e.g.
-// the 27-point stencil squared, cf ~ 6): sum duplicates first in a
-// shared-memory hash table (buffer `scr`, load <= 1/2), then compact the
-// distinct (key, sum) pairs back into `in`. Returns the distinct count.
-__device__ uint32_t hash_premerge(SortSmem& sm, int in, int scr, uint32_t n) {
+// the 27-point stencil squared, cf ~ 6): group duplicates first through a
+// shared-memory hash set (keys in buffer `scr`, load <= 1/2), then compact
+// the distinct (key, sum) pairs back into `in`. Returns the distinct count.
+// No floating-point atomics (an f64 atomicAdd on shared memory is a CAS spin
+// loop): a tuple takes a rank in its slot with a u16 counter add, a scan
+// turns the slot counts into group starts, values are scattered into their
+// groups and each group is summed by the thread owning its slot.
+__device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
+                                  long long& prof_t) {
     const int tid = threadIdx.x;
+    constexpr uint32_t EMPTY = 0xffffffffu;
     uint32_t* HK = sm.k[scr];
-    double* HV = sm.v[scr];
-    for (uint32_t i = tid; i < SM_CAP; i += SM_NT) {
-        HK[i] = 0xffffffffu;
-        HV[i] = 0.0;
-    }
+    uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);  // per-slot u16 counts -> starts
+    for (uint32_t i = tid; i < SM_CAP; i += SM_NT) HK[i] = EMPTY;
+    zero_cnt(sm);
     __syncthreads();
-    for (uint32_t i = tid; i < n; i += SM_NT) {
-        const uint32_t key = sm.k[in][i];
-        const double v = sm.v[in][i];
-        uint32_t h = (key * 0x9E3779B1u) >> (32 - __builtin_ctz(SM_CAP));
-        while (true) {
-            const uint32_t old = atomicCAS(&HK[h], 0xffffffffu, key);
-            if (old == 0xffffffffu || old == key) {
-                atomicAdd(&HV[h], v);
-                break;
-            }
-            h = (h + 1) & (SM_CAP - 1);
-        }
-    }
-    __syncthreads();
-    // compact occupied slots (ITEMS consecutive slots per thread)
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int j = 0; j < SM_ITEMS; ++j) cnt += HK[tid * SM_ITEMS + j] != 0xffffffffu;
-    uint32_t tot;
-    uint32_t o = block_exclusive_scan<SM_NT>(cnt, sm.s_warp32, tot);
+    PROF_MARK(8);
+    uint32_t hr[SM_ITEMS];  // slot << 16 | rank of the tuple within its slot
 #pragma unroll
     for (int j = 0; j < SM_ITEMS; ++j) {
-        const uint32_t slot = tid * SM_ITEMS + j;
-        if (HK[slot] != 0xffffffffu) {
-            sm.k[in][o] = HK[slot];
-            sm.v[in][o] = HV[slot];
-            ++o;
+        const uint32_t i = tid + j * SM_NT;
+        hr[j] = EMPTY;
+        if (i < n) {
+            const uint32_t key = sm.k[in][i];
+            uint32_t h = (key * 0x9E3779B1u) >> (32 - __builtin_ctz(SM_CAP));
+            while (true) {
+                const uint32_t old = atomicCAS(&HK[h], EMPTY, key);
+                if (old == EMPTY || old == key) break;
+                h = (h + 1) & (SM_CAP - 1);
+            }
+            const uint32_t sh16 = (h & 1u) * 16;
+            const uint32_t old = atomicAdd(&cntw[h >> 1], 1u << sh16);
+            hr[j] = h << 16 | ((old >> sh16) & 0xffffu);
         }
     }
     __syncthreads();
-    return tot;
+    PROF_MARK(9);
+    // this thread's slots [tid*8, tid*8+8): one uint4 of u16 counts
+    static_assert(SM_NB == SM_CAP, "one u16 counter per hash slot");
+    const uint4 raw = reinterpret_cast<const uint4*>(sm.cnt)[tid];
+    const uint32_t cw[4] = {raw.x, raw.y, raw.z, raw.w};
+    uint32_t occ = 0, tsum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t c = (cw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+        occ += c != 0;
+        tsum += c;
+    }
+    uint32_t tot;
+    // (distinct, tuples) prefixes in one scan: both <= SM_CAP < 2^16. The
+    // scan's barriers also end every read of the counters.
+    const uint32_t ex = block_exclusive_scan<SM_NT>(occ << 16 | tsum, sm.s_warp32, tot);
+    // per occupied slot: its group start replaces its key in HK (own slots
+    // only), the key moves to in[d] and (start, count) to grp[d]
+    // (d < n/2 <= SM_CAP/2: fits the counter array as u32)
+    uint32_t* grp = reinterpret_cast<uint32_t*>(sm.cnt);
+    {
+        uint32_t d = ex >> 16, p = ex & 0xffffu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t c = (cw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            if (c) {
+                const uint32_t slot = tid * 8 + j;
+                sm.k[in][d] = HK[slot];
+                HK[slot] = p;
+                grp[d] = p << 16 | c;
+                ++d;
+            }
+            p += c;
+        }
+    }
+    __syncthreads();
+    PROF_MARK(10);
+#pragma unroll
+    for (int j = 0; j < SM_ITEMS; ++j) {
+        if (hr[j] != EMPTY)
+            sm.v[scr][HK[hr[j] >> 16] + (hr[j] & 0xffffu)] = sm.v[in][tid + j * SM_NT];
+    }
+    __syncthreads();
+    PROF_MARK(11);
+    // one thread per distinct key sums its group
+    const uint32_t D = tot >> 16;
+    for (uint32_t d = tid; d < D; d += SM_NT) {
+        const uint32_t g = grp[d], p = g >> 16, c = g & 0xffffu;
+        double s = sm.v[scr][p];
+        for (uint32_t t = 1; t < c; ++t) s += sm.v[scr][p + t];
+        sm.v[in][d] = s;
+    }
+    __syncthreads();
+    return tot >> 16;
 }
 
 // Sort + merge the bin in buffer `in` using scratch buffer `scr`. Returns the
@@ -439,9 +486,10 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     if (tid == 0) bulk_wait_read();
     if (distinct * 2 <= n && n >= 64) {
         __syncthreads();  // thread 0's bulk_wait_read before anyone writes `scr`
-        n = hash_premerge(sm, in, scr, n);  // now n distinct keys, no duplicates
+        n = hash_premerge(a, sm, in, scr, n, prof_t);  // now n distinct keys, no duplicates
         zero_cnt(sm);
         __syncthreads();
+        PROF_MARK(7);
     }
     uint32_t* cntw = reinterpret_cast<uint32_t*>(sm.cnt);
     const int sh = bits > SM_NB_BITS ? bits - SM_NB_BITS : 0;
@@ -511,8 +559,17 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
                 r += (kj < key) | ((kj == key) & (j < i));
             }
         } else {  // all keys distinct
+            // clustered keys (the stencil after its premerge: ~25 per bucket)
+            // run long loops: four independent loads per trip
+            uint32_t j = lo;
 #pragma unroll 1
-            for (uint32_t j = lo; j < hi; ++j) r += sm.k[scr][j] < key;
+            for (; j + 4 <= hi; j += 4) {
+                const uint32_t k0 = sm.k[scr][j], k1 = sm.k[scr][j + 1], k2 = sm.k[scr][j + 2],
+                               k3 = sm.k[scr][j + 3];
+                r += (k0 < key) + (k1 < key) + (k2 < key) + (k3 < key);
+            }
+#pragma unroll 1
+            for (; j < hi; ++j) r += sm.k[scr][j] < key;
         }
         if (nodup) {  // final form: masked column ids, C-aligned offsets
             sm.k[in][lo + r + shK] = key & colmask;
