@@ -440,18 +440,23 @@ __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int s
     uint32_t* grp = reinterpret_cast<uint32_t*>(sm.cnt);
     {
         uint32_t d = ex >> 16, p = ex & 0xffffu;
+        uint4* hk4 = reinterpret_cast<uint4*>(HK) + tid * 2;  // own 8 slots, 2 x 16 B
+        const uint4 ka = hk4[0], kb = hk4[1];
+        const uint32_t kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+        uint32_t st[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint32_t c = (cw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+            st[j] = p;
             if (c) {
-                const uint32_t slot = tid * 8 + j;
-                sm.k[in][d] = HK[slot];
-                HK[slot] = p;
+                sm.k[in][d] = kk[j];
                 grp[d] = p << 16 | c;
                 ++d;
             }
             p += c;
         }
+        hk4[0] = make_uint4(st[0], st[1], st[2], st[3]);
+        hk4[1] = make_uint4(st[4], st[5], st[6], st[7]);
     }
     __syncthreads();
     PROF_MARK(10);
