@@ -55,7 +55,7 @@ class PbConfig:
     device: int = -1
     bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
     max_round_tuples: int = 0  # host path: tuples per bounded-memory round (0 = from free HBM)
-    expand_bands: int = 0  # row bands of the expand (0 or 1 = one pass, the default)
+    expand_bands: int = 0  # row bands of the expand (0 = auto, 1 = one pass)
 
     def to_c(self) -> _native.Config:
         c = _native.Config()

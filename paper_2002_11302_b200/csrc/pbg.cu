@@ -370,12 +370,19 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
 
         // ---- expand (pb_spgemm.cpp:180-258) ----
         // Optionally row-banded (k_band_*): expanding G row bands one after
-        // another keeps only nbins/G bins' write frontiers live in L2. Off by
-        // default: measured -10% expand time on ER 2^24 (260K bins) but +20%
-        // on the stencil and +8% on RMAT, whose B rows are then re-read G times.
+        // another keeps only nbins/G bins' write frontiers live in L2. Only
+        // chosen automatically for many-bin short-run inputs: +20 % on the
+        // stencil and +8 % on RMAT, whose B rows are then re-read G times.
         int g = static_cast<int>(cfg.reserved[1]);                    // caller / test hook
         if (const char* e = getenv("PBG_EXPAND_BANDS")) g = atoi(e);  // tuning hook
-        if (g < 1) g = 1;
+        if (g < 1) {
+            // auto: short-run inputs with > 200 K bins (C5a: 262 K) expand in
+            // ~100 K-bin bands (C5a 33.0 -> 32.1 ms with 3 bands, 6 bands
+            // slower again); C2's 65 K bins lose 12 % with 2 bands
+            g = 1;
+            if (hs[S_HEAVY] == 0 && flop <= 512 * m && nb > 200000)
+                g = static_cast<int>(std::min<uint64_t>(4, (nb + 99999) / 100000));
+        }
         if (g > BAND_MAX) g = BAND_MAX;
         if (static_cast<uint64_t>(g) > nb) g = static_cast<int>(nb);
         const uint64_t* xa_colptr = A.ptr;
