@@ -10,8 +10,18 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--bin-cap", type=int, default=0)
+ap.add_argument("--rmat", type=int, nargs=2, metavar=("SCALE", "EF"), default=None,
+                help="C = A*A for a seeded RMAT matrix instead of a config (single pass)")
+ap.add_argument("--row-band", type=float, default=1.0,
+                help="multiply only the first fraction of A's rows (one bounded round)")
 args = ap.parse_args()
-a, b = M.make_config(args.config)
+if args.rmat:
+    b = M.make_matrix("rmat", args.rmat[0], args.rmat[1], seed=1)
+    a = M.csr_to_csc(b)
+else:
+    a, b = M.make_config(args.config)
+if args.row_band < 1.0:
+    a = M.row_band(a, 0, int(a.nrows * args.row_band))
 dev = torch.device("cuda", 0)
 t = lambda x, dt: torch.from_numpy(x.view(dt)).to(dev)
 A = (t(a.colptr, np.int64), t(a.rowids, np.int32), t(a.values, np.float64))
