@@ -191,6 +191,21 @@ def test_expand_row_bands_invariant():
                            base.c.values)
 
 
+def test_expand_bands_auto_many_bins():
+    """The automatic band choice (> 200 K bins, short runs, no heavy row: C5a's
+    regime) engages and gives the one-pass product. Tiny bins (bin_cap 32)
+    on a sparse ER square reach that bin count at test size."""
+    csr = M.make_matrix("er", 23, 1, seed=7)
+    a = M.csr_to_csc(csr)
+    auto = gpu(a, csr, bin_cap=32)
+    one = gpu(a, csr, bin_cap=32, expand_bands=1)
+    assert auto.report["heavy_bins"] == 0 and auto.report["gpu_bins"] > 200000
+    assert auto.report["expand_bands"] == min(4, (auto.report["gpu_bins"] + 99999) // 100000)
+    assert one.report["expand_bands"] == 1
+    assert_csr_matches(auto.c.rowptr, auto.c.colids, auto.c.values, one.c.rowptr, one.c.colids,
+                       one.c.values)
+
+
 def test_bounded_memory_rounds_match_single_pass():
     """Forced row-band rounds (host path) give the single-pass product and
     the same reference-layout symbolic report."""
