@@ -143,8 +143,8 @@ int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t
  * GPU: C = A.B with A, B and C in CSC (column Gustavson SpGEMM, one shared-
  * memory hash table per output column, sized bit_ceil(2 f_j) like the
  * reference's). Same errors as pbg_multiply_begin (PBG_ERR_DIM,
- * PBG_ERR_FLOP_OVERFLOW); a column of more than 4096 products returns
- * PBG_ERR_UNIMPLEMENTED (use pbg_multiply_begin). Read with
+ * PBG_ERR_FLOP_OVERFLOW); columns of more than 4096 products (RMAT hubs)
+ * use a dense global-memory accumulator (k_hash_hub). Read with
  * pbg_multiply_fetch (rowptr = colptr[b.ncols+1], colids = row ids), free
  * with pbg_release. pbg_report: flop, nnz_c, t_symbolic (column flop +
  * scan), t_sort (hash + sort + compaction), t_total. */

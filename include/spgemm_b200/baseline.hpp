@@ -5,8 +5,7 @@
 // with sorted columns and duplicates summed; they differ only in summation
 // order, so heap_multiply runs the same GPU path. nthreads is ignored.
 // Errors: parameter_error (dimension mismatch, flop overflow);
-// std::runtime_error on CUDA failure, no GPU, or a column of more than 4096
-// products (use pb_multiply for such inputs).
+// std::runtime_error on CUDA failure or no GPU.
 #pragma once
 
 #include "spgemm_b200/types.hpp"

@@ -171,8 +171,8 @@ def hash_multiply(a: CscMatrix, b: CscMatrix, cfg: PbConfig | None = None) -> Ha
     """spgemm::hash_multiply (baseline.hpp:21-24, baseline.cpp:141-200) on the
     GPU: C = A·B, A, B and C in CSC — the column hash SpGEMM the paper finds
     faster than PB-SpGEMM above a compression factor of ~4 (SURVEY.md §8f
-    f3). Columns of more than 4096 products raise NotImplementedError (use
-    pb_multiply)."""
+    f3). Hub columns of more than 4096 products (RMAT) are summed in a dense
+    per-CTA accumulator in global memory instead of a shared-memory table."""
     cfg = cfg or PbConfig()
     lib = _native.pbg()
     ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))

@@ -106,7 +106,7 @@ struct pbg_context {
         in_a_val, in_b_ptr, in_b_idx, in_b_val;
     // heavy rows + work bins
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
-        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out, hflop, hbound, hcolcnt, hzero;
+        child_pos, hstat, wcnt, wpos, wb_nnz, wb_out, hflop, hbound, hcolcnt, hzero, hdense;
     DevBuf items[2][8];
     DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
@@ -129,7 +129,7 @@ struct pbg_context {
                           &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
                           &in_b_idx, &in_b_val, &heavy_excl, &hpad_excl, &bin_hidx, &hbin, &hoff,
                           &hhead, &hcount, &skeys, &svals, &child_cnt, &child_pos, &hstat, &wcnt,
-                          &wpos, &wb_nnz, &wb_out, &hflop, &hbound, &hcolcnt, &hzero})
+                          &wpos, &wb_nnz, &wb_out, &hflop, &hbound, &hcolcnt, &hzero, &hdense})
             b->release();
         for (auto& set : items)
             for (auto& b : set) b.release();
@@ -1297,22 +1297,31 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
     CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     // the exact 64-bit overflow test of column_symbolic (baseline.cpp:81-83)
+    uint64_t nhub = 0;  // columns above the shared-memory tables (k_hash_hub)
     {
         std::vector<uint64_t> hf(nbc);
         if (nbc) CUDA_TRY(cudaMemcpy(hf.data(), flop, nbc * 8, cudaMemcpyDeviceToHost));
         uint64_t tot = 0;
-        for (uint64_t x : hf)
+        for (uint64_t x : hf) {
+            nhub += x > HASH_BIG_F;
             if (__builtin_add_overflow(tot, x, &tot)) {
                 for (auto& e : ev) cudaEventDestroy(e);
                 return bail(fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits"));
             }
+        }
     }
     const uint64_t total = hs[0], maxf = hs[1];
-    if (maxf > HASH_BIG_F) {
+    // hub columns: one dense accumulator (nrows f64 sums + presence bitmap)
+    // per CTA, as many CTAs as fit in ~2 GB (at least one), at most one per SM
+    const uint64_t hub_words = (uint64_t(a->nrows) + 31) / 32;
+    const uint64_t hub_bytes = uint64_t(a->nrows) * 8 + hub_words * 4 + 16;
+    const uint64_t hub_ctas =
+        nhub ? std::max<uint64_t>(1, std::min<uint64_t>({nhub, uint64_t(ctx->num_sms),
+                                                         (2ull << 30) / hub_bytes}))
+             : 0;
+    if (hub_ctas && (rc = grow(ctx->hdense, hub_ctas * hub_bytes))) {
         for (auto& e : ev) cudaEventDestroy(e);
-        return bail(fail(PBG_ERR_UNIMPLEMENTED,
-                         "a column of " + std::to_string(maxf) + " products exceeds the hash path's " +
-                             std::to_string(HASH_BIG_F) + " (use pbg_multiply_begin)"));
+        return bail(rc);
     }
     if ((rc = grow(ctx->keys, total * 4 + 16)) || (rc = grow(ctx->vals, total * 8 + 16)) ||
         (rc = grow(ctx->ccol, total * 4 + 16)) || (rc = grow(ctx->cval, total * 8 + 16))) {
@@ -1369,6 +1378,12 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
         if (maxf > HASH_SMALL_F)
             k_hash_cols<512, 8192, 4096><<<ctx->num_sms, 512, sizeof(Big), st>>>(ha, HASH_SMALL_F,
                                                                                  HASH_BIG_F);
+        if (hub_ctas) {
+            auto* dense = static_cast<double*>(ctx->hdense.p);
+            k_hash_hub<512><<<static_cast<unsigned>(hub_ctas), 512, 0, st>>>(
+                ha, HASH_BIG_F, a->nrows, dense,
+                reinterpret_cast<uint32_t*>(dense + hub_ctas * uint64_t(a->nrows)));
+        }
     }
     launch_scan(ArrayIn{count}, colptr, nbc, nullptr, nbc, stat + tiles, tk + 1, nullptr, nullptr, st);
     if (nbc)

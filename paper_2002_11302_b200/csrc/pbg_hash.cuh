@@ -16,8 +16,8 @@
 //   * a scan of the per-column counts and a copy kernel give the tight CSC.
 // One CTA per column; each CTA walks columns in order, so consecutive
 // columns' A columns (banded matrices) come from L2. Columns up to
-// HASH_BIG_F products use the large-table kernel; beyond that the path
-// reports PBG_ERR_UNIMPLEMENTED (RMAT hub columns: use pb_multiply).
+// HASH_BIG_F products use the large-table kernel; hub columns beyond that
+// (RMAT) a dense per-CTA accumulator in global memory (k_hash_hub).
 #pragma once
 
 #include <cstdint>
@@ -317,6 +317,66 @@ __global__ void __launch_bounds__(NWARP * 32) k_hash_warp(HashArgs a, uint64_t l
         }
         if (lane == 0) a.count[j] = m;
         __syncwarp();
+    }
+}
+
+// Hub columns (f_j > HASH_BIG_F: RMAT hubs, more products than a shared-memory
+// table holds). Each CTA owns a dense accumulator in global memory — nrows f64
+// sums and a presence bitmap (exact-zero sums kept, as the reference's table
+// keeps them) — and walks the hub columns j = blockIdx.x, +gridDim.x, ...
+// One warp per B(i, j) entry, lanes over A(:, i): the products are added with
+// native f64 L2 atomics and their rows marked with atomicOr. Walking the
+// bitmap in word order (block scan of the popcounts) yields the column's rows
+// already sorted, so no sort follows; the walk resets the touched sums and
+// words for the next column. The sums start at -0.0, the exact additive
+// identity, so a single product keeps its sign as in the reference's
+// first-insert. The order of the f64 additions is not the reference's (its
+// table visits products in B-entry order), so values agree within rounding.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_hash_hub(HashArgs a, uint64_t lo_f, uint32_t nrows,
+                                                 double* __restrict__ dense,
+                                                 uint32_t* __restrict__ bits) {
+    __shared__ uint32_t s_warp[NT / 32 + 1];
+    const uint32_t nw = (nrows + 31) / 32;
+    double* dv = dense + uint64_t(blockIdx.x) * nrows;
+    uint32_t* bm = bits + uint64_t(blockIdx.x) * nw;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (uint32_t r = threadIdx.x; r < nrows; r += NT) dv[r] = -0.0;
+    for (uint32_t w = threadIdx.x; w < nw; w += NT) bm[w] = 0u;
+    __syncthreads();
+    for (uint64_t j = blockIdx.x; j < a.ncols; j += gridDim.x) {
+        if (a.flop[j] <= lo_f) continue;  // uniform over the CTA
+        const uint64_t b1 = a.b_colptr[j + 1];
+        for (uint64_t p = a.b_colptr[j] + wp; p < b1; p += NT / 32) {
+            const uint32_t i = a.b_rowids[p];
+            const double bv = a.b_vals[p];
+            const uint64_t q1 = a.a_colptr[i + 1];
+            for (uint64_t q = a.a_colptr[i] + lane; q < q1; q += 32) {
+                const uint32_t r = a.a_rowids[q];
+                atomicAdd(&dv[r], a.a_vals[q] * bv);
+                atomicOr(&bm[r >> 5], 1u << (r & 31));
+            }
+        }
+        __syncthreads();
+        const uint64_t base = a.bound[j];
+        uint32_t done = 0;
+        for (uint32_t w0 = 0; w0 < nw; w0 += NT) {
+            const uint32_t w = w0 + threadIdx.x;
+            const uint32_t word = w < nw ? __ldcg(bm + w) : 0u;
+            uint32_t tot;
+            uint32_t k = done + block_exclusive_scan<NT>(uint32_t(__popc(word)), s_warp, tot);
+            for (uint32_t x = word; x; x &= x - 1) {
+                const uint32_t r = w * 32 + (__ffs(x) - 1);
+                a.s_rows[base + k] = r;
+                a.s_vals[base + k] = __ldcg(dv + r);
+                dv[r] = -0.0;
+                ++k;
+            }
+            if (word) bm[w] = 0u;
+            done += tot;
+        }
+        if (threadIdx.x == 0) a.count[j] = done;
+        __syncthreads();
     }
 }
 

@@ -552,10 +552,7 @@ def test_hash_multiply_random_vs_reference(seed):
                           int(min(rng.integers(2, 12), 1 << scale)), seed=seed * 7 + k)
             for k in range(2)]
     a, b = M.csr_to_csc(mats[0]), M.csr_to_csc(mats[1])
-    try:
-        _hash_vs_reference(a, b)
-    except NotImplementedError:  # an RMAT hub column above the hash capacity
-        assert max(np.diff(b.colptr)) > 0
+    _hash_vs_reference(a, b)  # RMAT hub columns included (k_hash_hub)
 
 
 def test_hash_multiply_stencil_and_edges():
@@ -576,10 +573,22 @@ def test_hash_multiply_stencil_and_edges():
         api.hash_multiply(M.coo_to_csc(2, 3, [0], [0]), x, api.PbConfig(device=0))
 
 
-def test_hash_multiply_refuses_hub_columns():
-    # one B column of 8000 products: above the shared-memory table
+def test_hash_multiply_hub_columns():
+    # one B column of 8000 products: above the shared-memory tables, summed in
+    # the dense global-memory accumulator (k_hash_hub)
     k = 8000
     a = M.coo_to_csc(k, 1, np.arange(k), np.zeros(k, int), np.ones(k))
     b = M.coo_to_csc(1, 1, [0], [0], [2.0])
-    with pytest.raises(NotImplementedError):
-        api.hash_multiply(a, b, api.PbConfig(device=0))
+    c = _hash_vs_reference(a, b).c
+    assert list(c.colptr) == [0, k] and np.all(c.values == 2.0)
+    # hub column with an exact-zero cancellation kept in C: C(:,0) =
+    # A(:,0) - A(:,1), and A(:,1) is a single 1 at row 5
+    a2 = M.coo_to_csc(k, 2, np.r_[np.arange(k), [5]], np.r_[np.zeros(k, int), [1]], np.ones(k + 1))
+    b2 = M.coo_to_csc(2, 1, [0, 1], [0, 0], [1.0, -1.0])
+    c2 = _hash_vs_reference(a2, b2).c
+    assert c2.nnz == k and c2.values[5] == 0.0 and np.all(np.delete(c2.values, 5) == 1.0)
+    # RMAT scale 12 (hub columns of tens of thousands of products) against
+    # the reference's own hash_multiply
+    r = M.csr_to_csc(M.make_matrix("rmat", 12, 16, seed=3))
+    assert np.diff(r.colptr).max() > 64
+    _hash_vs_reference(r, r)
