@@ -36,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
-from paper_2002_11302_b200 import matrices as M  # noqa: E402
+M = None  # paper_2002_11302_b200.matrices, imported by the GPU arm only
 
 FALLBACK_HBM_GBS = 6650.0
 
@@ -162,7 +162,7 @@ def data_desc() -> str:
 def workload_name(cfg_name: str) -> str:
     if MATRIX_PATH:
         return f"matrix {Path(MATRIX_PATH).name}: C = A*A (mm_read, duplicates summed)"
-    return f"{cfg_name}: {M.CONFIG_NAMES[cfg_name]}"
+    return f"{cfg_name}: {CONFIG_NAMES[cfg_name]}"
 
 
 def build_inputs(cfg_name: str, seed: int = 1):
@@ -190,77 +190,124 @@ def build_inputs(cfg_name: str, seed: int = 1):
     return a_csc, a_csr
 
 
-def cpu_reference_run(a_csc, b_csr, steps: int, warmup: int, budget_s: float, nthreads: int):
-    """Times the reference's own pb_multiply (oracle/_ref, OpenMP, all host
-    threads) on a flop-balanced leading row band of A sized to the budget."""
+# The configs: generator kind, scale, edge factor. Kept here so
+# the reference arm needs nothing from the product package.
+CONFIGS = {
+    "C1": ("er", 16, 4), "C2": ("er", 20, 16), "C3": ("rmat", 20, 16),
+    "C4": ("stencil", 128, None), "C5a": ("er", 24, 8), "C5b": ("rmat", 24, 8),
+    "R16": ("rmat", 16, 16), "R18": ("rmat", 18, 16), "S64": ("stencil", 64, None),
+    "E22": ("er", 22, 8),
+}
+CONFIG_NAMES = {
+    "C1": "ER n=2^16 d=4, C=A*A, fp64 U[0,1)",
+    "C2": "ER n=2^20 d=16, C=A*A, fp64 U[0,1)",
+    "C3": "RMAT scale 20 ef 16 (a,b,c,d=.57,.19,.19,.05, dedup, no self-loops), C=A*A, fp64 U[0,1)",
+    "C4": "27-point stencil 128^3 (26 / -1), C=A*A",
+    "C5a": "ER n=2^24 d=8, C=A*A, fp64 U[0,1)",
+    "C5b": "RMAT scale 24 ef 8 (dedup, no self-loops), C=A*A, fp64 U[0,1)",
+    "R16": "dev: RMAT scale 16 ef 16, C=A*A",
+    "R18": "dev: RMAT scale 18 ef 16, C=A*A",
+    "S64": "dev: 27-point stencil 64^3, C=A*A",
+    "E22": "dev: ER n=2^22 d=8, C=A*A",
+}
+VALUE_SEED_XOR = 0x5EED5EED5EED5EED
+L2_NOTE = "inputs+tuples larger than L2 (tuples alone are 12 B x flop)"
+
+
+def reference_config(cfg_name: str, seed: int = 1):
+    """The config built by the reference library alone (oracle/_ref:
+    gen_er / gen_rmat / coo_to_csc / coo_to_csr + the SplitMix64 values),
+    pinned equal to the product's inputs by tests/test_oracle.py."""
     import oracle
-    impl = "reference" if oracle.ref_available() else "port"
-    kind = "reference" if impl == "reference" else "port"
-    if impl == "port":
-        nthreads = 1
-    rf = M.row_flop(a_csc, b_csr)
-    total = int(rf.sum())
-    # probe: 1/32 of the flop
-    cuts = M.band_cuts(rf, 32)
-    probe = M.row_band(a_csc, 0, int(cuts[1]))
-    t = time.perf_counter()
-    oracle.multiply(probe, b_csr, impl=impl, nthreads=nthreads)
-    rate = max(1.0, float(rf[:int(cuts[1])].sum())) / max(time.perf_counter() - t, 1e-6)
-    per_step = budget_s / max(1, steps + warmup)
-    frac = min(1.0, rate * per_step / max(total, 1))
-    g = max(1, int(round(1.0 / frac))) if frac < 1.0 else 1
-    r1 = int(M.band_cuts(rf, g)[1]) if g > 1 else a_csc.nrows
-    band = a_csc if r1 == a_csc.nrows else M.row_band(a_csc, 0, r1)
-    band_flop = int(rf[:r1].sum())
+    if MATRIX_PATH:
+        return oracle.RefConfig("mtx", path=MATRIX_PATH)
+    kind, scale, ef = CONFIGS[cfg_name]
+    return oracle.RefConfig(kind, scale, ef or 0, seed, seed ^ VALUE_SEED_XOR)
+
+
+def time_reference(rc, steps: int, warmup: int, budget_s: float, nthreads: int):
+    """The reference's own pb_multiply (oracle/_ref: unmodified sources,
+    OpenMP with nthreads) on the whole config, timed by its own PhaseReport
+    t_total (bench.cpp:84-93,130-138 take the median of t_total). Only when
+    (steps + warmup) full multiplies would exceed budget_s does each step
+    run a flop-balanced leading row band instead (said in `sample`)."""
+    # estimate the full step from a 1/16-flop band (fixed costs make this an
+    # over-estimate, so a config that fits is never cut)
+    frac = 1.0
+    if rc.flop > 0:
+        rc.band(1.0 / 16)
+        t, _, _ = rc.multiply(nthreads)
+        est = t[5] * 16
+        if est * (steps + warmup) > budget_s:
+            frac = max(1e-4, budget_s / (steps + warmup) / est)
+    r1, band_flop = rc.band(frac)
     for _ in range(warmup):
-        oracle.multiply(band, b_csr, impl=impl, nthreads=nthreads)
-    times = []
+        rc.multiply(nthreads)
+    times, phases, nnz_c, flop = [], [], 0, 0
     for _ in range(steps):
-        t = time.perf_counter()
-        oracle.multiply(band, b_csr, impl=impl, nthreads=nthreads, stepwise=False)
-        times.append(time.perf_counter() - t)
+        t, flop, nnz_c = rc.multiply(nthreads)
+        times.append(float(t[5]))
+        phases.append(t)
     med = statistics.median(times)
-    sample = (f"rows [0,{r1}) of {a_csc.nrows} ({band_flop} of {total} mults, "
-              f"{100.0 * band_flop / max(total, 1):.1f}%), median of {steps} after {warmup} warm-up")
-    return {"value": band_flop / med, "unit": "mult/s", "cores": nthreads, "kind": kind,
-            "sample": sample, "seconds_per_step": med, "times": times}
+    full = r1 == rc.nrows
+    sample = ((f"whole config (100%: {flop} of {rc.flop} mults)" if full else
+               f"rows [0,{r1}) of {rc.nrows} ({band_flop} of {rc.flop} mults, "
+               f"{100.0 * band_flop / max(rc.flop, 1):.1f}%: the whole config would exceed the "
+               f"{budget_s:.0f} s budget)") +
+              f", median PbResult.phases.t_total of {steps} after {warmup} warm-up")
+    mid = phases[times.index(med)] if med in times else phases[len(phases) // 2]
+    return {"value": flop / med if med > 0 else None, "unit": "mult/s", "cores": nthreads,
+            "kind": "reference", "sample": sample, "seconds_per_step": med, "times": times,
+            "full": full, "flop": flop, "nnz_c": nnz_c,
+            "phases_s": dict(zip(("symbolic", "expand", "sort", "compress", "convert", "total"),
+                                 (float(x) for x in mid)))}
 
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    # host-built inputs: nothing of this repository's GPU path touches this arm
-    t = time.time()
-    if MATRIX_PATH:
-        a_csr = M.matrix_from_mtx(MATRIX_PATH)
-        a_csc = M.csr_to_csc(a_csr)
-    else:
-        a_csc, a_csr = M.make_config(args.config)
-    log(f"[bench] {args.config}: n={a_csr.nrows} nnz={a_csr.nnz} host inputs in {time.time() - t:.1f}s")
-    nthreads = os.cpu_count() or 1
     os.environ.setdefault("OMP_PLACES", "cores")
     os.environ.setdefault("OMP_PROC_BIND", "close")
-    res = cpu_reference_run(a_csc, a_csr, args.steps, args.warmup, args.ref_budget, nthreads)
+    nthreads = os.cpu_count() or 1
+    t = time.time()
+    rc = reference_config(args.config)
+    log(f"[bench] {args.config}: n={rc.nrows} nnz={rc.nnz_a} flop={rc.flop} reference inputs "
+        f"in {time.time() - t:.1f}s")
+    res = time_reference(rc, args.steps, args.warmup, args.ref_budget, nthreads)
+    peak, _ = peak_hbm()
+    _, _, b_tot = model_bytes(rc.nnz_a, rc.nnz_b, res["flop"], res["nnz_c"])
+    t_step = res["seconds_per_step"]
     line = {
         "metric": "SpGEMM mults/sec", "value": res["value"], "unit": "mult/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": res["seconds_per_step"] * 1e3, "higher_is_better": True,
-        "scaling": args.scaling if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": data_desc(),
-        "config": {"workload": workload_name(args.config)},
+        "config": {"workload": workload_name(args.config), "n": rc.nrows, "nnz_a": rc.nnz_a,
+                   "flop": res["flop"], "nnz_c": res["nnz_c"], "model_bytes": b_tot,
+                   "model_GBps": b_tot / t_step / 1e9 if t_step else None,
+                   "model_frac_of_peak_per_gpu": None, "l2": L2_NOTE,
+                   "partition": "host CPU, OpenMP (rank 0 only)"},
         "impl": "reference",
+        "same_config": res["full"],
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "mult/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "phases_s": res["phases_s"],
     }
     print(json.dumps(line), flush=True)
+    rc.close()
     return 0
 
 
 def run_gpu_arm(args):
+    global M
     import torch
     import torch.distributed as dist
+
+    from paper_2002_11302_b200 import matrices
+    M = matrices
 
     from paper_2002_11302_b200 import api
 
@@ -471,7 +518,9 @@ def run_gpu_arm(args):
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            res = cpu_reference_run(a_csc, a_csr, 3, 1, args.cpu_budget, os.cpu_count() or 1)
+            rcfg = reference_config(args.config)
+            res = time_reference(rcfg, 3, 1, args.cpu_budget, os.cpu_count() or 1)
+            rcfg.close()
             cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, not required
             cpu = {"value": None, "unit": "mult/s", "cores": 0, "kind": "reference",
@@ -512,13 +561,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(M.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--matrix", default=None,
                     help="Matrix Market file: square it (C = A*A) instead of a synthetic config")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ref-budget", type=float, default=120.0)
+    ap.add_argument("--cpu-budget", type=float, default=30.0)
+    ap.add_argument("--ref-budget", type=float, default=240.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: per-GPU work fixed (weak, default) or total work fixed (strong)")

@@ -3,8 +3,8 @@
 //
 // Mirrors proj/include/spgemm/pb_spgemm.hpp: PbConfig (:11-17), the key
 // helpers (:20-41), choose_nbins (:45-46), SymbolicResult (:48-55), PbResult
-// and pb_multiply (:110-116); PhaseReport mirrors proj/include/spgemm/
-// report.hpp:26-52. The reference's stepwise API (symbolic/make_bins/expand/
+// and pb_multiply (:110-116); PhaseReport / WallTimer come from
+// spgemm_b200/report.hpp (proj/include/spgemm/report.hpp:9-52). The reference's stepwise API (symbolic/make_bins/expand/
 // sort_bins/compress_bins/convert_csr) exposes host BinSet internals and is
 // not offered; the GPU returns its conservation counters in PbResult instead.
 #pragma once
@@ -12,6 +12,7 @@
 #include <bit>
 #include <cstdint>
 
+#include "spgemm_b200/report.hpp"
 #include "spgemm_b200/types.hpp"
 
 namespace spgemm {
@@ -57,35 +58,6 @@ struct SymbolicResult {
     std::vector<std::uint64_t> per_bin_flop;
     std::vector<index_t> bin_row_starts;
     index_t uniform_rows_per_bin = 0;
-};
-
-struct PhaseReport {
-    double t_symbolic = 0.0;
-    double t_expand = 0.0;
-    double t_sort = 0.0;  // fused sort + merge + CSR assembly on the GPU
-    double t_compress = 0.0;
-    double t_convert = 0.0;
-    double t_total = 0.0;
-    double bytes_expand = 0.0;
-    double bytes_sort = 0.0;
-    double bytes_compress = 0.0;
-    double bw_expand = 0.0;
-    double bw_sort = 0.0;
-    double bw_compress = 0.0;
-    double mflops = 0.0;
-
-    // report.hpp:42-51 with the traffic model of roofline.hpp:56-63.
-    void derive(std::uint64_t nnz_a, std::uint64_t nnz_b, std::uint64_t nnz_c,
-                std::uint64_t flop, double b_bytes = 16.0) {
-        bytes_expand = b_bytes * static_cast<double>(nnz_a + nnz_b) +
-                       b_bytes * static_cast<double>(flop);
-        bytes_sort = b_bytes * static_cast<double>(flop);
-        bytes_compress = b_bytes * static_cast<double>(nnz_c);
-        if (t_expand > 0.0) bw_expand = bytes_expand / t_expand;
-        if (t_sort > 0.0) bw_sort = bytes_sort / t_sort;
-        if (t_compress > 0.0) bw_compress = bytes_compress / t_compress;
-        if (t_total > 0.0) mflops = static_cast<double>(flop) / t_total / 1e6;
-    }
 };
 
 struct PbResult {

@@ -282,6 +282,74 @@ def ref_convert(to_csr: bool, nrows: int, ncols: int, rows, cols, vals):
     return ptr, idx[:k].copy(), val[:k].copy()
 
 
+class RefConfig:
+    """A benchmark config built and multiplied by the reference library alone
+    (ref_shim.cpp ref_config_*): bench.py --impl reference uses only this, so
+    nothing of the product (libpbg*.so) is loaded in that arm."""
+
+    KINDS = {"er": 0, "rmat": 1, "stencil": 2}
+
+    def __init__(self, kind: str, scale: int = 0, ef: int = 0, seed: int = 1, vseed: int = 0,
+                 path: str | None = None):
+        lib = ref_lib()
+        lib.ref_config_make.argtypes = [C.c_int, C.c_int, u32, u64, u64, C.POINTER(vp)]
+        lib.ref_config_from_mtx.argtypes = [C.c_char_p, C.POINTER(vp)]
+        lib.ref_config_stats.argtypes = [vp, vp]
+        lib.ref_config_get.argtypes = [vp] * 7
+        lib.ref_config_band.argtypes = [vp, f64, C.POINTER(u32), C.POINTER(u64)]
+        lib.ref_config_multiply.argtypes = [vp, C.c_int, vp, vp]
+        lib.ref_config_free.argtypes = [vp]
+        self._lib = lib
+        self._h = vp()
+        if kind == "mtx":
+            rc = lib.ref_config_from_mtx(str(path).encode(), C.byref(self._h))
+        else:
+            rc = lib.ref_config_make(self.KINDS[kind], scale, ef or 0, seed, vseed,
+                                     C.byref(self._h))
+        if rc:
+            raise OracleError(rc, lib.ref_last_error().decode())
+        st = np.zeros(4, np.uint64)
+        lib.ref_config_stats(self._h, _ptr(st))
+        self.nrows, self.nnz_a, self.flop, self.nnz_b = (int(x) for x in st)
+
+    def arrays(self):
+        """(colptr, rowids, values) of the CSC and (rowptr, colids, values) of the CSR."""
+        n, k = self.nrows, self.nnz_a
+        a = (np.empty(n + 1, np.uint64), np.empty(max(k, 1), np.uint32), np.empty(max(k, 1)))
+        b = (np.empty(n + 1, np.uint64), np.empty(max(k, 1), np.uint32), np.empty(max(k, 1)))
+        self._lib.ref_config_get(self._h, *(_ptr(x) for x in a + b))
+        return (a[0], a[1][:k], a[2][:k]), (b[0], b[1][:k], b[2][:k])
+
+    def band(self, frac: float):
+        """Left operand = the leading rows holding ~frac of the flop; returns
+        (r1, band_flop). frac >= 1 restores the whole matrix."""
+        r1, bf = u32(0), u64(0)
+        rc = self._lib.ref_config_band(self._h, frac, C.byref(r1), C.byref(bf))
+        if rc:
+            raise OracleError(rc, self._lib.ref_last_error().decode())
+        return r1.value, bf.value
+
+    def multiply(self, nthreads: int):
+        """One reference pb_multiply; returns (phase times[6], flop, nnz_c)."""
+        t = np.zeros(6)
+        o = np.zeros(2, np.uint64)
+        rc = self._lib.ref_config_multiply(self._h, nthreads, _ptr(t), _ptr(o))
+        if rc:
+            raise OracleError(rc, self._lib.ref_last_error().decode())
+        return t, int(o[0]), int(o[1])
+
+    def close(self):
+        if self._h:
+            self._lib.ref_config_free(self._h)
+            self._h = vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def value(vseed: int, r: int, c: int) -> float:
     return port_lib().orc_value(vseed, r, c)
 

@@ -291,4 +291,177 @@ int ref_dense_multiply(uint32_t m, uint32_t k, uint32_t n, uint64_t annz, const 
     });
 }
 
+// ---- bench.py --impl reference: the benchmark configs built and multiplied
+// with the reference library alone (nothing of the product is loaded). ----
+//
+// kind 0: gen_er (generate.cpp:20-54); kind 1: gen_rmat (generate.cpp:56-90,
+// duplicates collapsed) minus self-loops; kind 2: the 27-point stencil on a
+// scale^3 grid (26 on the diagonal, -1 off it; not a reference generator).
+// Values U[0,1) = SplitMix64(split_seed(vseed, row << 32 | col)).next_unit()
+// (generate.hpp:12-40) for kinds 0/1. A is kept as CSC (left operand) and
+// CSR (right operand) converted by the reference's coo_to_csc / coo_to_csr
+// (convert.cpp:82-98) — the reference bench's --matrix squaring path
+// (spgemm_bench.cpp:55-58).
+struct RefConfig {
+    CscMatrix a;        // full left operand
+    CsrMatrix b;        // right operand
+    CscMatrix band;     // rows [0, r1) of a (same dims), when a band is chosen
+    bool use_band = false;
+    std::vector<std::uint64_t> row_flop;
+    std::uint64_t flop = 0;
+};
+
+int ref_config_make(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t vseed, void** out) {
+    return guarded([&] {
+        CooMatrix coo;
+        if (kind == 0 || kind == 1) {
+            coo = kind == 0 ? gen_er(GenSpec::er(scale, ef, seed))
+                            : gen_rmat(GenSpec::rmat(scale, ef, seed));
+            if (kind == 1) {
+                std::size_t w = 0;
+                for (std::size_t i = 0; i < coo.entries.size(); ++i)
+                    if (coo.entries[i].row != coo.entries[i].col) coo.entries[w++] = coo.entries[i];
+                coo.entries.resize(w);
+            }
+            for (auto& e : coo.entries)
+                e.val = SplitMix64(split_seed(vseed, (std::uint64_t(e.row) << 32) | e.col)).next_unit();
+        } else if (kind == 2) {
+            const std::int64_t g = scale;
+            const std::int64_t n = g * g * g;
+            coo.dims = {static_cast<index_t>(n), static_cast<index_t>(n)};
+            coo.entries.reserve(static_cast<std::size_t>(n) * 27);
+            for (std::int64_t r = 0; r < n; ++r) {
+                const std::int64_t x = r % g, y = (r / g) % g, z = r / (g * g);
+                for (int dz = -1; dz <= 1; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const std::int64_t X = x + dx, Y = y + dy, Z = z + dz;
+                            if (X < 0 || Y < 0 || Z < 0 || X >= g || Y >= g || Z >= g) continue;
+                            const bool diag = dx == 0 && dy == 0 && dz == 0;
+                            coo.entries.push_back({static_cast<index_t>(r),
+                                                   static_cast<index_t>((Z * g + Y) * g + X),
+                                                   diag ? 26.0 : -1.0});
+                        }
+            }
+        } else {
+            throw parameter_error("ref_config_make: unknown kind");
+        }
+        auto* c = new RefConfig;
+        c->a = coo_to_csc(coo);
+        c->b = coo_to_csr(coo);
+        // per-row flop of A*B (the quantity balanced_starts accumulates,
+        // pb_spgemm.cpp:58-82) for band sampling
+        c->row_flop.assign(c->a.dims.nrows, 0);
+        for (index_t k = 0; k < c->a.dims.ncols; ++k) {
+            const std::uint64_t bk = c->b.rowptr[k + 1] - c->b.rowptr[k];
+            for (offset_t p = c->a.colptr[k]; p < c->a.colptr[k + 1]; ++p)
+                c->row_flop[c->a.rowids[p]] += bk;
+        }
+        for (auto f : c->row_flop) c->flop += f;
+        *out = c;
+    });
+}
+
+// A Matrix Market file squared: mm_read (mmio.cpp:33-105) -> coo_to_csc /
+// coo_to_csr, as the reference bench's --matrix path (spgemm_bench.cpp:55-58).
+int ref_config_from_mtx(const char* path, void** out) {
+    return guarded([&] {
+        CooMatrix coo = mm_read(std::string(path));
+        if (coo.dims.nrows != coo.dims.ncols) throw parameter_error("--matrix needs a square matrix");
+        auto* c = new RefConfig;
+        c->a = coo_to_csc(coo);
+        c->b = coo_to_csr(coo);
+        c->row_flop.assign(c->a.dims.nrows, 0);
+        for (index_t k = 0; k < c->a.dims.ncols; ++k) {
+            const std::uint64_t bk = c->b.rowptr[k + 1] - c->b.rowptr[k];
+            for (offset_t p = c->a.colptr[k]; p < c->a.colptr[k + 1]; ++p)
+                c->row_flop[c->a.rowids[p]] += bk;
+        }
+        for (auto f : c->row_flop) c->flop += f;
+        *out = c;
+    });
+}
+
+// stats[0..3] = nrows, nnz(A), flop(A*A), nnz(B)
+void ref_config_stats(void* h, uint64_t* stats) {
+    auto* c = static_cast<RefConfig*>(h);
+    stats[0] = c->a.dims.nrows;
+    stats[1] = c->a.nnz();
+    stats[2] = c->flop;
+    stats[3] = c->b.nnz();
+}
+
+// The CSC (left) and CSR (right) arrays, for the test that pins this builder
+// to the product's input builder.
+void ref_config_get(void* h, uint64_t* a_colptr, uint32_t* a_rowids, double* a_vals,
+                    uint64_t* b_rowptr, uint32_t* b_colids, double* b_vals) {
+    auto* c = static_cast<RefConfig*>(h);
+    std::memcpy(a_colptr, c->a.colptr.data(), c->a.colptr.size() * 8);
+    std::memcpy(a_rowids, c->a.rowids.data(), c->a.rowids.size() * 4);
+    std::memcpy(a_vals, c->a.values.data(), c->a.values.size() * 8);
+    std::memcpy(b_rowptr, c->b.rowptr.data(), c->b.rowptr.size() * 8);
+    std::memcpy(b_colids, c->b.colids.data(), c->b.colids.size() * 4);
+    std::memcpy(b_vals, c->b.values.data(), c->b.values.size() * 8);
+}
+
+// Restrict the left operand to the leading rows holding about frac of the
+// flop (frac >= 1: the whole matrix). *r1 / *band_flop describe the band.
+int ref_config_band(void* h, double frac, uint32_t* r1, uint64_t* band_flop) {
+    return guarded([&] {
+        auto* c = static_cast<RefConfig*>(h);
+        const index_t m = c->a.dims.nrows;
+        if (frac >= 1.0) {
+            c->use_band = false;
+            c->band = CscMatrix{};
+            *r1 = m;
+            *band_flop = c->flop;
+            return;
+        }
+        const double target = frac * static_cast<double>(c->flop);
+        index_t r = 0;
+        std::uint64_t acc = 0;
+        while (r < m && static_cast<double>(acc) < target) acc += c->row_flop[r++];
+        CscMatrix& bd = c->band;
+        bd.dims = c->a.dims;
+        bd.colptr.assign(c->a.dims.ncols + 1, 0);
+        bd.rowids.clear();
+        bd.values.clear();
+        for (index_t k = 0; k < c->a.dims.ncols; ++k) {
+            for (offset_t p = c->a.colptr[k]; p < c->a.colptr[k + 1]; ++p)
+                if (c->a.rowids[p] < r) {
+                    bd.rowids.push_back(c->a.rowids[p]);
+                    bd.values.push_back(c->a.values[p]);
+                }
+            bd.colptr[k + 1] = bd.rowids.size();
+        }
+        c->use_band = true;
+        *r1 = r;
+        *band_flop = acc;
+    });
+}
+
+// One spgemm::pb_multiply (pb_spgemm.hpp:116) with the default PbConfig and
+// nthreads threads, on the config (or its band). times[0..5] = the
+// reference's own PhaseReport (t_symbolic, t_expand, t_sort, t_compress,
+// t_convert, t_total: its WallTimer laps, pb_spgemm.cpp:330-361 — how
+// bench.cpp:84-93,130-138 times a run). out[0..1] = flop, nnz(C).
+int ref_config_multiply(void* h, int nthreads, double* times, uint64_t* out) {
+    return guarded([&] {
+        auto* c = static_cast<RefConfig*>(h);
+        PbConfig cfg;
+        cfg.nthreads = nthreads;
+        PbResult res = pb_multiply(c->use_band ? c->band : c->a, c->b, cfg);
+        times[0] = res.phases.t_symbolic;
+        times[1] = res.phases.t_expand;
+        times[2] = res.phases.t_sort;
+        times[3] = res.phases.t_compress;
+        times[4] = res.phases.t_convert;
+        times[5] = res.phases.t_total;
+        out[0] = res.sym.flop;
+        out[1] = res.c.nnz();
+    });
+}
+
+void ref_config_free(void* h) { delete static_cast<RefConfig*>(h); }
+
 }  // extern "C"

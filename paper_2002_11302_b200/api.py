@@ -103,6 +103,18 @@ def _host_arrays(m):
     return m.rowptr, m.colids, m.values
 
 
+def _checked_arrays(a, b):
+    """Host arrays of both operands with the reference's element types (u64
+    pointers, u32 indices, f64 values); anything else is a TypeError before
+    any native view is built."""
+    ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))
+    bp, bi, bv = (np.ascontiguousarray(x) for x in _host_arrays(b))
+    if ap.dtype != np.uint64 or bp.dtype != np.uint64 or ai.dtype != np.uint32 \
+            or bi.dtype != np.uint32 or av.dtype != np.float64 or bv.dtype != np.float64:
+        raise TypeError("expected u64 pointers, u32 indices, f64 values")
+    return (ap, ai, av), (bp, bi, bv)
+
+
 def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
                 symbolic: bool = True, out=None) -> PbResult:
     """C = A·B on the GPU, A in CSC, B in CSR, C in CSR (host buffers in/out).
@@ -111,11 +123,9 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
     large enough for C; the returned CsrMatrix views them."""
     cfg = cfg or PbConfig()
     lib = _native.pbg()
-    ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))
-    bp, bi, bv = (np.ascontiguousarray(x) for x in _host_arrays(b))
-    if ap.dtype != np.uint64 or bp.dtype != np.uint64 or ai.dtype != np.uint32 \
-            or bi.dtype != np.uint32 or av.dtype != np.float64 or bv.dtype != np.float64:
-        raise TypeError("expected u64 pointers, u32 indices, f64 values")
+    if not isinstance(a, CscMatrix) or not isinstance(b, CsrMatrix):
+        raise TypeError("pb_multiply takes A in CSC and B in CSR")
+    (ap, ai, av), (bp, bi, bv) = _checked_arrays(a, b)
     va = _view(a.nrows, a.ncols, ap, ai, av)
     vb = _view(b.nrows, b.ncols, bp, bi, bv)
     c_cfg = cfg.to_c()
@@ -175,10 +185,9 @@ def hash_multiply(a: CscMatrix, b: CscMatrix, cfg: PbConfig | None = None) -> Ha
     per-CTA accumulator in global memory instead of a shared-memory table."""
     cfg = cfg or PbConfig()
     lib = _native.pbg()
-    ap, ai, av = (np.ascontiguousarray(x) for x in _host_arrays(a))
-    bp, bi, bv = (np.ascontiguousarray(x) for x in _host_arrays(b))
-    if not isinstance(b, CscMatrix):
-        raise TypeError("hash_multiply takes B in CSC")
+    if not isinstance(a, CscMatrix) or not isinstance(b, CscMatrix):
+        raise TypeError("hash_multiply takes A and B in CSC")
+    (ap, ai, av), (bp, bi, bv) = _checked_arrays(a, b)
     va = _view(a.nrows, a.ncols, ap, ai, av)
     vb = _view(b.nrows, b.ncols, bp, bi, bv)
     c_cfg = cfg.to_c()

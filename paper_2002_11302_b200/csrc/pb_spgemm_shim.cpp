@@ -125,6 +125,46 @@ CscMatrix heap_multiply(const CscMatrix& a, const CscMatrix& b, int nthreads) {
     return hash_multiply(a, b, nthreads);  // same result; the GPU path has one column kernel
 }
 
+// ---- structural validation (convert.cpp:8-80), host-side ----
+void validate(const CooMatrix& m) {
+    if (m.dims.nrows < 1 || m.dims.ncols < 1) throw structural_error("empty dims");
+    for (const CooEntry& e : m.entries) {
+        if (e.row >= m.dims.nrows || e.col >= m.dims.ncols)
+            throw structural_error("coo entry (" + std::to_string(e.row) + "," +
+                                   std::to_string(e.col) + ") out of " +
+                                   std::to_string(m.dims.nrows) + "x" +
+                                   std::to_string(m.dims.ncols));
+        if (e.val != e.val) throw structural_error("coo entry holds NaN");
+    }
+}
+
+namespace {
+void check_compressed(MatrixDims dims, const std::vector<offset_t>& ptr,
+                      const std::vector<index_t>& ids, std::size_t nvals, index_t nmajor,
+                      index_t nminor, const std::string& what) {
+    if (dims.nrows < 1 || dims.ncols < 1) throw structural_error("empty dims");
+    const bool shape_ok = ptr.size() == static_cast<std::size_t>(nmajor) + 1 && ptr.front() == 0 &&
+                          ptr.back() == ids.size() && ids.size() == nvals;
+    if (!shape_ok) throw structural_error(what + ": bad pointer array shape");
+    for (index_t j = 0; j < nmajor; ++j) {
+        if (ptr[j] > ptr[j + 1]) throw structural_error(what + ": ptr not monotone");
+        for (offset_t p = ptr[j]; p < ptr[j + 1]; ++p) {
+            if (ids[p] >= nminor) throw structural_error(what + ": id out of range");
+            if (p > ptr[j] && ids[p - 1] >= ids[p])
+                throw structural_error(what + ": ids not strictly increasing");
+        }
+    }
+}
+}  // namespace
+
+void validate(const CscMatrix& m) {
+    check_compressed(m.dims, m.colptr, m.rowids, m.values.size(), m.dims.ncols, m.dims.nrows, "csc");
+}
+
+void validate(const CsrMatrix& m) {
+    check_compressed(m.dims, m.rowptr, m.colids, m.values.size(), m.dims.nrows, m.dims.ncols, "csr");
+}
+
 CooMatrix mm_read(const std::string& path) {
     pbgh_mm* h = nullptr;
     std::uint32_t nr = 0, nc = 0;

@@ -792,6 +792,41 @@ int make_context(int device, pbg_context** out) {
     return PBG_OK;
 }
 
+// Takes a pooled context of the current device and wraps it in a handle
+// right away, runs body(h), and releases the handle (returning the context
+// to the pool) on every error path, CUDA_TRY returns included.
+template <class Body>
+int with_handle(const pbg_config& cfg, pbg_handle** out, Body&& body) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    pbg_context* ctx = pool_get(dev);
+    int rc;
+    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
+    auto* h = new pbg_handle;
+    h->ctx = ctx;
+    h->cfg = cfg;
+    rc = body(h);
+    if (rc) {
+        pbg_release(h);
+        return rc;
+    }
+    *out = h;
+    return PBG_OK;
+}
+
+// cudaEvent_t owned for one scope
+struct ScopedEvents {
+    cudaEvent_t e[4] = {};
+    ScopedEvents() {
+        for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~ScopedEvents() {
+        for (auto& x : e)
+            if (x) cudaEventDestroy(x);
+    }
+    cudaEvent_t operator[](int i) const { return e[i]; }
+};
+
 int copy_in(DevBuf& b, const void* src, size_t bytes, cudaStream_t st) {
     int rc = grow(b, bytes);
     if (rc) return rc;
@@ -1160,100 +1195,67 @@ int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const ui
     int rc;
     if ((rc = validate_cfg(cfg))) return rc;
     if ((rc = set_device(cfg.device))) return rc;
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    pbg_context* ctx = pool_get(dev);
-    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
-    cudaStream_t st = nullptr;
-    // major = row (CSR) or col (CSC)
-    const uint32_t nmajor = to_csc ? ncols : nrows, nminor = to_csc ? nrows : ncols;
-    const uint32_t* major = to_csc ? cols : rows;
-    const uint32_t* minor = to_csc ? rows : cols;
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, st);
-    rc = copy_in(ctx->in_a_idx, major, nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_b_idx, minor, nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_b_val, vals, nnz * 8, st);
-    if (!rc) rc = grow(ctx->in_a_ptr, (nnz + 1) * 8);
-    if (!rc) rc = grow(ctx->in_b_ptr, (nnz + 1) * 8);
-    if (!rc) rc = grow(ctx->in_a_val, (nnz + 1) * 8);
-    if (!rc) rc = grow(ctx->zero_block, 64);
-    cudaEventRecord(e1, st);
-    if (rc) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return rc;
-    }
-    auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
-    CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
-    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
-        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
-        static_cast<double*>(ctx->in_a_val.p), static_cast<const uint32_t*>(ctx->in_a_idx.p),
-        static_cast<const uint32_t*>(ctx->in_b_idx.p), maxes);
-    unsigned long long mx[2] = {0, 0};
-    CUDA_TRY(cudaMemcpyAsync(mx, maxes, 16, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    // validate (convert.cpp:8-37): every entry inside the matrix
-    if (nnz && (mx[0] >= nmajor || mx[1] >= nminor))
-        return fail(PBG_ERR_ARG, "COO entry out of range (structural_error)");
-    const pbg_csx_view da{nmajor, static_cast<uint32_t>(nnz), nnz,
-                          static_cast<const uint64_t*>(ctx->in_a_ptr.p),
-                          static_cast<const uint32_t*>(ctx->in_a_idx.p),
-                          static_cast<const double*>(ctx->in_a_val.p)};
-    const pbg_csx_view db{static_cast<uint32_t>(nnz), nminor, nnz,
-                          static_cast<const uint64_t*>(ctx->in_b_ptr.p),
-                          static_cast<const uint32_t*>(ctx->in_b_idx.p),
-                          static_cast<const double*>(ctx->in_b_val.p)};
-    auto* h = new pbg_handle;
-    h->ctx = ctx;
-    h->cfg = cfg;
-    h->t_h2d = ms * 1e-3;
-    if ((rc = run_pipeline(ctx, da, db, cfg, st))) {
-        pbg_release(h);
-        return rc;
-    }
-    if (nnz_out) *nnz_out = ctx->nnz_c;
-    *out = h;
-    return PBG_OK;
+    return with_handle(cfg, out, [&](pbg_handle* h) -> int {
+        pbg_context* ctx = h->ctx;
+        cudaStream_t st = nullptr;
+        // major = row (CSR) or col (CSC)
+        const uint32_t nmajor = to_csc ? ncols : nrows, nminor = to_csc ? nrows : ncols;
+        const uint32_t* major = to_csc ? cols : rows;
+        const uint32_t* minor = to_csc ? rows : cols;
+        ScopedEvents ev;
+        CUDA_TRY(cudaEventRecord(ev[0], st));
+        int r = copy_in(ctx->in_a_idx, major, nnz * 4, st);
+        if (!r) r = copy_in(ctx->in_b_idx, minor, nnz * 4, st);
+        if (!r) r = copy_in(ctx->in_b_val, vals, nnz * 8, st);
+        if (!r) r = grow(ctx->in_a_ptr, (nnz + 1) * 8);
+        if (!r) r = grow(ctx->in_b_ptr, (nnz + 1) * 8);
+        if (!r) r = grow(ctx->in_a_val, (nnz + 1) * 8);
+        if (!r) r = grow(ctx->zero_block, 64);
+        if (r) return r;
+        CUDA_TRY(cudaEventRecord(ev[1], st));
+        auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
+        CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
+        k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+            nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+            static_cast<double*>(ctx->in_a_val.p), static_cast<const uint32_t*>(ctx->in_a_idx.p),
+            static_cast<const uint32_t*>(ctx->in_b_idx.p), maxes);
+        unsigned long long mx[2] = {0, 0};
+        CUDA_TRY(cudaMemcpyAsync(mx, maxes, 16, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]);
+        // validate (convert.cpp:8-37): every entry inside the matrix
+        if (nnz && (mx[0] >= nmajor || mx[1] >= nminor))
+            return fail(PBG_ERR_ARG, "COO entry out of range (structural_error)");
+        const pbg_csx_view da{nmajor, static_cast<uint32_t>(nnz), nnz,
+                              static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                              static_cast<const double*>(ctx->in_a_val.p)};
+        const pbg_csx_view db{static_cast<uint32_t>(nnz), nminor, nnz,
+                              static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                              static_cast<const double*>(ctx->in_b_val.p)};
+        h->t_h2d = ms * 1e-3;
+        if ((r = run_pipeline(ctx, da, db, cfg, st))) return r;
+        if (nnz_out) *nnz_out = ctx->nnz_c;
+        return PBG_OK;
+    });
 }
 
-int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
-                            pbg_handle** out, uint64_t* nnz_c) {
+}  // extern "C"
+
+namespace {
+// pbg_hash_multiply_begin after validation; every error return releases the
+// handle (with_handle)
+int hash_body(pbg_handle* h, const pbg_csx_view* a, const pbg_csx_view* b, uint64_t* nnz_c) {
     using namespace pbg;
-    if (!out) return fail(PBG_ERR_ARG, "out is null");
-    *out = nullptr;
-    int rc;
-    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
-    pbg_config cfg;
-    if (cfg_in) cfg = *cfg_in;
-    else pbg_default_config(&cfg);
-    if (a->ncols != b->nrows)  // require_multipliable (types.hpp:97-102)
-        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
-                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
-                                     "x" + std::to_string(b->ncols));
-    if ((rc = set_device(cfg.device))) return rc;
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    pbg_context* ctx = pool_get(dev);
-    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
-    auto* h = new pbg_handle;
-    h->ctx = ctx;
-    h->cfg = cfg;
+    pbg_context* ctx = h->ctx;
     cudaStream_t st = nullptr;
-    auto bail = [&](int code) {
-        pbg_release(h);
-        return code;
-    };
+    int rc;
+    auto bail = [&](int code) { return code; };
     const uint64_t na = uint64_t(a->ncols) + 1, nbc = uint64_t(b->ncols);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    ScopedEvents eh;
+    cudaEvent_t e0 = eh[0], e1 = eh[1];
     cudaEventRecord(e0, st);
     rc = copy_in(ctx->in_a_ptr, a->ptr, na * 8, st);
     if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
@@ -1262,11 +1264,7 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
     if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
     if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
     cudaEventRecord(e1, st);
-    if (rc) {
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        return bail(rc);
-    }
+    if (rc) return bail(rc);
     const auto* a_ptr = static_cast<const uint64_t*>(ctx->in_a_ptr.p);
     const auto* b_ptr = static_cast<const uint64_t*>(ctx->in_b_ptr.p);
     // scan status words + tickets + scalars for the two scans (zeroed)
@@ -1284,8 +1282,7 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
     auto* bound = static_cast<uint64_t*>(ctx->hbound.p);
     auto* count = static_cast<uint64_t*>(ctx->hcolcnt.p);
     auto* colptr = static_cast<uint64_t*>(ctx->rowptr.p);
-    cudaEvent_t ev[4];
-    for (auto& e : ev) cudaEventCreate(&e);
+    ScopedEvents ev;
     cudaEventRecord(ev[0], st);
     CUDA_TRY(cudaMemsetAsync(zb, 0, zbytes, st));
     if (nbc) k_hash_colflop<<<blocks_for(nbc, 256), 256, 0, st>>>(a_ptr, b_ptr,
@@ -1305,7 +1302,6 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
         for (uint64_t x : hf) {
             nhub += x > HASH_BIG_F;
             if (__builtin_add_overflow(tot, x, &tot)) {
-                for (auto& e : ev) cudaEventDestroy(e);
                 return bail(fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits"));
             }
         }
@@ -1319,15 +1315,10 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
         nhub ? std::max<uint64_t>(1, std::min<uint64_t>({nhub, uint64_t(ctx->num_sms),
                                                          (2ull << 30) / hub_bytes}))
              : 0;
-    if (hub_ctas && (rc = grow(ctx->hdense, hub_ctas * hub_bytes))) {
-        for (auto& e : ev) cudaEventDestroy(e);
-        return bail(rc);
-    }
+    if (hub_ctas && (rc = grow(ctx->hdense, hub_ctas * hub_bytes))) return bail(rc);
     if ((rc = grow(ctx->keys, total * 4 + 16)) || (rc = grow(ctx->vals, total * 8 + 16)) ||
-        (rc = grow(ctx->ccol, total * 4 + 16)) || (rc = grow(ctx->cval, total * 8 + 16))) {
-        for (auto& e : ev) cudaEventDestroy(e);
+        (rc = grow(ctx->ccol, total * 4 + 16)) || (rc = grow(ctx->cval, total * 8 + 16)))
         return bail(rc);
-    }
     HashArgs ha{a_ptr, static_cast<const uint32_t*>(ctx->in_a_idx.p),
                 static_cast<const double*>(ctx->in_a_val.p), b_ptr,
                 static_cast<const uint32_t*>(ctx->in_b_idx.p),
@@ -1400,9 +1391,6 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
     cudaEventElapsedTime(&t_sym, ev[0], ev[1]);
     cudaEventElapsedTime(&t_num, ev[1], ev[2]);
     cudaEventElapsedTime(&t_h2d, e0, e1);
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     ctx->m = nbc;  // the "rows" of the fetched pointer array are C's columns
     ctx->k = a->ncols;
     ctx->n = a->nrows;
@@ -1420,8 +1408,30 @@ int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const 
     ctx->have_result = true;
     h->t_h2d = t_h2d * 1e-3;
     if (nnz_c) *nnz_c = nnz;
-    *out = h;
     return PBG_OK;
+}
+}  // namespace
+
+
+
+extern "C" {
+
+int pbg_hash_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
+                            pbg_handle** out, uint64_t* nnz_c) {
+    using namespace pbg;
+    if (!out) return fail(PBG_ERR_ARG, "out is null");
+    *out = nullptr;
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    if (a->ncols != b->nrows)  // require_multipliable (types.hpp:97-102)
+        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
+                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
+                                     "x" + std::to_string(b->ncols));
+    if ((rc = set_device(cfg.device))) return rc;
+    return with_handle(cfg, out, [&](pbg_handle* h) -> int { return hash_body(h, a, b, nnz_c); });
 }
 
 int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t vseed, int to_csc,
@@ -1441,72 +1451,65 @@ int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t
     int rc;
     if ((rc = validate_cfg(cfg))) return rc;
     if ((rc = set_device(cfg.device))) return rc;
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    pbg_context* ctx = pool_get(dev);
-    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
-    cudaStream_t st = nullptr;
-    if ((rc = grow(ctx->in_a_idx, (raw + 1) * 4)) || (rc = grow(ctx->in_b_idx, (raw + 1) * 4)) ||
-        (rc = grow(ctx->in_b_val, (raw + 1) * 8)) || (rc = grow(ctx->in_a_ptr, (raw + 1) * 8)) ||
-        (rc = grow(ctx->in_b_ptr, (raw + 1) * 8)) || (rc = grow(ctx->in_a_val, (raw + 1) * 8)) ||
-        (rc = grow(ctx->zero_block, 64)))
-        return rc;
-    auto* rows = static_cast<uint32_t*>(ctx->in_a_idx.p);
-    auto* cols = static_cast<uint32_t*>(ctx->in_b_idx.p);
-    uint64_t nnz = raw;
-    if (kind == 0) {
-        k_gen_er<<<blocks_for(n, 256), 256, 0, st>>>(scale, ef, seed, rows, cols);
-    } else {
-        // draws, then self-loops dropped by a compaction (duplicates are
-        // collapsed by the conversion below)
-        const uint64_t tiles = (raw + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
-        if ((rc = grow(ctx->gen_r, raw * 4)) || (rc = grow(ctx->gen_c, raw * 4)) ||
-            (rc = grow(ctx->gen_pos, (raw + 1) * 8)) || (rc = grow(ctx->gen_stat, (tiles + 16) * 8)))
+    return with_handle(cfg, out, [&](pbg_handle* h) -> int {
+        pbg_context* ctx = h->ctx;
+        cudaStream_t st = nullptr;
+        int rc;
+        if ((rc = grow(ctx->in_a_idx, (raw + 1) * 4)) || (rc = grow(ctx->in_b_idx, (raw + 1) * 4)) ||
+            (rc = grow(ctx->in_b_val, (raw + 1) * 8)) || (rc = grow(ctx->in_a_ptr, (raw + 1) * 8)) ||
+            (rc = grow(ctx->in_b_ptr, (raw + 1) * 8)) || (rc = grow(ctx->in_a_val, (raw + 1) * 8)) ||
+            (rc = grow(ctx->zero_block, 64)))
             return rc;
-        auto* gr = static_cast<uint32_t*>(ctx->gen_r.p);
-        auto* gc = static_cast<uint32_t*>(ctx->gen_c.p);
-        auto* pos = static_cast<uint64_t*>(ctx->gen_pos.p);
-        auto* gst = static_cast<unsigned long long*>(ctx->gen_stat.p);
-        CUDA_TRY(cudaMemsetAsync(gst, 0, (tiles + 16) * 8, st));
-        k_gen_rmat<<<blocks_for(raw, 256), 256, 0, st>>>(scale, raw, seed, 0.57, 0.19, 0.19, gr, gc);
-        launch_scan(OffDiagIn{gr, gc}, pos, raw, nullptr, raw, gst + 16,
-                    reinterpret_cast<unsigned int*>(gst), nullptr, nullptr, st);
-        k_compact_offdiag<<<blocks_for(raw, 256), 256, 0, st>>>(gr, gc, pos, raw, rows, cols);
-        CUDA_TRY(cudaMemcpyAsync(&nnz, pos + raw, 8, cudaMemcpyDeviceToHost, st));
-    }
-    auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
-    CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    const uint32_t* major = to_csc ? cols : rows;
-    const uint32_t* minor = to_csc ? rows : cols;
-    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
-        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
-        static_cast<double*>(ctx->in_a_val.p), major, minor, maxes);
-    // B's values: 1.0 (duplicates sum to their multiplicity; replaced below)
-    k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
-        nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
-        static_cast<double*>(ctx->in_b_val.p), major, minor, maxes);
-    const pbg_csx_view da{static_cast<uint32_t>(n), static_cast<uint32_t>(nnz), nnz,
-                          static_cast<const uint64_t*>(ctx->in_a_ptr.p), major,
-                          static_cast<const double*>(ctx->in_a_val.p)};
-    const pbg_csx_view db{static_cast<uint32_t>(nnz), static_cast<uint32_t>(n), nnz,
-                          static_cast<const uint64_t*>(ctx->in_b_ptr.p), minor,
-                          static_cast<const double*>(ctx->in_b_val.p)};
-    auto* h = new pbg_handle;
-    h->ctx = ctx;
-    h->cfg = cfg;
-    if ((rc = run_pipeline(ctx, da, db, cfg, st))) {
-        pbg_release(h);
-        return rc;
-    }
-    k_fill_values<<<blocks_for(n, 256), 256, 0, st>>>(
-        vseed, n, static_cast<const uint64_t*>(ctx->rowptr.p), static_cast<const uint32_t*>(ctx->ccol.p),
-        static_cast<double*>(ctx->cval.p), to_csc);
-    CUDA_TRY(cudaStreamSynchronize(st));
-    CUDA_TRY(cudaGetLastError());
-    if (nnz_out) *nnz_out = ctx->nnz_c;
-    *out = h;
-    return PBG_OK;
+        auto* rows = static_cast<uint32_t*>(ctx->in_a_idx.p);
+        auto* cols = static_cast<uint32_t*>(ctx->in_b_idx.p);
+        uint64_t nnz = raw;
+        if (kind == 0) {
+            k_gen_er<<<blocks_for(n, 256), 256, 0, st>>>(scale, ef, seed, rows, cols);
+        } else {
+            // draws, then self-loops dropped by a compaction (duplicates are
+            // collapsed by the conversion below)
+            const uint64_t tiles = (raw + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+            if ((rc = grow(ctx->gen_r, raw * 4)) || (rc = grow(ctx->gen_c, raw * 4)) ||
+                (rc = grow(ctx->gen_pos, (raw + 1) * 8)) || (rc = grow(ctx->gen_stat, (tiles + 16) * 8)))
+                return rc;
+            auto* gr = static_cast<uint32_t*>(ctx->gen_r.p);
+            auto* gc = static_cast<uint32_t*>(ctx->gen_c.p);
+            auto* pos = static_cast<uint64_t*>(ctx->gen_pos.p);
+            auto* gst = static_cast<unsigned long long*>(ctx->gen_stat.p);
+            CUDA_TRY(cudaMemsetAsync(gst, 0, (tiles + 16) * 8, st));
+            k_gen_rmat<<<blocks_for(raw, 256), 256, 0, st>>>(scale, raw, seed, 0.57, 0.19, 0.19, gr, gc);
+            launch_scan(OffDiagIn{gr, gc}, pos, raw, nullptr, raw, gst + 16,
+                        reinterpret_cast<unsigned int*>(gst), nullptr, nullptr, st);
+            k_compact_offdiag<<<blocks_for(raw, 256), 256, 0, st>>>(gr, gc, pos, raw, rows, cols);
+            CUDA_TRY(cudaMemcpyAsync(&nnz, pos + raw, 8, cudaMemcpyDeviceToHost, st));
+        }
+        auto* maxes = static_cast<unsigned long long*>(ctx->zero_block.p);
+        CUDA_TRY(cudaMemsetAsync(maxes, 0, 16, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        const uint32_t* major = to_csc ? cols : rows;
+        const uint32_t* minor = to_csc ? rows : cols;
+        k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+            nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+            static_cast<double*>(ctx->in_a_val.p), major, minor, maxes);
+        // B's values: 1.0 (duplicates sum to their multiplicity; replaced below)
+        k_coo_views<<<blocks_for(nnz + 1, 256), 256, 0, st>>>(
+            nnz, static_cast<uint64_t*>(ctx->in_a_ptr.p), static_cast<uint64_t*>(ctx->in_b_ptr.p),
+            static_cast<double*>(ctx->in_b_val.p), major, minor, maxes);
+        const pbg_csx_view da{static_cast<uint32_t>(n), static_cast<uint32_t>(nnz), nnz,
+                              static_cast<const uint64_t*>(ctx->in_a_ptr.p), major,
+                              static_cast<const double*>(ctx->in_a_val.p)};
+        const pbg_csx_view db{static_cast<uint32_t>(nnz), static_cast<uint32_t>(n), nnz,
+                              static_cast<const uint64_t*>(ctx->in_b_ptr.p), minor,
+                              static_cast<const double*>(ctx->in_b_val.p)};
+        if ((rc = run_pipeline(ctx, da, db, cfg, st))) return rc;
+        k_fill_values<<<blocks_for(n, 256), 256, 0, st>>>(
+            vseed, n, static_cast<const uint64_t*>(ctx->rowptr.p), static_cast<const uint32_t*>(ctx->ccol.p),
+            static_cast<double*>(ctx->cval.p), to_csc);
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaGetLastError());
+        if (nnz_out) *nnz_out = ctx->nnz_c;
+        return PBG_OK;
+    });
 }
 
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,

@@ -58,7 +58,7 @@ struct HashArgs {
     uint32_t* s_rows;       // scratch output (flop-bound sized)
     double* s_vals;
     uint64_t* count;        // merged entries per column
-    unsigned int* err;      // bit0: a column above HASH_BIG_F
+    unsigned int* err;      // reserved (no error is raised by the column kernels)
 };
 
 template <int NT, int TMAX, int MMAX>
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) k_hash_cols(HashArgs a, uint64_t lo_f, uin
 #endif
         for (uint32_t s = tid; s < T; s += NT) {
             sm.key[s] = HASH_EMPTY;
-            sm.val[s] = 0.0;
+            sm.val[s] = -0.0;  // the additive identity: a lone -0.0 product keeps its sign
         }
         __syncthreads();
         // ---- accumulate: warp w takes B entries w, w + NW, ...; lanes walk A(:, i)
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NWARP * 32) k_hash_warp(HashArgs a, uint64_t l
         while (T < f + 1) T <<= 1;
         for (uint32_t s2 = lane; s2 < T; s2 += 32) {
             K[s2] = HASH_EMPTY;
-            V[s2] = 0.0;
+            V[s2] = -0.0;  // as k_hash_cols / k_hash_hub
         }
         __syncwarp();
         // ---- products, 32 B entries per chunk, flattened over the lanes
@@ -337,12 +337,14 @@ __global__ void __launch_bounds__(NT) k_hash_hub(HashArgs a, uint64_t lo_f, uint
                                                  double* __restrict__ dense,
                                                  uint32_t* __restrict__ bits) {
     __shared__ uint32_t s_warp[NT / 32 + 1];
-    const uint32_t nw = (nrows + 31) / 32;
+    // 64-bit word / row arithmetic: nrows up to 2^32 - 1 (the host sizes the
+    // bitmap with the same 64-bit count)
+    const uint64_t nw = (uint64_t(nrows) + 31) / 32;
     double* dv = dense + uint64_t(blockIdx.x) * nrows;
     uint32_t* bm = bits + uint64_t(blockIdx.x) * nw;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    for (uint32_t r = threadIdx.x; r < nrows; r += NT) dv[r] = -0.0;
-    for (uint32_t w = threadIdx.x; w < nw; w += NT) bm[w] = 0u;
+    for (uint64_t r = threadIdx.x; r < nrows; r += NT) dv[r] = -0.0;
+    for (uint64_t w = threadIdx.x; w < nw; w += NT) bm[w] = 0u;
     __syncthreads();
     for (uint64_t j = blockIdx.x; j < a.ncols; j += gridDim.x) {
         if (a.flop[j] <= lo_f) continue;  // uniform over the CTA
@@ -360,13 +362,13 @@ __global__ void __launch_bounds__(NT) k_hash_hub(HashArgs a, uint64_t lo_f, uint
         __syncthreads();
         const uint64_t base = a.bound[j];
         uint32_t done = 0;
-        for (uint32_t w0 = 0; w0 < nw; w0 += NT) {
-            const uint32_t w = w0 + threadIdx.x;
+        for (uint64_t w0 = 0; w0 < nw; w0 += NT) {
+            const uint64_t w = w0 + threadIdx.x;
             const uint32_t word = w < nw ? __ldcg(bm + w) : 0u;
             uint32_t tot;
             uint32_t k = done + block_exclusive_scan<NT>(uint32_t(__popc(word)), s_warp, tot);
             for (uint32_t x = word; x; x &= x - 1) {
-                const uint32_t r = w * 32 + (__ffs(x) - 1);
+                const uint32_t r = static_cast<uint32_t>(w * 32 + (__ffs(x) - 1));
                 a.s_rows[base + k] = r;
                 a.s_vals[base + k] = __ldcg(dv + r);
                 dv[r] = -0.0;
@@ -378,14 +380,6 @@ __global__ void __launch_bounds__(NT) k_hash_hub(HashArgs a, uint64_t lo_f, uint
         if (threadIdx.x == 0) a.count[j] = done;
         __syncthreads();
     }
-}
-
-// Columns above the large-table capacity: flag them (the host reports
-// PBG_ERR_UNIMPLEMENTED).
-__global__ void k_hash_check(const uint64_t* __restrict__ flop, uint64_t ncols, uint64_t hi_f,
-                             unsigned int* err) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j < ncols && flop[j] > hi_f) atomicOr(err, 1u);
 }
 
 // Tight CSC from the scratch ranges (ScratchOutput::compact, baseline.cpp:

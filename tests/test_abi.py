@@ -86,3 +86,43 @@ def test_cpp_dropin_compiles_and_keeps_error_contract(tmp_path):
     if not api.device_available():
         r = subprocess.run([str(exe), "nodevice"], capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _build_report_test(tmp_path):
+    shim = build.build_shim()
+    exe = tmp_path / "report_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "cpp" / "report_test.cpp"), "-L", str(shim.parent),
+                    "-lspgemm_b200", f"-Wl,-rpath,{shim.parent}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_report_roofline_headers(tmp_path):
+    """report.hpp / roofline.hpp / validate(): the reference's measurement
+    callers compile against include/spgemm_b200 and the roofline KATs of
+    test_roofline.cpp hold (no device needed for these)."""
+    exe = _build_report_test(tmp_path)
+    if not api.device_available():
+        r = subprocess.run([str(exe), "nodevice"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_report_run_once_on_gpu(tmp_path):
+    exe = _build_report_test(tmp_path)
+    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_hash_multiply_rejects_wrong_types_before_native_views():
+    a_csr = M.make_matrix("er", 6, 2, 1)
+    a = M.csr_to_csc(a_csr)
+    with pytest.raises(TypeError):
+        api.hash_multiply(a_csr, a)  # CSR left operand
+    with pytest.raises(TypeError):
+        api.hash_multiply(a, a_csr)  # CSR right operand
+    bad = M.CscMatrix(a.nrows, a.ncols, a.colptr, a.rowids.astype(np.int64), a.values)
+    with pytest.raises(TypeError):
+        api.hash_multiply(bad, a)
+    with pytest.raises(TypeError):
+        api.pb_multiply(a_csr, a_csr)

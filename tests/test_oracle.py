@@ -94,3 +94,27 @@ def test_port_equals_reference_live(seed):
         assert np.array_equal(p.colids, q.colids)
         assert np.array_equal(p.values, q.values)
         assert np.array_equal(p.per_bin_flop, q.per_bin_flop)
+
+
+@pytest.mark.parametrize("kind,scale,ef", [("er", 16, 4), ("rmat", 12, 8), ("stencil", 8, None)])
+def test_reference_arm_inputs_match_product_inputs(kind, scale, ef):
+    """bench.py --impl reference builds its inputs with the reference library
+    alone (oracle.RefConfig); they must be the product's inputs bit for bit."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2002_11302_b200 import matrices as M
+    rc = oracle.RefConfig(kind, scale, ef or 0, 1, 1 ^ M.VALUE_SEED_XOR)
+    (ap, ai, av), (bp, bi, bv) = rc.arrays()
+    csr = M.make_matrix(kind, scale, ef, 1)
+    csc = M.csr_to_csc(csr)
+    for x, y in [(ap, csc.colptr), (ai, csc.rowids), (av, csc.values), (bp, csr.rowptr),
+                 (bi, csr.colids), (bv, csr.values)]:
+        assert np.array_equal(x, y)
+    assert rc.flop == int(M.row_flop(csc, csr).sum())
+    t, flop, nnz = rc.multiply(2)
+    assert flop == rc.flop and t[5] > 0
+    r1, bf = rc.band(0.25)
+    assert 0 < r1 < rc.nrows and 0 < bf < rc.flop
+    _, flop_b, _ = rc.multiply(2)
+    assert flop_b == bf
+    rc.close()
