@@ -72,12 +72,25 @@ typedef struct pbg_config {
     int32_t balanced_bins; /* reference-layout report only                 */
     int32_t device;        /* CUDA ordinal, -1 = current device            */
     uint32_t bin_cap;      /* GPU bin capacity in tuples, 0 = default 4096 */
-    /* reserved[0]: cap on tuples per round of the host path (0 = from free
-     * HBM); when flop exceeds it, pbg_multiply_begin runs flop-balanced row
-     * bands one after another and assembles C on the host.
+    /* host path: devices to split C's rows over. 0/1 = the
+     * one device `device`; G > 1 = devices device, device+1, ... each taking
+     * a flop-balanced row band of A (cut on the device, balanced_starts
+     * rule) against all of B; -1 = every visible device. */
+    int32_t ngpus;
+    uint32_t flags;        /* PBG_FLAG_* */
+    /* reserved[0]: cap on tuples per round (0 = from free HBM); above it a
+     * device multiplies its rows as flop-balanced bands one after another.
      * reserved[1]: force the number of expand row bands (0 = auto). */
     uint64_t reserved[4];
 } pbg_config;
+
+/* pbg_config.flags */
+enum {
+    /* test hook: with ngpus > the visible device count, bands wrap around the
+     * devices (several contexts on one device; bands never wait on each
+     * other) so the multi-device path runs on a one-GPU box */
+    PBG_FLAG_WRAP_DEVICES = 1
+};
 
 /* spgemm::PhaseReport times (report.hpp:26-33) measured with CUDA events,
  * plus the acceptance counters (acceptance.cpp:46-58). t_sort covers the
@@ -99,6 +112,10 @@ typedef struct pbg_report {
     uint32_t pad0;
     double t_count;            /* per-bin distinct-key count + offset scan (in t_sort) */
     double t_sortmerge_kernel; /* the sort+merge+CSR kernel alone (in t_sort)     */
+    uint32_t ngpus;            /* devices the row bands ran on (host path)        */
+    uint32_t nrounds;          /* most bounded-memory rounds on one device        */
+    double t_device_max;       /* slowest device: its bands' t_total summed       */
+    double t_device_min;       /* fastest device                                  */
 } pbg_report;
 
 typedef struct pbg_handle pbg_handle;
@@ -119,6 +136,17 @@ int pbg_multiply_begin(const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
  * be NULL. */
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
                        pbg_report* rep);
+/* One call, C written straight into caller-owned host arrays: rowptr
+ * [nrows+1], colids/values of capacity cap entries (pinned memory makes the
+ * copies asynchronous). C = A*B is computed as flop-balanced row bands sized
+ * to free HBM, each band's copy to the host overlapping the next band's
+ * multiply — products whose tuples or C exceed HBM (C3) run without host
+ * staging. With cfg.ngpus > 1 the bands run on several devices. Returns
+ * PBG_ERR_ARG with *nnz_c = the bands' nnz so far when cap is too small.
+ * rep->t_d2h = wall time of the whole call. */
+int pbg_multiply_into(const pbg_csx_view* a_csc, const pbg_csx_view* b_csr, const pbg_config* cfg,
+                      uint64_t* rowptr, uint32_t* colids, double* values, uint64_t cap,
+                      uint64_t* nnz_c, pbg_report* rep);
 /* coo_to_csr / coo_to_csc (convert.cpp:41-98) on the GPU, through the same
  * pipeline: the conversion is the product A.B with A(major(e), e) = 1 and
  * B(e, minor(e)) = val(e), so duplicates are summed (exact zeros kept) and
@@ -173,6 +201,29 @@ int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg, uint64_t* per_
                          uint64_t* per_bin_flop, uint32_t* bin_row_starts);
 /* Kernel launches issued by the last pbg_multiply_device call. */
 uint32_t pbg_context_launches(pbg_context* ctx);
+
+/* ---- row bands on the device (pbg_bands.cuh) ----------- */
+/* Flop-balanced cuts of the rows of C = A*B into nbands bands (device-
+ * resident A in CSC, B in CSR): cuts[0] = 0, cuts[nbands] = nrows(A), cut j
+ * after the first row whose inclusive flop prefix reaches j/nbands of the
+ * total (the reference's balanced_starts rule, pb_spgemm.cpp:58-82). *flop
+ * (may be NULL) = flop of the whole product. Host destination for cuts. */
+int pbg_band_cuts_device(pbg_context* ctx, const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
+                         uint32_t nbands, void* stream, uint32_t* cuts, uint64_t* flop);
+/* C(r0:r1, :) = A(r0:r1, :) * B for device-resident A (the whole CSC) and B:
+ * the row slab of A is extracted on the device, the product has r1 - r0 rows
+ * (band-local rowptr) and is read with pbg_context_result like a
+ * pbg_multiply_device product. */
+int pbg_multiply_device_band(pbg_context* ctx, const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
+                             uint32_t r0, uint32_t r1, const pbg_config* cfg, void* stream,
+                             uint64_t* nnz_c, pbg_report* rep);
+/* Checksum of the context's last product (its own rows numbered from
+ * row_base): out[0] = nnz, out[1] = row-count hash, out[2] = (row, col)
+ * hash (order-free, sums of mixed words: bands add up to the whole); *vsum =
+ * sum of the values. The checksum-and-discard mode of products whose C is
+ * kept nowhere (C5b). */
+int pbg_context_checksum(pbg_context* ctx, uint64_t row_base, void* stream, uint64_t* out,
+                         double* vsum);
 
 /* ---- reference helpers with no device work --------------------------- */
 /* choose_nbins (pb_spgemm.cpp:10-18) */

@@ -38,7 +38,10 @@ class CsxView(C.Structure):
 class Config(C.Structure):
     _fields_ = [("nbins", u32), ("lbin_bytes", u32), ("l2_bytes", u64),
                 ("nthreads", i32), ("balanced_bins", i32), ("device", i32),
-                ("bin_cap", u32), ("reserved", u64 * 4)]
+                ("bin_cap", u32), ("ngpus", i32), ("flags", u32), ("reserved", u64 * 4)]
+
+
+PBG_FLAG_WRAP_DEVICES = 1
 
 
 class Report(C.Structure):
@@ -50,7 +53,8 @@ class Report(C.Structure):
                 ("nbins", u32), ("gpu_bins", u32), ("heavy_bins", u32), ("bin_cap", u32),
                 ("tuple_bytes", u64), ("sort_fallbacks", u64),
                 ("expand_bands", u32), ("pad0", u32),
-                ("t_count", f64), ("t_sortmerge_kernel", f64)]
+                ("t_count", f64), ("t_sortmerge_kernel", f64),
+                ("ngpus", u32), ("nrounds", u32), ("t_device_max", f64), ("t_device_min", f64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -62,6 +66,8 @@ PBG_EXPORTS = {
     "pbg_device_available": (C.c_int, []),
     "pbg_multiply_begin": (C.c_int, [P(CsxView), P(CsxView), P(Config), P(vp), P(u64)]),
     "pbg_multiply_fetch": (C.c_int, [vp, vp, vp, vp, P(Report)]),
+    "pbg_multiply_into": (C.c_int, [P(CsxView), P(CsxView), P(Config), vp, vp, vp, u64, P(u64),
+                                    P(Report)]),
     "pbg_generate_begin": (C.c_int, [C.c_int, C.c_int, u32, u64, u64, C.c_int, P(Config), P(vp),
                                      P(u64)]),
     "pbg_hash_multiply_begin": (C.c_int, [P(CsxView), P(CsxView), P(Config), P(vp), P(u64)]),
@@ -75,6 +81,10 @@ PBG_EXPORTS = {
     "pbg_context_result": (C.c_int, [vp, P(vp), P(vp), P(vp)]),
     "pbg_context_symbolic": (C.c_int, [vp, P(Config), vp, vp, vp]),
     "pbg_context_launches": (u32, [vp]),
+    "pbg_band_cuts_device": (C.c_int, [vp, P(CsxView), P(CsxView), u32, vp, vp, P(u64)]),
+    "pbg_multiply_device_band": (C.c_int, [vp, P(CsxView), P(CsxView), u32, u32, P(Config), vp,
+                                           P(u64), P(Report)]),
+    "pbg_context_checksum": (C.c_int, [vp, u64, vp, vp, P(f64)]),
     "pbg_choose_nbins": (u32, [u64, u32, u64, u32]),
 }
 

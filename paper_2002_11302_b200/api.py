@@ -56,6 +56,8 @@ class PbConfig:
     bin_cap: int = 0  # GPU shared-memory bin capacity in tuples (0 = 4096)
     max_round_tuples: int = 0  # host path: tuples per bounded-memory round (0 = from free HBM)
     expand_bands: int = 0  # row bands of the expand (0 = auto, 1 = one pass)
+    ngpus: int = 0  # host path: devices to split C's rows over (0/1 = one, -1 = all)
+    wrap_devices: bool = False  # test hook: more bands than devices wrap around them
 
     def to_c(self) -> _native.Config:
         c = _native.Config()
@@ -65,6 +67,8 @@ class PbConfig:
         c.device, c.bin_cap = self.device, self.bin_cap
         c.reserved[0] = self.max_round_tuples
         c.reserved[1] = self.expand_bands
+        c.ngpus = self.ngpus
+        c.flags = _native.PBG_FLAG_WRAP_DEVICES if self.wrap_devices else 0
         return c
 
 
@@ -119,8 +123,10 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
                 symbolic: bool = True, out=None) -> PbResult:
     """C = A·B on the GPU, A in CSC, B in CSR, C in CSR (host buffers in/out).
 
-    ``out`` = (rowptr, colids, values) caller-owned host arrays (e.g. pinned)
-    large enough for C; the returned CsrMatrix views them."""
+    ``out`` = (rowptr, colids, values) caller-owned host arrays (e.g. pinned):
+    C is written straight into them by pbg_multiply_into (row bands whose
+    copies overlap the next band's multiply; no host staging, so products
+    whose C exceeds HBM work too). The returned CsrMatrix views them."""
     cfg = cfg or PbConfig()
     lib = _native.pbg()
     if not isinstance(a, CscMatrix) or not isinstance(b, CsrMatrix):
@@ -129,6 +135,27 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
     va = _view(a.nrows, a.ncols, ap, ai, av)
     vb = _view(b.nrows, b.ncols, bp, bi, bv)
     c_cfg = cfg.to_c()
+    if out is not None:
+        rowptr, colids, values = out
+        if rowptr.size < a.nrows + 1 or rowptr.dtype != np.uint64 or colids.dtype != np.uint32 \
+                or values.dtype != np.float64 or colids.size != values.size:
+            raise TypeError("out = (u64 rowptr[nrows+1], u32 colids[cap], f64 values[cap])")
+        nnz = C.c_uint64(0)
+        rep = _native.Report()
+        rc = lib.pbg_multiply_into(C.byref(va), C.byref(vb), C.byref(c_cfg), rowptr.ctypes.data,
+                                   colids.ctypes.data, values.ctypes.data, colids.size,
+                                   C.byref(nnz), C.byref(rep))
+        if rc:
+            _raise(rc)
+        k = nnz.value
+        r = rep.as_dict()
+        phases = {key: r[key] for key in ("t_symbolic", "t_expand", "t_sort", "t_compress",
+                                          "t_convert", "t_total", "t_h2d", "t_d2h")}
+        c = CsrMatrix(a.nrows, b.ncols, rowptr[:a.nrows + 1], colids[:k], values[:k])
+        if c.nnz != rep.merged_total:
+            raise InternalError("compressed counts disagree with output nnz")
+        return PbResult(c, SymbolicResult(flop=rep.flop, nbins=rep.nbins), phases,
+                        rep.tuples_into_sort, rep.merged_total, r)
     h = C.c_void_p()
     nnz = C.c_uint64(0)
     rc = lib.pbg_multiply_begin(C.byref(va), C.byref(vb), C.byref(c_cfg), C.byref(h), C.byref(nnz))
@@ -136,12 +163,9 @@ def pb_multiply(a: CscMatrix, b: CsrMatrix, cfg: PbConfig | None = None,
         _raise(rc)
     try:
         k = nnz.value
-        if out is not None and out[1].size >= k and out[0].size >= a.nrows + 1:
-            rowptr, colids, values = out
-        else:
-            rowptr = np.empty(a.nrows + 1, np.uint64)
-            colids = np.empty(max(k, 1), np.uint32)
-            values = np.empty(max(k, 1), np.float64)
+        rowptr = np.empty(a.nrows + 1, np.uint64)
+        colids = np.empty(max(k, 1), np.uint32)
+        values = np.empty(max(k, 1), np.float64)
         rep = _native.Report()
         rc = lib.pbg_multiply_fetch(h, rowptr.ctypes.data, colids.ctypes.data,
                                     values.ctypes.data, C.byref(rep))
@@ -302,6 +326,45 @@ class DeviceContext:
         if rc:
             _raise(rc)
         return nnz.value, rep.as_dict()
+
+    def band_cuts(self, a_view, b_view, nbands: int, stream: int = 0):
+        """Flop-balanced row cuts of A*B into nbands bands, computed on the
+        device (balanced_starts rule, pb_spgemm.cpp:58-82): (cuts, flop)."""
+        cuts = np.zeros(nbands + 1, np.uint32)
+        flop = C.c_uint64(0)
+        rc = self._lib.pbg_band_cuts_device(self._ctx, C.byref(a_view), C.byref(b_view), nbands,
+                                            C.c_void_p(stream or None), cuts.ctypes.data,
+                                            C.byref(flop))
+        if rc:
+            _raise(rc)
+        return cuts, flop.value
+
+    def multiply_band(self, a_view, b_view, r0: int, r1: int, cfg: PbConfig | None = None,
+                      stream: int = 0):
+        """C(r0:r1, :) = A(r0:r1, :)·B with the row slab of the device-resident
+        A extracted on the device; the band's CSR (r1 - r0 rows) stays in the
+        context (result_pointers)."""
+        cfg = cfg or PbConfig()
+        c_cfg = cfg.to_c()
+        nnz = C.c_uint64(0)
+        rep = _native.Report()
+        rc = self._lib.pbg_multiply_device_band(self._ctx, C.byref(a_view), C.byref(b_view), r0, r1,
+                                                C.byref(c_cfg), C.c_void_p(stream or None),
+                                                C.byref(nnz), C.byref(rep))
+        if rc:
+            _raise(rc)
+        return nnz.value, rep.as_dict()
+
+    def checksum(self, row_base: int = 0, stream: int = 0):
+        """(nnz, row hash, (row, col) hash, value sum) of the last product; the
+        hashes are sums, so the bands of a product add up to its checksum."""
+        out = np.zeros(3, np.uint64)
+        vs = C.c_double(0)
+        rc = self._lib.pbg_context_checksum(self._ctx, row_base, C.c_void_p(stream or None),
+                                            out.ctypes.data, C.byref(vs))
+        if rc:
+            _raise(rc)
+        return int(out[0]), int(out[1]), int(out[2]), vs.value
 
     def result_pointers(self):
         rp, ci, va = C.c_void_p(), C.c_void_p(), C.c_void_p()

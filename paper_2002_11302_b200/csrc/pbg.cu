@@ -5,11 +5,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "pbg.h"
@@ -17,6 +20,7 @@
 #include "pbg_heavy.cuh"
 #include "pbg_sort.cuh"
 #include "pbg_hash.cuh"
+#include "pbg_bands.cuh"
 
 namespace {
 
@@ -111,6 +115,11 @@ struct pbg_context {
     DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
     DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
     DevBuf wb[7];
+    // row bands (pbg_bands.cuh): row-flop prefix / per-column flop of the
+    // whole product, cuts, the current slab of A, checksum words
+    DevBuf bd_zero, bd_rowflop, bd_rowoff, bd_colflop, bd_cuts, sl_cnt, sl_colptr, sl_rowids,
+        sl_vals, ck;
+    DevBuf alt_rowptr, alt_ccol, alt_cval;  // second C of pbg_multiply_into's overlapped rounds
     size_t zero_bytes = 0;
     cudaEvent_t ev[8] = {};
     bool ev_ok = false;
@@ -135,25 +144,36 @@ struct pbg_context {
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
         for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &gen_r, &gen_c, &gen_pos, &gen_stat, &va_colptr, &va_rowids, &va_vals,
-                          &vcolflop, &bcuts, &vstat})
+                          &vcolflop, &bcuts, &vstat, &bd_zero, &bd_rowflop, &bd_rowoff, &bd_colflop,
+                          &bd_cuts, &sl_cnt, &sl_colptr, &sl_rowids, &sl_vals, &ck, &alt_rowptr,
+                          &alt_ccol, &alt_cval})
             b->release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
     }
 };
 
-struct pbg_handle {
+// Rows [r0, r1) of C from one row band: resident in a device context
+// (ctx != nullptr, the band's own CSR there) or staged in host memory.
+struct BandPart {
     pbg_context* ctx = nullptr;
-    pbg_config cfg{};
-    double t_h2d = 0.0;
-    // bounded-memory rounds: C assembled on the host band by band
-    bool rounds = false;
-    uint32_t nrounds = 1;
-    std::vector<uint64_t> rowptr;
+    uint32_t r0 = 0, r1 = 0;
+    uint64_t nnz = 0;
+    std::vector<uint64_t> rowptr;  // staged: band-local rowptr (r1 - r0 + 1)
     std::vector<uint32_t> colids;
     std::vector<double> values;
-    std::vector<uint64_t> row_flop;   // host per-row flop (reference-layout report)
-    std::vector<uint64_t> col_flop;   // host per-column flop
+};
+
+struct pbg_handle {
+    pbg_context* ctx = nullptr;       // device of band 0 (the only one without bands)
+    pbg_config cfg{};
+    double t_h2d = 0.0;
+    // banded product (several devices and/or bounded-memory rounds): C is
+    // the concatenation of the parts in row order; empty = C is ctx's product
+    bool banded = false;
+    std::vector<BandPart> parts;
+    std::vector<pbg_context*> extra;  // contexts of the other devices (pooled on release)
+    uint64_t m = 0, k = 0, nnz_c = 0;
     pbg_report rep{};
 };
 
@@ -520,7 +540,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             hc.skeys = static_cast<uint32_t*>(ctx->skeys.p);
             hc.svals = static_cast<double*>(ctx->svals.p);
             nitems = H;
-            static bool hv_attr[64] = {};
+            static std::atomic<bool> hv_attr[64] = {};  // per device; a concurrent double set is benign
             if (!hv_attr[ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(sizeof(HvScatterSmem))));
@@ -621,7 +641,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
         auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
-            static bool attr_set[2][64] = {};  // [shape][device]
+            static std::atomic<bool> attr_set[2][64] = {};  // [shape][device]
             if (!attr_set[big_table][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
@@ -655,7 +675,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         ++L;
         CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
-        static bool attr_set[64] = {};
+        static std::atomic<bool> attr_set[64] = {};
         if (!attr_set[ctx->device & 63]) {
             CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(sizeof(SortSmem))));
@@ -883,111 +903,262 @@ uint32_t reference_nbins(const pbg_config& cfg, uint64_t flop, uint64_t m, int c
     return nbr;
 }
 
-// Bounded-memory rounds: flop-balanced row bands of A, each
-// extracted on the host as its own CSC, multiplied on the device against the
-// resident B, and its CSR band appended on the host. Every band is the
-// reference product of those rows (C(r0:r1,:) = A(r0:r1,:) * B).
-int multiply_in_rounds(pbg_handle* h, const pbg_csx_view& a, const pbg_csx_view& b,
-                       const pbg_config& cfg, uint32_t nrounds, cudaStream_t st) {
-    pbg_context* ctx = h->ctx;
+// ---------------------------------------------------------------------------
+// Row bands on the device (pbg_bands.cuh). C(r0:r1, :) =
+// A(r0:r1, :) * B: the multi-GPU split (one band per device) and the
+// bounded-memory rounds (bands one after another on a device) are built from
+// these helpers, with no host pass over the matrices.
+
+// Exclusive per-row flop prefix of the whole product into bd_rowoff [m+1]
+// ([m] = flop) and per-column flop into bd_colflop [k] — the reference's
+// symbolic (pb_spgemm.cpp:86-106) at row granularity, the quantity its
+// balanced_starts accumulates (:58-82). Exact 128-bit overflow check (:103).
+int dev_row_prefix(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
+                   cudaStream_t st, uint64_t* flop_out) {
+    using namespace pbg;
+    const uint64_t m = A.nrows, k = A.ncols;
+    const uint64_t tiles = (m + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    const size_t zbytes = (16 + tiles) * 8;
     int rc;
-    const uint64_t m = a.nrows, k = a.ncols;
-    // per-row / per-column flop on the host
-    h->row_flop.assign(m, 0);
-    h->col_flop.assign(k, 0);
-    for (uint64_t j = 0; j < k; ++j) {
-        const uint64_t lb = b.ptr[j + 1] - b.ptr[j];
-        h->col_flop[j] = (a.ptr[j + 1] - a.ptr[j]) * lb;
-        for (uint64_t p = a.ptr[j]; p < a.ptr[j + 1]; ++p) h->row_flop[a.idx[p]] += lb;
+    if ((rc = grow(ctx->bd_zero, zbytes)) || (rc = grow(ctx->bd_rowflop, (m + 1) * 8)) ||
+        (rc = grow(ctx->bd_rowoff, (m + 2) * 8)) || (rc = grow(ctx->bd_colflop, (k + 1) * 8)))
+        return rc;
+    auto* zb = static_cast<unsigned long long*>(ctx->bd_zero.p);
+    unsigned int* tk = reinterpret_cast<unsigned int*>(zb);  // scan ticket
+    unsigned long long* sc = zb + 8;                         // lo, hi, scan total
+    auto* rowflop = static_cast<unsigned long long*>(ctx->bd_rowflop.p);
+    auto* rowoff = static_cast<uint64_t*>(ctx->bd_rowoff.p);
+    CUDA_TRY(cudaMemsetAsync(zb, 0, zbytes, st));
+    if (k) {
+        k_colflop_total<<<std::min<unsigned>(blocks_for(k, 256), 4 * ctx->num_sms), 256, 0, st>>>(
+            A.ptr, B.ptr, k, sc + 0, sc + 1);
+        k_colflop_each<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, B.ptr, k,
+                                                          static_cast<uint64_t*>(ctx->bd_colflop.p));
     }
-    uint64_t flop = 0;
-    for (uint64_t r = 0; r < m; ++r) flop += h->row_flop[r];
-    std::vector<uint32_t> cuts(nrounds + 1, static_cast<uint32_t>(m));
-    cuts[0] = 0;
-    {
-        unsigned __int128 acc = 0;
-        uint32_t j = 1;
-        for (uint64_t r = 0; r < m && j < nrounds; ++r) {
-            acc += h->row_flop[r];
-            while (j < nrounds && acc * nrounds >= (unsigned __int128)flop * j) cuts[j++] = static_cast<uint32_t>(r + 1);
-        }
+    if (m) {
+        CUDA_TRY(cudaMemsetAsync(rowflop, 0, m * 8, st));
+        if (k) k_rowflop<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, B.ptr, k, rowflop);
+        launch_scan(ArrayIn{reinterpret_cast<const uint64_t*>(rowflop)}, rowoff, m, nullptr, m,
+                    zb + 16, tk, sc + 2, nullptr, st);
+    } else {
+        CUDA_TRY(cudaMemsetAsync(rowoff, 0, 8, st));
     }
-    // B stays resident for every round
-    rc = copy_in(ctx->in_b_ptr, b.ptr, (uint64_t(b.nrows) + 1) * 8, st);
-    if (!rc) rc = copy_in(ctx->in_b_idx, b.idx, b.nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_b_val, b.val, b.nnz * 8, st);
+    unsigned long long hs[3];
+    CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    if (hs[1] != 0 || hs[0] > ST_VAL) return fail(PBG_ERR_FLOP_OVERFLOW, "flop count overflows 64 bits");
+    if (m && hs[2] != hs[0]) return fail(PBG_ERR_INTERNAL, "row and column flop totals disagree");
+    *flop_out = hs[0];
+    return PBG_OK;
+}
+
+// Flop-balanced cuts of rows [lo, hi) into g bands from bd_rowoff
+// (dev_row_prefix first); off[j] = flop prefix at cut j. Host outputs.
+int dev_cuts(pbg_context* ctx, uint32_t lo, uint32_t hi, uint32_t g, cudaStream_t st,
+             uint32_t* cuts, uint64_t* off) {
+    using namespace pbg;
+    int rc;
+    if ((rc = grow(ctx->bd_cuts, (g + 1) * 12 + 16))) return rc;
+    auto* dc = static_cast<uint32_t*>(ctx->bd_cuts.p);
+    auto* doff = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->bd_cuts.p) + ((g + 1) * 4 + 15) / 16 * 16);
+    k_cut_search<<<blocks_for(g + 1, 128), 128, 0, st>>>(static_cast<const uint64_t*>(ctx->bd_rowoff.p),
+                                                         lo, hi, g, dc, doff);
+    CUDA_TRY(cudaMemcpyAsync(cuts, dc, (g + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (off) CUDA_TRY(cudaMemcpyAsync(off, doff, (g + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    return PBG_OK;
+}
+
+// The CSC row slab A(r0:r1, :) (rows renumbered from 0) in the sl_* buffers.
+int dev_slab(pbg_context* ctx, const pbg_csx_view& A, uint32_t r0, uint32_t r1, cudaStream_t st,
+             pbg_csx_view* out) {
+    using namespace pbg;
+    const uint64_t k = A.ncols;
+    const uint64_t tiles = (k + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    int rc;
+    if ((rc = grow(ctx->sl_cnt, (k + 1 + 16 + tiles) * 8)) || (rc = grow(ctx->sl_colptr, (k + 2) * 8)))
+        return rc;
+    auto* cnt = static_cast<uint64_t*>(ctx->sl_cnt.p);
+    auto* zb = reinterpret_cast<unsigned long long*>(cnt + k + 1);  // ticket, total, status
+    auto* colptr = static_cast<uint64_t*>(ctx->sl_colptr.p);
+    CUDA_TRY(cudaMemsetAsync(zb, 0, (16 + tiles) * 8, st));
+    if (k) k_slab_count<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, k, r0, r1, cnt);
+    launch_scan(ArrayIn{cnt}, colptr, k, nullptr, k, zb + 16, reinterpret_cast<unsigned int*>(zb),
+                zb + 8, nullptr, st);
+    uint64_t total = 0;
+    CUDA_TRY(cudaMemcpyAsync(&total, colptr + k, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if ((rc = grow(ctx->sl_rowids, total * 4 + 16)) || (rc = grow(ctx->sl_vals, total * 8 + 16))) return rc;
+    if (k)
+        k_slab_copy<<<blocks_for(k, 256), 256, 0, st>>>(
+            A.ptr, A.idx, A.val, k, r0, r1, colptr, static_cast<uint32_t*>(ctx->sl_rowids.p),
+            static_cast<double*>(ctx->sl_vals.p));
+    *out = pbg_csx_view{r1 - r0, A.ncols, total, colptr,
+                        static_cast<const uint32_t*>(ctx->sl_rowids.p),
+                        static_cast<const double*>(ctx->sl_vals.p)};
+    return PBG_OK;
+}
+
+// C(r0:r1, :) into the context (band-local CSR).
+int dev_band_multiply(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B, uint32_t r0,
+                      uint32_t r1, const pbg_config& cfg, cudaStream_t st) {
+    if (r0 == 0 && r1 == A.nrows) return run_pipeline(ctx, A, B, cfg, st);
+    pbg_csx_view slab;
+    int rc = dev_slab(ctx, A, r0, r1, st, &slab);
     if (rc) return rc;
+    return run_pipeline(ctx, slab, B, cfg, st);
+}
+
+void add_report(pbg_report& t, const pbg_report& r) {
+    t.t_symbolic += r.t_symbolic;
+    t.t_expand += r.t_expand;
+    t.t_sort += r.t_sort;
+    t.t_total += r.t_total;
+    t.t_count += r.t_count;
+    t.t_sortmerge_kernel += r.t_sortmerge_kernel;
+    t.flop += r.flop;
+    t.nnz_c += r.nnz_c;
+    t.tuples_into_sort += r.tuples_into_sort;
+    t.merged_total += r.merged_total;
+    t.gpu_bins += r.gpu_bins;
+    t.heavy_bins += r.heavy_bins;
+    t.sort_fallbacks += r.sort_fallbacks;
+    t.tuple_bytes = std::max(t.tuple_bytes, r.tuple_bytes);
+    t.bin_cap = r.bin_cap;
+    t.expand_bands = std::max(t.expand_bands, r.expand_bands);
+}
+
+// Tuples one pass of the host path may hold on this device (tuples + C
+// upper bound + heavy-row scratch + headroom), from free HBM.
+int tuple_budget(pbg_context* ctx, const pbg_csx_view& a, const pbg_csx_view& b,
+                 const pbg_config& cfg, uint64_t* max_tuples) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t inputs = (uint64_t(a.ncols) + uint64_t(b.nrows) + 2) * 8 + (a.nnz + b.nnz) * 12;
+    const uint64_t work_rows = (uint64_t(a.nrows) + 2) * 96;
+    const uint64_t reserve = 2ull << 30;
+    // HBM the context already holds is reusable by the pass
+    const uint64_t held = ctx->keys.cap + ctx->vals.cap + ctx->ccol.cap + ctx->cval.cap +
+                          ctx->skeys.cap + ctx->svals.cap;
+    const uint64_t avail = free_b + held;
+    const uint64_t budget =
+        avail > inputs + work_rows + reserve ? avail - inputs - work_rows - reserve : 0;
+    const uint64_t per_tuple = 40;  // tuples 12 + C bound 12 + heavy scratch 12 + headroom
+    uint64_t mt = std::max<uint64_t>(budget / per_tuple, 1);
+    if (cfg.reserved[0]) mt = std::min<uint64_t>(mt, cfg.reserved[0]);
+    *max_tuples = mt;
+    return PBG_OK;
+}
+
+// Rows [lo, hi) on one device as R flop-balanced bands one after another
+// (bd_rowoff holds the whole product's prefix). A single band may stay in
+// the context (keep); otherwise every band's CSR is copied to host memory.
+int device_rounds(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B, uint32_t lo,
+                  uint32_t hi, uint32_t R, const pbg_config& cfg, cudaStream_t st, bool keep,
+                  std::vector<BandPart>& parts, pbg_report& tot) {
+    std::vector<uint32_t> cuts(R + 1);
+    int rc;
+    if (R == 1) {
+        cuts[0] = lo;
+        cuts[1] = hi;
+    } else if ((rc = dev_cuts(ctx, lo, hi, R, st, cuts.data(), nullptr))) {
+        return rc;
+    }
+    for (uint32_t r = 0; r < R; ++r) {
+        BandPart p;
+        p.r0 = cuts[r];
+        p.r1 = cuts[r + 1];
+        if (p.r0 == p.r1) {  // empty band (a single row heavier than its share)
+            p.rowptr.assign(1, 0);
+            parts.push_back(std::move(p));
+            continue;
+        }
+        if ((rc = dev_band_multiply(ctx, A, B, p.r0, p.r1, cfg, st))) return rc;
+        add_report(tot, ctx->rep);
+        p.nnz = ctx->nnz_c;
+        if (keep && R == 1) {
+            p.ctx = ctx;
+        } else {
+            const uint64_t n = p.r1 - p.r0;
+            p.rowptr.resize(n + 1);
+            p.colids.resize(p.nnz);
+            p.values.resize(p.nnz);
+            CUDA_TRY(cudaMemcpyAsync(p.rowptr.data(), ctx->rowptr.p, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+            if (p.nnz) {
+                CUDA_TRY(cudaMemcpyAsync(p.colids.data(), ctx->ccol.p, p.nnz * 4, cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaMemcpyAsync(p.values.data(), ctx->cval.p, p.nnz * 8, cudaMemcpyDeviceToHost, st));
+            }
+            CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        parts.push_back(std::move(p));
+    }
+    tot.nrounds = std::max(tot.nrounds, R);
+    return PBG_OK;
+}
+
+struct OwnStream {
+    cudaStream_t s = nullptr;
+    ~OwnStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+// One device of the multi-device host path: uploads A and B, cuts the rows
+// into G flop-balanced bands on the device (every device computes the same
+// cuts: no exchange), multiplies its band (in rounds if it does not fit) and
+// keeps it in its context.
+struct DevJob {
+    int device = 0;
+    uint32_t index = 0;
+    pbg_context* ctx = nullptr;
+    int rc = 0;
+    std::string err;
+    std::vector<BandPart> parts;
+    pbg_report rep{};
+    double t_h2d = 0.0;
+};
+
+int device_job(DevJob& j, const pbg_csx_view& a, const pbg_csx_view& b, const pbg_config& cfg,
+               uint32_t G) {
+    CUDA_TRY(cudaSetDevice(j.device));
+    int rc;
+    j.ctx = pool_get(j.device);
+    if (!j.ctx && (rc = make_context(j.device, &j.ctx))) return rc;
+    pbg_context* ctx = j.ctx;
+    OwnStream os;
+    CUDA_TRY(cudaStreamCreateWithFlags(&os.s, cudaStreamNonBlocking));
+    cudaStream_t st = os.s;
+    ScopedEvents ev;
+    CUDA_TRY(cudaEventRecord(ev[0], st));
+    if ((rc = copy_in(ctx->in_a_ptr, a.ptr, (uint64_t(a.ncols) + 1) * 8, st)) ||
+        (rc = copy_in(ctx->in_a_idx, a.idx, a.nnz * 4, st)) ||
+        (rc = copy_in(ctx->in_a_val, a.val, a.nnz * 8, st)) ||
+        (rc = copy_in(ctx->in_b_ptr, b.ptr, (uint64_t(b.nrows) + 1) * 8, st)) ||
+        (rc = copy_in(ctx->in_b_idx, b.idx, b.nnz * 4, st)) ||
+        (rc = copy_in(ctx->in_b_val, b.val, b.nnz * 8, st)))
+        return rc;
+    CUDA_TRY(cudaEventRecord(ev[1], st));
+    const pbg_csx_view da{a.nrows, a.ncols, a.nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                          static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                          static_cast<const double*>(ctx->in_a_val.p)};
     const pbg_csx_view db{b.nrows, b.ncols, b.nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
                           static_cast<const uint32_t*>(ctx->in_b_idx.p),
                           static_cast<const double*>(ctx->in_b_val.p)};
-    h->rounds = true;
-    h->nrounds = nrounds;
-    h->rowptr.assign(m + 1, 0);
-    h->colids.clear();
-    h->values.clear();
-    pbg_report tot{};
-    std::vector<uint64_t> sp(k + 1);
-    std::vector<uint32_t> si;
-    std::vector<double> sv;
-    std::vector<uint64_t> brow;
-    for (uint32_t rd = 0; rd < nrounds; ++rd) {
-        const uint32_t r0 = cuts[rd], r1 = cuts[rd + 1];
-        // host row slab of A (rows renumbered from 0), pbgh_csc_row_band
-        // semantics; row ids inside a column need not be sorted
-        si.clear();
-        sv.clear();
-        sp[0] = 0;
-        for (uint64_t j = 0; j < k; ++j) {
-            for (uint64_t q = a.ptr[j]; q < a.ptr[j + 1]; ++q) {
-                const uint32_t r = a.idx[q];
-                if (r < r0 || r >= r1) continue;
-                si.push_back(r - r0);
-                sv.push_back(a.val[q]);
-            }
-            sp[j + 1] = si.size();
-        }
-        rc = copy_in(ctx->in_a_ptr, sp.data(), (k + 1) * 8, st);
-        if (!rc) rc = copy_in(ctx->in_a_idx, si.data(), si.size() * 4, st);
-        if (!rc) rc = copy_in(ctx->in_a_val, sv.data(), sv.size() * 8, st);
-        if (rc) return rc;
-        const pbg_csx_view da{r1 - r0, a.ncols, si.size(), static_cast<const uint64_t*>(ctx->in_a_ptr.p),
-                              static_cast<const uint32_t*>(ctx->in_a_idx.p),
-                              static_cast<const double*>(ctx->in_a_val.p)};
-        if ((rc = run_pipeline(ctx, da, db, cfg, st))) return rc;
-        const uint64_t base = h->colids.size(), bn = ctx->nnz_c;
-        brow.resize(uint64_t(r1 - r0) + 1);
-        CUDA_TRY(cudaMemcpy(brow.data(), ctx->rowptr.p, brow.size() * 8, cudaMemcpyDeviceToHost));
-        for (uint64_t r = 0; r < uint64_t(r1 - r0); ++r) h->rowptr[r0 + r] = base + brow[r];
-        h->colids.resize(base + bn);
-        h->values.resize(base + bn);
-        if (bn) {
-            CUDA_TRY(cudaMemcpy(h->colids.data() + base, ctx->ccol.p, bn * 4, cudaMemcpyDeviceToHost));
-            CUDA_TRY(cudaMemcpy(h->values.data() + base, ctx->cval.p, bn * 8, cudaMemcpyDeviceToHost));
-        }
-        const pbg_report& r = ctx->rep;
-        tot.t_symbolic += r.t_symbolic;
-        tot.t_expand += r.t_expand;
-        tot.t_sort += r.t_sort;
-        tot.t_total += r.t_total;
-        tot.t_count += r.t_count;
-        tot.t_sortmerge_kernel += r.t_sortmerge_kernel;
-        tot.flop += r.flop;
-        tot.tuples_into_sort += r.tuples_into_sort;
-        tot.merged_total += r.merged_total;
-        tot.gpu_bins += r.gpu_bins;
-        tot.heavy_bins += r.heavy_bins;
-        tot.sort_fallbacks += r.sort_fallbacks;
-        tot.tuple_bytes = std::max(tot.tuple_bytes, r.tuple_bytes);
-        tot.bin_cap = r.bin_cap;
-    }
-    h->rowptr[m] = h->colids.size();
-    tot.nnz_c = h->colids.size();
-    tot.nnz_a = a.nnz;
-    tot.nnz_b = b.nnz;
-    tot.nbins = reference_nbins(cfg, flop, m, ctx->col_bits);
-    h->rep = tot;
-    if (tot.flop != flop || tot.merged_total != tot.nnz_c)
-        return fail(PBG_ERR_INTERNAL, "round totals disagree with the full product");
+    uint64_t flop = 0;
+    if ((rc = dev_row_prefix(ctx, da, db, st, &flop))) return rc;
+    std::vector<uint32_t> cuts(G + 1);
+    std::vector<uint64_t> off(G + 1);
+    if ((rc = dev_cuts(ctx, 0, a.nrows, G, st, cuts.data(), off.data()))) return rc;
+    const uint32_t lo = cuts[j.index], hi = cuts[j.index + 1];
+    const uint64_t band_flop = off[j.index + 1] - off[j.index];
+    uint64_t max_tuples = 1;
+    if ((rc = tuple_budget(ctx, a, b, cfg, &max_tuples))) return rc;
+    const uint32_t R = static_cast<uint32_t>(std::max<uint64_t>(1, (band_flop + max_tuples - 1) / max_tuples));
+    if ((rc = device_rounds(ctx, da, db, lo, hi, R, cfg, st, true, j.parts, j.rep))) return rc;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ev[0], ev[1]) == cudaSuccess) j.t_h2d = ms * 1e-3;
     return PBG_OK;
 }
 
@@ -1114,71 +1285,253 @@ int pbg_multiply_begin(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_c
                                      "x" + std::to_string(b->ncols));
     if ((rc = validate_cfg(cfg))) return rc;
     if ((rc = set_device(cfg.device))) return rc;
-    int dev = 0;
-    CUDA_TRY(cudaGetDevice(&dev));
-    pbg_context* ctx = pool_get(dev);
-    if (!ctx && (rc = make_context(dev, &ctx))) return rc;
-    auto* h = new pbg_handle;
-    h->ctx = ctx;
-    h->cfg = cfg;
-    cudaStream_t st = nullptr;
-    // ---- memory plan: one pass, or bounded-memory rounds over row bands ----
-    // (configs whose tuples + C exceed HBM run band by band).
-    // The pass starts optimistically; its symbolic phase knows flop exactly
-    // and stops before any tuple storage is allocated when it does not fit.
-    size_t free_b = 0, total_b = 0;
-    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t inputs = (uint64_t(a->ncols) + uint64_t(b->nrows) + 2) * 8 + (a->nnz + b->nnz) * 12;
-    const uint64_t work_rows = (uint64_t(a->nrows) + 2) * 96;
-    const uint64_t reserve = 2ull << 30;
-    // HBM the pool already holds is reusable by this pass
-    const uint64_t held = ctx->keys.cap + ctx->vals.cap + ctx->ccol.cap + ctx->cval.cap +
-                          ctx->skeys.cap + ctx->svals.cap;
-    const uint64_t avail = free_b + held;
-    uint64_t budget = avail > inputs + work_rows + reserve ? avail - inputs - work_rows - reserve : 0;
-    // 12 B tuples + a C upper bound of 12 B per tuple, plus run plans / scratch slack
-    const uint64_t per_tuple = 40;  // tuples 12 + C bound 12 + heavy scratch 12 + headroom
-    uint64_t max_tuples = std::max<uint64_t>(budget / per_tuple, 1);
-    if (cfg.reserved[0]) max_tuples = std::min<uint64_t>(max_tuples, cfg.reserved[0]);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, st);
-    rc = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st);
-    if (!rc) rc = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st);
-    if (!rc) rc = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st);
-    if (!rc) rc = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st);
-    if (!rc) rc = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st);
-    cudaEventRecord(e1, st);
-    if (!rc) {
-        pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
-                        static_cast<const uint32_t*>(ctx->in_a_idx.p),
-                        static_cast<const double*>(ctx->in_a_val.p)};
-        pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
-                        static_cast<const uint32_t*>(ctx->in_b_idx.p),
-                        static_cast<const double*>(ctx->in_b_val.p)};
+    int count = 0, base = 0;
+    CUDA_TRY(cudaGetDeviceCount(&count));
+    CUDA_TRY(cudaGetDevice(&base));
+    const int G = cfg.ngpus < 0 ? count : std::max(1, cfg.ngpus);
+    if (G > 1 && base + G > count && !(cfg.flags & PBG_FLAG_WRAP_DEVICES))
+        return fail(PBG_ERR_ARG, "ngpus " + std::to_string(G) + " from device " + std::to_string(base) +
+                                     " exceeds the " + std::to_string(count) + " visible devices");
+    if (G > 1) {
+        // ---- multi-device: one flop-balanced row band per device (§8e) ----
+        std::vector<DevJob> jobs(G);
+        for (int t = 0; t < G; ++t) {
+            jobs[t].device = (base + t) % count;
+            jobs[t].index = static_cast<uint32_t>(t);
+        }
+        std::vector<std::thread> th;
+        for (int t = 0; t < G; ++t)
+            th.emplace_back([&, t] {
+                jobs[t].rc = device_job(jobs[t], *a, *b, cfg, static_cast<uint32_t>(G));
+                if (jobs[t].rc) jobs[t].err = g_err;  // g_err is thread-local
+            });
+        for (auto& x : th) x.join();
+        auto* h = new pbg_handle;
+        h->cfg = cfg;
+        h->banded = true;
+        h->m = a->nrows;
+        h->k = a->ncols;
+        h->ctx = jobs[0].ctx;
+        for (int t = 1; t < G; ++t)
+            if (jobs[t].ctx) h->extra.push_back(jobs[t].ctx);
+        int first_rc = 0;
+        std::string first_err;
+        pbg_report tot{};
+        double tmax = 0, tmin = 1e300;
+        for (auto& j : jobs) {
+            if (j.rc && !first_rc) {
+                first_rc = j.rc;
+                first_err = j.err;
+            }
+            for (auto& p : j.parts) h->parts.push_back(std::move(p));
+            add_report(tot, j.rep);
+            tot.nrounds = std::max(tot.nrounds, j.rep.nrounds);
+            tmax = std::max(tmax, j.rep.t_total);
+            tmin = std::min(tmin, j.rep.t_total);
+            h->t_h2d = std::max(h->t_h2d, j.t_h2d);
+        }
+        if (first_rc) {
+            pbg_release(h);
+            return fail(first_rc, first_err);
+        }
+        tot.t_total = tmax;  // the devices run concurrently
+        tot.t_device_max = tmax;
+        tot.t_device_min = tmin;
+        tot.ngpus = static_cast<uint32_t>(G);
+        tot.nnz_a = a->nnz;
+        tot.nnz_b = b->nnz;
+        tot.nbins = reference_nbins(cfg, tot.flop, a->nrows, h->ctx->col_bits);
+        for (auto& p : h->parts) h->nnz_c += p.nnz;
+        h->rep = tot;
+        if (tot.merged_total != h->nnz_c) {
+            pbg_release(h);
+            return fail(PBG_ERR_INTERNAL, "band totals disagree with the assembled product");
+        }
+        if (nnz_c) *nnz_c = h->nnz_c;
+        *out = h;
+        return PBG_OK;
+    }
+    return with_handle(cfg, out, [&](pbg_handle* h) -> int {
+        pbg_context* ctx = h->ctx;
+        cudaStream_t st = nullptr;
+        // ---- memory plan: one pass, or bounded-memory rounds over row bands ----
+        // The pass starts optimistically; its symbolic phase knows flop exactly
+        // and stops before any tuple storage is allocated when it does not fit.
+        uint64_t max_tuples = 1;
+        int r = tuple_budget(ctx, *a, *b, cfg, &max_tuples);
+        if (r) return r;
+        ScopedEvents ev;
+        CUDA_TRY(cudaEventRecord(ev[0], st));
+        if ((r = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st)) ||
+            (r = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st)) ||
+            (r = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st)) ||
+            (r = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st)) ||
+            (r = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st)) ||
+            (r = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st)))
+            return r;
+        CUDA_TRY(cudaEventRecord(ev[1], st));
+        const pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                              static_cast<const double*>(ctx->in_a_val.p)};
+        const pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                              static_cast<const double*>(ctx->in_b_val.p)};
         ctx->round_tuples = max_tuples;
-        rc = run_pipeline(ctx, da, db, cfg, st);
+        r = run_pipeline(ctx, da, db, cfg, st);
         ctx->round_tuples = 0;
-    }
-    float ms = 0;
-    if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
-        h->t_h2d = ms * 1e-3;
-    if (rc == kNeedsRounds) {
-        const uint64_t flop = ctx->flop;
-        const uint32_t nrounds = static_cast<uint32_t>((flop + max_tuples - 1) / max_tuples);
-        rc = multiply_in_rounds(h, *a, *b, cfg, nrounds, st);
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (rc) {
+        float ms = 0;
+        if (cudaEventSynchronize(ev[1]) == cudaSuccess && cudaEventElapsedTime(&ms, ev[0], ev[1]) == cudaSuccess)
+            h->t_h2d = ms * 1e-3;
+        if (r == kNeedsRounds) {
+            // bounded-memory rounds: flop-balanced row bands cut and extracted
+            // on the device, each band's CSR copied to host memory
+            uint64_t flop = 0;
+            if ((r = dev_row_prefix(ctx, da, db, st, &flop))) return r;
+            const uint32_t R = static_cast<uint32_t>((flop + max_tuples - 1) / max_tuples);
+            h->banded = true;
+            h->m = a->nrows;
+            h->k = a->ncols;
+            pbg_report tot{};
+            if ((r = device_rounds(ctx, da, db, 0, a->nrows, R, cfg, st, false, h->parts, tot))) return r;
+            for (auto& p : h->parts) h->nnz_c += p.nnz;
+            tot.ngpus = 1;
+            tot.t_device_max = tot.t_device_min = tot.t_total;
+            tot.nnz_a = a->nnz;
+            tot.nnz_b = b->nnz;
+            tot.nbins = reference_nbins(cfg, flop, a->nrows, ctx->col_bits);
+            h->rep = tot;
+            if (tot.flop != flop || tot.merged_total != h->nnz_c)
+                return fail(PBG_ERR_INTERNAL, "round totals disagree with the full product");
+        } else if (r) {
+            return r;
+        }
+        if (nnz_c) *nnz_c = h->banded ? h->nnz_c : ctx->nnz_c;
+        return PBG_OK;
+    });
+}
+
+int pbg_multiply_into(const pbg_csx_view* a, const pbg_csx_view* b, const pbg_config* cfg_in,
+                      uint64_t* rowptr, uint32_t* colids, double* values, uint64_t cap,
+                      uint64_t* nnz_c, pbg_report* rep) {
+    if (!rowptr || (cap && (!colids || !values))) return fail(PBG_ERR_ARG, "output arrays are null");
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    int rc;
+    if (cfg.ngpus > 1 || cfg.ngpus < 0) {
+        // several devices: their bands stay on the devices, then one
+        // concurrent copy per device at the offsets of the bands before it
+        pbg_handle* h = nullptr;
+        uint64_t nnz = 0;
+        if ((rc = pbg_multiply_begin(a, b, &cfg, &h, &nnz))) return rc;
+        if (nnz > cap) {
+            pbg_release(h);
+            if (nnz_c) *nnz_c = nnz;
+            return fail(PBG_ERR_ARG, "output capacity " + std::to_string(cap) + " below nnz(C) " +
+                                         std::to_string(nnz));
+        }
+        rc = pbg_multiply_fetch(h, rowptr, colids, values, rep);
         pbg_release(h);
+        if (!rc && nnz_c) *nnz_c = nnz;
         return rc;
     }
-    if (nnz_c) *nnz_c = h->rounds ? h->colids.size() : ctx->nnz_c;
-    *out = h;
-    return PBG_OK;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    if (a->ncols != b->nrows)
+        return fail(PBG_ERR_DIM, "dimension mismatch: " + std::to_string(a->nrows) + "x" +
+                                     std::to_string(a->ncols) + " * " + std::to_string(b->nrows) +
+                                     "x" + std::to_string(b->ncols));
+    if ((rc = validate_cfg(cfg))) return rc;
+    if ((rc = set_device(cfg.device))) return rc;
+    pbg_handle* hh = nullptr;
+    rc = with_handle(cfg, &hh, [&](pbg_handle* h) -> int {
+        pbg_context* ctx = h->ctx;
+        cudaStream_t st = nullptr;  // compute
+        OwnStream cs;               // copies out
+        CUDA_TRY(cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking));
+        uint64_t max_tuples = 1;
+        int r = tuple_budget(ctx, *a, *b, cfg, &max_tuples);
+        if (r) return r;
+        max_tuples = std::max<uint64_t>(1, max_tuples * 40 / 52);  // + a second C (12 B per tuple)
+        const auto t0 = std::chrono::steady_clock::now();
+        if ((r = copy_in(ctx->in_a_ptr, a->ptr, (uint64_t(a->ncols) + 1) * 8, st)) ||
+            (r = copy_in(ctx->in_a_idx, a->idx, a->nnz * 4, st)) ||
+            (r = copy_in(ctx->in_a_val, a->val, a->nnz * 8, st)) ||
+            (r = copy_in(ctx->in_b_ptr, b->ptr, (uint64_t(b->nrows) + 1) * 8, st)) ||
+            (r = copy_in(ctx->in_b_idx, b->idx, b->nnz * 4, st)) ||
+            (r = copy_in(ctx->in_b_val, b->val, b->nnz * 8, st)))
+            return r;
+        const pbg_csx_view da{a->nrows, a->ncols, a->nnz, static_cast<const uint64_t*>(ctx->in_a_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_a_idx.p),
+                              static_cast<const double*>(ctx->in_a_val.p)};
+        const pbg_csx_view db{b->nrows, b->ncols, b->nnz, static_cast<const uint64_t*>(ctx->in_b_ptr.p),
+                              static_cast<const uint32_t*>(ctx->in_b_idx.p),
+                              static_cast<const double*>(ctx->in_b_val.p)};
+        uint64_t flop = 0;
+        if ((r = dev_row_prefix(ctx, da, db, st, &flop))) return r;
+        const uint32_t R = static_cast<uint32_t>(std::max<uint64_t>(1, (flop + max_tuples - 1) / max_tuples));
+        std::vector<uint32_t> cuts(R + 1);
+        if ((r = dev_cuts(ctx, 0, a->nrows, R, st, cuts.data(), nullptr))) return r;
+        pbg_report tot{};
+        uint64_t base = 0;
+        ScopedEvents ev;  // ev[0]/ev[1]: copies of the C in buffer set 0/1 done
+        bool pending[2] = {false, false};
+        int set = 0;  // buffer set the context's C arrays are currently
+        for (uint32_t q = 0; q < R; ++q) {
+            const uint32_t r0 = cuts[q], r1 = cuts[q + 1];
+            if (r0 == r1) continue;
+            // the copy that last read this buffer set has finished
+            if (pending[set]) CUDA_TRY(cudaStreamWaitEvent(st, ev[set], 0));
+            if ((r = dev_band_multiply(ctx, da, db, r0, r1, cfg, st))) return r;
+            add_report(tot, ctx->rep);
+            const uint64_t bn = ctx->nnz_c, n = r1 - r0;
+            if (base + bn > cap) {
+                CUDA_TRY(cudaDeviceSynchronize());
+                if (nnz_c) *nnz_c = base + bn;
+                return fail(PBG_ERR_ARG, "output capacity " + std::to_string(cap) + " below nnz(C)");
+            }
+            // band -> caller arrays on the copy stream, while the next band computes
+            if (n) pbg::k_add_base<<<blocks_for(n, 256), 256, 0, st>>>(static_cast<uint64_t*>(ctx->rowptr.p), n, base);
+            CUDA_TRY(cudaEventRecord(ev[2], st));
+            CUDA_TRY(cudaStreamWaitEvent(cs.s, ev[2], 0));
+            CUDA_TRY(cudaMemcpyAsync(rowptr + r0, ctx->rowptr.p, n * 8, cudaMemcpyDeviceToHost, cs.s));
+            if (bn) {
+                CUDA_TRY(cudaMemcpyAsync(colids + base, ctx->ccol.p, bn * 4, cudaMemcpyDeviceToHost, cs.s));
+                CUDA_TRY(cudaMemcpyAsync(values + base, ctx->cval.p, bn * 8, cudaMemcpyDeviceToHost, cs.s));
+            }
+            CUDA_TRY(cudaEventRecord(ev[set], cs.s));
+            pending[set] = true;
+            base += bn;
+            // the next band writes the other buffer set
+            std::swap(ctx->rowptr, ctx->alt_rowptr);
+            std::swap(ctx->ccol, ctx->alt_ccol);
+            std::swap(ctx->cval, ctx->alt_cval);
+            set ^= 1;
+        }
+        CUDA_TRY(cudaStreamSynchronize(cs.s));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (set) {  // leave the context's buffers as they were
+            std::swap(ctx->rowptr, ctx->alt_rowptr);
+            std::swap(ctx->ccol, ctx->alt_ccol);
+            std::swap(ctx->cval, ctx->alt_cval);
+        }
+        ctx->have_result = false;  // its C arrays no longer hold one product
+        rowptr[a->nrows] = base;
+        if (tot.flop != flop || tot.merged_total != base)
+            return fail(PBG_ERR_INTERNAL, "round totals disagree with the full product");
+        tot.ngpus = 1;
+        tot.nrounds = R;
+        tot.t_device_max = tot.t_device_min = tot.t_total;
+        tot.nnz_a = a->nnz;
+        tot.nnz_b = b->nnz;
+        tot.nnz_c = base;
+        tot.nbins = reference_nbins(cfg, flop, a->nrows, ctx->col_bits);
+        tot.t_d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (rep) *rep = tot;
+        if (nnz_c) *nnz_c = base;
+        return PBG_OK;
+    });
+    if (hh) pbg_release(hh);
+    return rc;
 }
 
 int pbg_coo_convert_begin(uint32_t nrows, uint32_t ncols, uint64_t nnz, const uint32_t* rows,
@@ -1328,7 +1681,7 @@ int hash_body(pbg_handle* h, const pbg_csx_view* a, const pbg_csx_view* b, uint6
     CUDA_TRY(cudaMemsetAsync(count, 0, (nbc + 1) * 8, st));
     using Small = HashSmem<128, 2048, 1024>;
     using Big = HashSmem<512, 8192, 4096>;
-    static bool attr[64] = {};
+    static std::atomic<bool> attr[64] = {};
     if (!attr[ctx->device & 63]) {
         CUDA_TRY(cudaFuncSetAttribute(k_hash_cols<128, 2048, 1024>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Small)));
@@ -1338,7 +1691,7 @@ int hash_body(pbg_handle* h, const pbg_csx_view* a, const pbg_csx_view* b, uint6
     }
     using W512 = HashWarpSmem<512, 8>;
     using W1K = HashWarpSmem<1024, 8>;
-    static bool wattr[64] = {};
+    static std::atomic<bool> wattr[64] = {};
     if (!wattr[ctx->device & 63]) {
         CUDA_TRY(cudaFuncSetAttribute(k_hash_warp<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)sizeof(W512)));
@@ -1512,34 +1865,88 @@ int pbg_generate_begin(int kind, int scale, uint32_t ef, uint64_t seed, uint64_t
     });
 }
 
+// Band parts into the caller's arrays: part i's rows land at its rows, its
+// entries after the entries of parts 0..i-1. Device-resident parts (one per
+// device) are copied concurrently, one host thread per part.
+int fetch_parts(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values) {
+    const size_t np = h->parts.size();
+    std::vector<uint64_t> base(np + 1, 0);
+    for (size_t i = 0; i < np; ++i) base[i + 1] = base[i] + h->parts[i].nnz;
+    std::vector<int> rcs(np, 0);
+    std::vector<std::string> errs(np);
+    auto one = [&](size_t i) -> int {
+        BandPart& p = h->parts[i];
+        const uint64_t n = p.r1 - p.r0, bs = base[i];
+        if (!p.ctx) {
+            if (rowptr)
+                for (uint64_t r = 0; r < n; ++r) rowptr[p.r0 + r] = bs + p.rowptr[r];
+            if (colids && p.nnz) std::memcpy(colids + bs, p.colids.data(), p.nnz * 4);
+            if (values && p.nnz) std::memcpy(values + bs, p.values.data(), p.nnz * 8);
+            return PBG_OK;
+        }
+        pbg_context* ctx = p.ctx;
+        CUDA_TRY(cudaSetDevice(ctx->device));
+        OwnStream os;
+        CUDA_TRY(cudaStreamCreateWithFlags(&os.s, cudaStreamNonBlocking));
+        if (rowptr && n) {
+            pbg::k_add_base<<<blocks_for(n, 256), 256, 0, os.s>>>(static_cast<uint64_t*>(ctx->rowptr.p), n, bs);
+            CUDA_TRY(cudaMemcpyAsync(rowptr + p.r0, ctx->rowptr.p, n * 8, cudaMemcpyDeviceToHost, os.s));
+            pbg::k_add_base<<<blocks_for(n, 256), 256, 0, os.s>>>(static_cast<uint64_t*>(ctx->rowptr.p), n, 0 - bs);
+        }
+        if (colids && p.nnz)
+            CUDA_TRY(cudaMemcpyAsync(colids + bs, ctx->ccol.p, p.nnz * 4, cudaMemcpyDeviceToHost, os.s));
+        if (values && p.nnz)
+            CUDA_TRY(cudaMemcpyAsync(values + bs, ctx->cval.p, p.nnz * 8, cudaMemcpyDeviceToHost, os.s));
+        CUDA_TRY(cudaStreamSynchronize(os.s));
+        CUDA_TRY(cudaGetLastError());
+        return PBG_OK;
+    };
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < np; ++i) {
+        if (h->parts[i].ctx) {
+            th.emplace_back([&, i] {
+                rcs[i] = one(i);
+                if (rcs[i]) errs[i] = g_err;
+            });
+        } else {
+            rcs[i] = one(i);
+        }
+    }
+    for (auto& x : th) x.join();
+    for (size_t i = 0; i < np; ++i)
+        if (rcs[i]) return fail(rcs[i], errs[i]);
+    if (rowptr) rowptr[h->m] = base[np];
+    return PBG_OK;
+}
+
 int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double* values,
                        pbg_report* rep) {
     if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");
-    if (h->rounds) {
-        if (rowptr) std::memcpy(rowptr, h->rowptr.data(), h->rowptr.size() * 8);
-        if (colids) std::memcpy(colids, h->colids.data(), h->colids.size() * 4);
-        if (values) std::memcpy(values, h->values.data(), h->values.size() * 8);
-        if (rep) *rep = h->rep;
+    if (h->banded) {
+        const auto t0 = std::chrono::steady_clock::now();
+        int rc = fetch_parts(h, rowptr, colids, values);
+        if (rc) return rc;
+        if (rep) {
+            *rep = h->rep;
+            rep->t_h2d = h->t_h2d;
+            rep->t_d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
         return PBG_OK;
     }
     if (!h->ctx->have_result) return fail(PBG_ERR_ARG, "invalid handle");
     pbg_context* ctx = h->ctx;
     CUDA_TRY(cudaSetDevice(ctx->device));
-    cudaEvent_t e0, e1;
-    CUDA_TRY(cudaEventCreate(&e0));
-    CUDA_TRY(cudaEventCreate(&e1));
-    cudaEventRecord(e0, nullptr);
+    ScopedEvents ev;
+    cudaEventRecord(ev[0], nullptr);
     if (rowptr) CUDA_TRY(cudaMemcpyAsync(rowptr, ctx->rowptr.p, (ctx->m + 1) * 8, cudaMemcpyDeviceToHost, nullptr));
     if (colids && ctx->nnz_c)
         CUDA_TRY(cudaMemcpyAsync(colids, ctx->ccol.p, ctx->nnz_c * 4, cudaMemcpyDeviceToHost, nullptr));
     if (values && ctx->nnz_c)
         CUDA_TRY(cudaMemcpyAsync(values, ctx->cval.p, ctx->nnz_c * 8, cudaMemcpyDeviceToHost, nullptr));
-    cudaEventRecord(e1, nullptr);
-    CUDA_TRY(cudaEventSynchronize(e1));
+    cudaEventRecord(ev[1], nullptr);
+    CUDA_TRY(cudaEventSynchronize(ev[1]));
     float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
     if (rep) {
         *rep = ctx->rep;
         rep->t_h2d = h->t_h2d;
@@ -1551,16 +1958,86 @@ int pbg_multiply_fetch(pbg_handle* h, uint64_t* rowptr, uint32_t* colids, double
 int pbg_symbolic_fetch(pbg_handle* h, uint64_t* per_column_flop, uint64_t* per_bin_flop,
                        uint32_t* bin_row_starts) {
     if (!h || !h->ctx) return fail(PBG_ERR_ARG, "invalid handle");
-    if (h->rounds)
-        return reference_layout(h->cfg, h->rep.nbins, h->row_flop, h->col_flop, per_column_flop,
-                                per_bin_flop, bin_row_starts, h->rep.flop, h->ctx->col_bits);
-    return pbg_context_symbolic(h->ctx, &h->cfg, per_column_flop, per_bin_flop, bin_row_starts);
+    if (!h->banded)
+        return pbg_context_symbolic(h->ctx, &h->cfg, per_column_flop, per_bin_flop, bin_row_starts);
+    // banded: the whole product's row / column flop were computed on the
+    // device of band 0 (dev_row_prefix)
+    pbg_context* ctx = h->ctx;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    const uint64_t m = h->m, k = h->k;
+    std::vector<uint64_t> off(m + 1), rf(m), cf(k);
+    CUDA_TRY(cudaMemcpy(off.data(), ctx->bd_rowoff.p, (m + 1) * 8, cudaMemcpyDeviceToHost));
+    if (k) CUDA_TRY(cudaMemcpy(cf.data(), ctx->bd_colflop.p, k * 8, cudaMemcpyDeviceToHost));
+    for (uint64_t r = 0; r < m; ++r) rf[r] = off[r + 1] - off[r];
+    return reference_layout(h->cfg, h->rep.nbins, rf, cf, per_column_flop, per_bin_flop,
+                            bin_row_starts, h->rep.flop, h->ctx->col_bits);
 }
 
 void pbg_release(pbg_handle* h) {
     if (!h) return;
     if (h->ctx) pool_put(h->ctx);
+    for (pbg_context* c : h->extra) pool_put(c);
     delete h;
+}
+
+int pbg_band_cuts_device(pbg_context* ctx, const pbg_csx_view* a, const pbg_csx_view* b,
+                         uint32_t nbands, void* stream, uint32_t* cuts, uint64_t* flop) {
+    if (!ctx || !cuts) return fail(PBG_ERR_ARG, "context / cuts is null");
+    if (nbands == 0) return fail(PBG_ERR_ARG, "nbands must be positive");
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    if (a->ncols != b->nrows) return fail(PBG_ERR_DIM, "dimension mismatch");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t f = 0;
+    if ((rc = dev_row_prefix(ctx, *a, *b, st, &f))) return rc;
+    if ((rc = dev_cuts(ctx, 0, a->nrows, nbands, st, cuts, nullptr))) return rc;
+    if (flop) *flop = f;
+    return PBG_OK;
+}
+
+int pbg_multiply_device_band(pbg_context* ctx, const pbg_csx_view* a, const pbg_csx_view* b,
+                             uint32_t r0, uint32_t r1, const pbg_config* cfg_in, void* stream,
+                             uint64_t* nnz_c, pbg_report* rep) {
+    if (!ctx) return fail(PBG_ERR_ARG, "context is null");
+    int rc;
+    if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
+    if (a->ncols != b->nrows) return fail(PBG_ERR_DIM, "dimension mismatch");
+    if (r0 > r1 || r1 > a->nrows) return fail(PBG_ERR_ARG, "row band outside A");
+    pbg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pbg_default_config(&cfg);
+    if ((rc = validate_cfg(cfg))) return rc;
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    if ((rc = dev_band_multiply(ctx, *a, *b, r0, r1, cfg, static_cast<cudaStream_t>(stream)))) return rc;
+    if (nnz_c) *nnz_c = ctx->nnz_c;
+    if (rep) *rep = ctx->rep;
+    return PBG_OK;
+}
+
+int pbg_context_checksum(pbg_context* ctx, uint64_t row_base, void* stream, uint64_t* out,
+                         double* vsum) {
+    if (!ctx || !ctx->have_result || !out) return fail(PBG_ERR_ARG, "no product in this context");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc;
+    if ((rc = grow(ctx->ck, 64))) return rc;
+    auto* ck = static_cast<unsigned long long*>(ctx->ck.p);
+    CUDA_TRY(cudaMemsetAsync(ck, 0, 32, st));
+    const uint64_t m = ctx->m;
+    if (m)
+        pbg::k_csr_checksum<<<std::min<unsigned>(blocks_for(m, 256), 8 * ctx->num_sms), 256, 0, st>>>(
+            static_cast<const uint64_t*>(ctx->rowptr.p), static_cast<const uint32_t*>(ctx->ccol.p),
+            static_cast<const double*>(ctx->cval.p), m, row_base, ck, reinterpret_cast<double*>(ck + 3));
+    unsigned long long hs[4];
+    CUDA_TRY(cudaMemcpyAsync(hs, ck, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    out[0] = hs[0];
+    out[1] = hs[1];
+    out[2] = hs[2];
+    if (vsum) std::memcpy(vsum, &hs[3], 8);
+    return PBG_OK;
 }
 
 }  // extern "C"

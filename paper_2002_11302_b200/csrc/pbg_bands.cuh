@@ -1,0 +1,195 @@
+// pbg_bands.cuh — output row bands on the device.
+//
+// C(r0:r1, :) = A(r0:r1, :) · B, so a flop-balanced row band of A is a unit
+// of work that needs nothing from the other bands: the multi-GPU split (one
+// band per device) and the bounded-memory rounds (bands one after another
+// on a device) are both built from the kernels here, with no host pass over
+// the matrices.
+//
+//   k_cut_search  flop-balanced cuts from the row-flop prefix of symbolic
+//                 (the rule of the reference's balanced_starts,
+//                 pb_spgemm.cpp:58-82: cut j sits after the first row whose
+//                 inclusive flop prefix reaches j/G of the total)
+//   k_slab_count / k_slab_copy
+//                 the CSC row slab A(r0:r1, :) with rows renumbered from 0
+//                 (stable inside every column; long columns are walked by
+//                 the whole warp, so RMAT hub columns do not serialise)
+//   k_csr_checksum
+//                 nnz, row-count and column-id hashes and the value sum of a
+//                 CSR band: the checksum-and-discard mode of products whose C
+//                 does not fit anywhere (C5b), and a cheap band identity check
+//   k_add_base    rowptr of a band shifted to its place in the global CSR
+#pragma once
+
+#include <cstdint>
+
+#include "pbg_device.cuh"
+
+namespace pbg {
+
+// Cuts of the rows [lo, hi) into g flop-balanced bands: cuts[0] = lo,
+// cuts[g] = hi, and for 0 < j < g the smallest t in (lo, hi] with
+// (row_off[t] - row_off[lo]) * g >= (row_off[hi] - row_off[lo]) * j, i.e. the
+// row after the first one whose inclusive flop prefix reaches j/g of the
+// range (row_off = exclusive row-flop prefix). 128-bit products: exact.
+// off[j] = row_off[cuts[j]] (the flop prefix at every cut).
+__global__ void k_cut_search(const uint64_t* __restrict__ row_off, uint32_t lo, uint32_t hi,
+                             uint32_t g, uint32_t* cuts, uint64_t* off) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > g) return;
+    uint32_t c;
+    if (j == 0 || lo == hi) {
+        c = j == g ? hi : lo;
+    } else if (j == g) {
+        c = hi;
+    } else {
+        const uint64_t base = row_off[lo];
+        const unsigned __int128 target = static_cast<unsigned __int128>(row_off[hi] - base) * j;
+        uint64_t a = uint64_t(lo) + 1, b = hi;
+        while (a < b) {
+            const uint64_t mid = a + (b - a) / 2;
+            if (static_cast<unsigned __int128>(row_off[mid] - base) * g >= target) b = mid;
+            else a = mid + 1;
+        }
+        c = static_cast<uint32_t>(a);
+    }
+    cuts[j] = c;
+    off[j] = row_off[c];
+}
+
+// Per-column flop nnz(A(:, i)) * nnz(B(i, :)) (the reference's
+// per_column_flop, pb_spgemm.cpp:93-101).
+__global__ void k_colflop_each(const uint64_t* __restrict__ a_colptr,
+                               const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < k) out[i] = (a_colptr[i + 1] - a_colptr[i]) * (b_rowptr[i + 1] - b_rowptr[i]);
+}
+
+constexpr uint64_t SLAB_LONG = 64;  // columns longer than this are walked by a warp
+
+// cnt[j] = #{p in column j : r0 <= rowids[p] < r1}
+__global__ void k_slab_count(const uint64_t* __restrict__ a_colptr,
+                             const uint32_t* __restrict__ a_rowids, uint64_t k, uint32_t r0,
+                             uint32_t r1, uint64_t* cnt) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t p0 = 0, p1 = 0;
+    if (j < k) {
+        p0 = a_colptr[j];
+        p1 = a_colptr[j + 1];
+    }
+    const bool longcol = p1 - p0 > SLAB_LONG;
+    uint64_t c = 0;
+    if (!longcol)
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint32_t r = a_rowids[p];
+            c += r >= r0 && r < r1;
+        }
+    uint32_t lm = __ballot_sync(FULL, longcol);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint64_t q0 = __shfl_sync(FULL, p0, src), q1 = __shfl_sync(FULL, p1, src);
+        uint64_t s = 0;
+        for (uint64_t p = q0 + lane; p < q1; p += 32) {
+            const uint32_t r = a_rowids[p];
+            s += r >= r0 && r < r1;
+        }
+        s = warp_sum(s);
+        if (lane == src) c = s;
+    }
+    if (j < k) cnt[j] = c;
+}
+
+// The slab's rowids (renumbered, r - r0) and values at the scanned column
+// starts, in column order (stable).
+__global__ void k_slab_copy(const uint64_t* __restrict__ a_colptr,
+                            const uint32_t* __restrict__ a_rowids,
+                            const double* __restrict__ a_vals, uint64_t k, uint32_t r0,
+                            uint32_t r1, const uint64_t* __restrict__ s_colptr,
+                            uint32_t* s_rowids, double* s_vals) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    uint64_t p0 = 0, p1 = 0, q = 0;
+    if (j < k) {
+        p0 = a_colptr[j];
+        p1 = a_colptr[j + 1];
+        q = s_colptr[j];
+    }
+    const bool longcol = p1 - p0 > SLAB_LONG;
+    if (!longcol)
+        for (uint64_t p = p0; p < p1; ++p) {
+            const uint32_t r = a_rowids[p];
+            if (r >= r0 && r < r1) {
+                s_rowids[q] = r - r0;
+                s_vals[q] = a_vals[p];
+                ++q;
+            }
+        }
+    uint32_t lm = __ballot_sync(FULL, longcol);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint64_t c0 = __shfl_sync(FULL, p0, src), c1 = __shfl_sync(FULL, p1, src);
+        uint64_t dst = __shfl_sync(FULL, q, src);
+        for (uint64_t base = c0; base < c1; base += 32) {
+            const uint64_t p = base + lane;
+            uint32_t r = 0;
+            bool in = false;
+            if (p < c1) {
+                r = a_rowids[p];
+                in = r >= r0 && r < r1;
+            }
+            const uint32_t m = __ballot_sync(FULL, in);
+            if (in) {
+                const uint64_t at = dst + __popc(m & lanemask_lt());
+                s_rowids[at] = r - r0;
+                s_vals[at] = a_vals[p];
+            }
+            dst += __popc(m);
+        }
+    }
+}
+
+// Band checksum: out[0] += nnz, out[1] += sum over rows of (row count x
+// row hash), out[2] += sum of the mixed (row, col) words — sums, so the
+// checksums of the bands of a product add up to the product's; *vsum += the
+// value sum (f64 atomics: an identity check within rounding, not exact).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_csr_checksum(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ colids,
+                               const double* __restrict__ vals, uint64_t m, uint64_t row_base,
+                               unsigned long long* out, double* vsum) {
+    uint64_t h_rows = 0, h_cols = 0;
+    double vs = 0.0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < m;
+         r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p0 = rowptr[r], p1 = rowptr[r + 1];
+        h_rows += (p1 - p0) * mix64(row_base + r + 1);
+        for (uint64_t p = p0; p < p1; ++p) {
+            h_cols += mix64((static_cast<uint64_t>(row_base + r) << 32) | colids[p]);
+            vs += vals[p];
+        }
+    }
+    h_rows = warp_sum(h_rows);
+    h_cols = warp_sum(h_cols);
+    vs = warp_sum(vs);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[1], static_cast<unsigned long long>(h_rows));
+        atomicAdd(&out[2], static_cast<unsigned long long>(h_cols));
+        atomicAdd(vsum, vs);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&out[0], static_cast<unsigned long long>(rowptr[m] - rowptr[0]));
+}
+
+__global__ void k_add_base(uint64_t* __restrict__ p, uint64_t n, uint64_t base) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] += base;
+}
+
+}  // namespace pbg
