@@ -9,15 +9,21 @@ n=2^20, d=16), the config BASELINE.json quotes its multiply count on.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2]
     python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
 
-N>1 (torchrun), the path shards by output rows with no exchange step:
-  --scaling weak (default): rank r multiplies its own C2-sized row block A_r
-      (the config's generator with seed 1+r) of the row-stacked
-      A = [A_0; ...; A_{N-1}] by the shared B (the seed-1 matrix, built on
-      every rank from the same seed), so per-GPU work is fixed as N grows;
-  --scaling strong: the config's rows are cut into N flop-balanced bands and
-      rank r multiplies its CSC row-slab by all of B (broadcast once over NCCL
-      at setup).
-No collective runs in the timed region; the step time is the max over ranks.
+N>1 (torchrun), the path shards by output rows with no exchange step
+(SURVEY.md §8e):
+  --scaling strong (default): rank 0 builds A, broadcasts A (CSC) and B (CSR)
+      once over NCCL at setup; every rank cuts the rows into N flop-balanced
+      bands on its device (the balanced_starts rule; identical cuts, no
+      exchange), builds its CSC row slab of A on the device, and each step
+      multiplies that slab by all of B. Config 5 (C5a / C5b) is the scaling
+      run of BASELINE.json; C2 at N=1 equals the BENCH line.
+  --scaling weak: rank r multiplies its own C2-sized row block A_r (seed 1+r)
+      by the shared B, so per-GPU work is fixed as N grows.
+A band whose tuples exceed HBM runs as bounded-memory rounds (sub-bands cut
+and sliced on the device inside every step). No collective runs in the timed
+region; the step time is the max over ranks; afterwards an all-gather of the
+band nnz places every band in the global CSR and an order-free checksum of C
+is summed over ranks.
 """
 from __future__ import annotations
 
@@ -282,7 +288,7 @@ def run_reference_arm(args):
         "metric": "SpGEMM mults/sec", "value": res["value"], "unit": "mult/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": data_desc(),
         "config": {"workload": workload_name(args.config), "n": rc.nrows, "nnz_a": rc.nnz_a,
                    "flop": res["flop"], "nnz_c": res["nnz_c"], "model_bytes": b_tot,
@@ -301,16 +307,22 @@ def run_reference_arm(args):
     return 0
 
 
+def host_ram_bytes() -> int:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 0
+
+
 def run_gpu_arm(args):
     global M
     import torch
     import torch.distributed as dist
 
-    from paper_2002_11302_b200 import matrices
-    M = matrices
-
     from paper_2002_11302_b200 import api
+    from paper_2002_11302_b200 import matrices
 
+    M = matrices
     ws, rank, local = dist_env()
     # test hooks: PBG_BENCH_DEVICE pins every rank to one device and
     # PBG_BENCH_BACKEND=gloo replaces NCCL, so the N>1 control flow can be
@@ -318,92 +330,116 @@ def run_gpu_arm(args):
     local = int(os.environ.get("PBG_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("PBG_BENCH_BACKEND", "nccl")
     if ws > 1:
-        backend = os.environ.get("PBG_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-
-    a_csc, a_csr = build_inputs(args.config)
-    n = a_csr.nrows
     weak = ws > 1 and args.scaling == "weak"
-    if weak:
-        # rank r: its own row block A_r of the row-stacked A, times the shared B
-        if rank > 0:
-            a_csc = build_inputs(args.config, seed=1 + rank)[0]
-        rf = M.row_flop(a_csc, a_csr)
-        r0, r1 = 0, n
-        a_band = a_csc
-    else:
-        # row bands (flop-balanced), rank r owns rows [cuts[r], cuts[r+1])
-        rf = M.row_flop(a_csc, a_csr)
-        if ws > 1:
-            cuts = M.band_cuts(rf, ws)
-            r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
-            a_band = M.row_band(a_csc, r0, r1)
+    bdev = dev if backend == "nccl" else torch.device("cpu")  # where collectives' tensors live
+
+    def to_dev(x, dt):
+        return torch.from_numpy(np.ascontiguousarray(x).view(dt)).to(dev)
+
+    # ---- inputs (setup, untimed). strong (default): rank 0 builds A once and
+    # broadcasts A (CSC, for the row slabs) and B (CSR) over NCCL; every rank
+    # then cuts the rows into ws flop-balanced bands ON THE DEVICE (identical
+    # cuts everywhere, no exchange) and takes band `rank`. weak: rank r
+    # multiplies its own A_r (seed 1+r) by the shared B.
+    n = k_a = k_b = 0
+    if weak or ws == 1 or rank == 0:
+        a_csc, a_csr = build_inputs(args.config, seed=1)
+        n, k_a, k_b = a_csc.nrows, a_csc.nnz, a_csr.nnz
+    if ws > 1 and not weak:
+        meta = torch.tensor([n, k_a, a_csr.nnz] if rank == 0 else [0, 0, 0], dtype=torch.int64,
+                            device=bdev)
+        dist.broadcast(meta, 0)
+        n, k_a, k_b = (int(x) for x in meta.tolist())
+        if rank == 0:
+            At = [to_dev(a_csc.colptr, np.int64), to_dev(a_csc.rowids, np.int32),
+                  to_dev(a_csc.values, np.float64)]
+            Bt = [to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
+                  to_dev(a_csr.values, np.float64)]
         else:
-            r0, r1 = 0, n
-            a_band = a_csc
-    nnz_a = a_band.nnz
-    # bounded-memory rounds: a rank whose tuples (+ C upper bound) exceed its
-    # HBM budget multiplies its band as R flop-balanced sub-bands per step
-    band_flop = int(rf[r0:r1].sum())
+            At = [torch.empty(n + 1, dtype=torch.int64, device=dev),
+                  torch.empty(k_a, dtype=torch.int32, device=dev),
+                  torch.empty(k_a, dtype=torch.float64, device=dev)]
+            Bt = [torch.empty(n + 1, dtype=torch.int64, device=dev),
+                  torch.empty(k_b, dtype=torch.int32, device=dev),
+                  torch.empty(k_b, dtype=torch.float64, device=dev)]
+        t0 = time.time()
+        for t in At + Bt:  # NCCL broadcast over NVLink (gloo: through the host)
+            if backend == "nccl":
+                dist.broadcast(t, 0)
+            else:
+                h = t.cpu()
+                dist.broadcast(h, 0)
+                t.copy_(h)
+        torch.cuda.synchronize()
+        t_bcast = time.time() - t0
+    else:
+        if weak and rank > 0:
+            a_csc = build_inputs(args.config, seed=1 + rank)[0]
+        At = [to_dev(a_csc.colptr, np.int64), to_dev(a_csc.rowids, np.int32),
+              to_dev(a_csc.values, np.float64)]
+        Bt = [to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
+              to_dev(a_csr.values, np.float64)]
+        k_a, t_bcast = At[1].numel(), 0.0
+    torch.cuda.synchronize()
+    ctx = api.DeviceContext(local)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    va = api.DeviceContext.view(n, n, *At)
+    vb = api.DeviceContext.view(n, n, *Bt)
+    if ws > 1 and not weak:
+        cuts, _ = ctx.band_cuts(va, vb, ws, sp)
+        r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    else:
+        r0, r1 = 0, n
+    _, band_flop = ctx.band_cuts(va, vb, 1, sp, rows=(r0, r1))
+    # bounded-memory rounds: a band whose tuples (+ C bound) exceed the HBM
+    # budget runs as R flop-balanced sub-bands, cut and sliced on the device
+    # inside every step (as the host path's rounds)
     free_b, _ = torch.cuda.mem_get_info(dev)
-    budget = max(1, int(0.7 * (free_b - 2 * (a_csr.nnz * 12 + a_band.nnz * 12))))
+    budget = max(1, int(0.7 * (free_b - 2 * (k_b * 12 + k_a * 12))))
     per_tuple = 40  # tuples 12 + C bound 12 + heavy-row scratch 12 + grow-only headroom
     if args.max_round_tuples:
         rounds = max(1, -(-band_flop // args.max_round_tuples))
     else:
         rounds = max(1, -(-band_flop * per_tuple // budget))
     if rounds > 1:
-        sub = M.band_cuts(rf[r0:r1], rounds)
-        slabs = [M.row_band(a_band, int(sub[i]), int(sub[i + 1])) for i in range(rounds)]
-        log(f"[bench] rank {rank}: {rounds} bounded-memory rounds of ~{band_flop // rounds} mults")
+        sub, _ = ctx.band_cuts(va, vb, rounds, sp, rows=(r0, r1))
+        sub = [int(x) for x in sub]
+        log(f"[bench] rank {rank}: rows [{r0},{r1}) in {rounds} bounded-memory rounds of "
+            f"~{band_flop // rounds} mults")
+        va_step, slab_keep = None, None
+    elif (r0, r1) != (0, n):
+        slab_keep, va_step = ctx.row_slab(va, r0, r1, sp)  # this rank's row slab of A
     else:
-        slabs = [a_band]
-
-    def to_dev(x, dt):
-        return torch.from_numpy(x.view(dt)).to(dev)
-
-    A_slabs = [(to_dev(s.colptr, np.int64), to_dev(s.rowids, np.int32),
-                to_dev(s.values, np.float64)) for s in slabs]
-    if ws > 1 and not weak:  # B broadcast once from rank 0 over NCCL (setup, untimed)
-        if rank == 0:
-            Bt = [to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
-                  to_dev(a_csr.values, np.float64)]
-        else:
-            Bt = [torch.empty(n + 1, dtype=torch.int64, device=dev),
-                  torch.empty(a_csr.nnz, dtype=torch.int32, device=dev),
-                  torch.empty(a_csr.nnz, dtype=torch.float64, device=dev)]
-        for t in Bt:
-            dist.broadcast(t, 0)
-        B = tuple(Bt)
-    else:
-        B = (to_dev(a_csr.rowptr, np.int64), to_dev(a_csr.colids, np.int32),
-             to_dev(a_csr.values, np.float64))
+        slab_keep, va_step = None, va
     torch.cuda.synchronize()
-
-    ctx = api.DeviceContext(local)
-    vas = [api.DeviceContext.view(s.nrows, s.ncols, *t) for s, t in zip(slabs, A_slabs)]
-    vb = api.DeviceContext.view(a_csr.nrows, a_csr.ncols, *B)
+    cfg = api.PbConfig(device=local)
+    sums_keys = ("flop", "nnz_c", "t_symbolic", "t_expand", "t_sort", "t_total", "t_count",
+                 "t_sortmerge_kernel", "tuples_into_sort", "merged_total")
 
     def one_step():
-        """One multiply of this rank's band (all its rounds); per-phase times summed."""
-        tot = None
-        launches = 0
-        for va in vas:
-            _, rep = ctx.multiply(va, vb, cfg, stream.cuda_stream)
+        """One multiply of this rank's rows (all its rounds); phase times summed."""
+        if rounds == 1:
+            _, rep = ctx.multiply(va_step, vb, cfg, sp)
+            return dict(rep), ctx.launches()
+        tot, launches = None, 0
+        for q in range(rounds):
+            if sub[q] == sub[q + 1]:
+                continue
+            _, rep = ctx.multiply_band(va, vb, sub[q], sub[q + 1], cfg, sp)
             launches += ctx.launches()
             if tot is None:
                 tot = dict(rep)
             else:
-                for key in ("flop", "nnz_c", "t_symbolic", "t_expand", "t_sort", "t_total",
-                            "t_count", "t_sortmerge_kernel", "tuples_into_sort", "merged_total"):
+                for key in sums_keys:
                     tot[key] += rep[key]
         return tot, launches
-    cfg = api.PbConfig(device=local)
-    stream = torch.cuda.current_stream(dev)
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
@@ -436,33 +472,74 @@ def run_gpu_arm(args):
 
     flop_local = step_reps[-1]["flop"]
     nnz_local = step_reps[-1]["nnz_c"]
+    # identity of this rank's product (single round: its C is still in the
+    # context): nnz + order-free hashes, summed over ranks below
+    ck = ctx.checksum(row_base=r0) if rounds == 1 else (nnz_local, 0, 0, 0.0)
     t_sort = statistics.mean(r["t_sortmerge_kernel"] for r in step_reps)
     t_count = statistics.mean(r["t_count"] for r in step_reps)
     t_exp = statistics.mean(r["t_expand"] for r in step_reps)
     t_sym = statistics.mean(r["t_symbolic"] for r in step_reps)
-    stats = torch.tensor([t_local, t_sort, t_exp, t_sym, t_count], dtype=torch.float64, device=dev)
-    sums = torch.tensor([flop_local, nnz_local, a_band.nnz], dtype=torch.float64, device=dev)
-    nnz_a_local = a_band.nnz
+    stats = torch.tensor([t_local, t_sort, t_exp, t_sym, t_count], dtype=torch.float64, device=bdev)
+    sums = torch.tensor([flop_local, nnz_local, slab_keep[1].numel() if slab_keep else k_a],
+                        dtype=torch.float64, device=bdev)
+    # 64-bit order-free hashes as 32-bit halves: int64 sums over ranks cannot overflow
+    hashes = torch.tensor([ck[1] & 0xffffffff, ck[1] >> 32, ck[2] & 0xffffffff, ck[2] >> 32],
+                          dtype=torch.int64, device=bdev)
+    nnz_a_local = slab_keep[1].numel() if slab_keep else k_a
+    all_t = None
     if ws > 1:
+        # per-rank band times and nnz (the band-nnz exchange that places each
+        # band in the global CSR: an all-gather of ws u64)
+        g_t = [torch.zeros(1, dtype=torch.float64, device=bdev) for _ in range(ws)]
+        dist.all_gather(g_t, torch.tensor([t_local], dtype=torch.float64, device=bdev))
+        all_t = [float(x.item()) for x in g_t]
+        g_n = [torch.zeros(1, dtype=torch.int64, device=bdev) for _ in range(ws)]
+        dist.all_gather(g_n, torch.tensor([nnz_local], dtype=torch.int64, device=bdev))
+        band_nnz = [int(x.item()) for x in g_n]
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        dist.all_reduce(hashes, op=dist.ReduceOp.SUM)
+    else:
+        band_nnz = [nnz_local]
     t_step, t_sort_max, t_exp_max, t_sym_max, t_count_max = stats.tolist()
     flop, nnz_c, nnz_a = (int(x) for x in sums.tolist())
 
-    # e2e through the public API with host buffers (pinned), N>1: each rank its band
+    # e2e through the public API with host buffers (pinned): H2D of this
+    # rank's A rows and B, the multiply, D2H of its C rows, every step
     e2e = None
-    if args.e2e_steps > 0 and (rounds > 1 or nnz_local * 12 > 32e9):
+    c_bytes = nnz_local * 12 + (r1 - r0 + 1) * 8
+    if args.e2e_steps > 0 and (nnz_local != band_nnz[rank] or c_bytes > 0.7 * host_ram_bytes()):
         e2e = {"value": None, "unit": "mult/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "note": "skipped: C does not fit pinned host staging for this config"}
+               "note": f"skipped: C ({c_bytes / 1e9:.0f} GB) does not fit host memory; "
+                       "checksum-and-discard mode"}
     elif args.e2e_steps > 0:
-        pin = lambda x: torch.from_numpy(x).pin_memory().numpy()  # noqa: E731
-        ah = M.CscMatrix(a_band.nrows, a_band.ncols, pin(a_band.colptr), pin(a_band.rowids),
-                         pin(a_band.values))
-        bh = M.CsrMatrix(a_csr.nrows, a_csr.ncols, pin(a_csr.rowptr), pin(a_csr.colids),
-                         pin(a_csr.values))
-        out = (torch.empty(a_band.nrows + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64),
-               torch.empty(max(nnz_local, 1), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
-               torch.empty(max(nnz_local, 1), dtype=torch.float64).pin_memory().numpy())
+        if slab_keep is not None:
+            a_band_cp = slab_keep[0].cpu().numpy().view(np.uint64)
+            a_band = M.CscMatrix(r1 - r0, n, a_band_cp, slab_keep[1].cpu().numpy().view(np.uint32),
+                                 slab_keep[2].cpu().numpy())
+        elif (r0, r1) != (0, n):
+            (cp, ri, vv), _ = ctx.row_slab(va, r0, r1, sp)
+            a_band = M.CscMatrix(r1 - r0, n, cp.cpu().numpy().view(np.uint64),
+                                 ri.cpu().numpy().view(np.uint32), vv.cpu().numpy())
+        else:
+            a_band = M.CscMatrix(n, n, At[0].cpu().numpy().view(np.uint64),
+                                 At[1].cpu().numpy().view(np.uint32), At[2].cpu().numpy())
+        b_host = M.CsrMatrix(n, n, Bt[0].cpu().numpy().view(np.uint64),
+                             Bt[1].cpu().numpy().view(np.uint32), Bt[2].cpu().numpy())
+
+        def pinned(x, tdt, dt):
+            t = torch.empty(x.size, dtype=tdt, pin_memory=True)
+            t.numpy().view(dt)[:] = x
+            return t.numpy().view(dt)
+        ah = M.CscMatrix(a_band.nrows, n, pinned(a_band.colptr, torch.int64, np.uint64),
+                         pinned(a_band.rowids, torch.int32, np.uint32),
+                         pinned(a_band.values, torch.float64, np.float64))
+        bh = M.CsrMatrix(n, n, pinned(b_host.rowptr, torch.int64, np.uint64),
+                         pinned(b_host.colids, torch.int32, np.uint32),
+                         pinned(b_host.values, torch.float64, np.float64))
+        out = (torch.empty(a_band.nrows + 1, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64),
+               torch.empty(max(nnz_local, 1), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
+               torch.empty(max(nnz_local, 1), dtype=torch.float64, pin_memory=True).numpy())
         hcfg = api.PbConfig(device=local)
         api.pb_multiply(ah, bh, hcfg, symbolic=False, out=out)  # warm
         if ws > 1:
@@ -471,10 +548,10 @@ def run_gpu_arm(args):
         for _ in range(args.e2e_steps):
             res = api.pb_multiply(ah, bh, hcfg, symbolic=False, out=out)
         te = (time.perf_counter() - t0) / args.e2e_steps
-        h2d = (a_band.colptr.nbytes + a_band.rowids.nbytes + a_band.values.nbytes +
-               a_csr.rowptr.nbytes + a_csr.colids.nbytes + a_csr.values.nbytes)
+        h2d = (ah.colptr.nbytes + ah.rowids.nbytes + ah.values.nbytes + bh.rowptr.nbytes +
+               bh.colids.nbytes + bh.values.nbytes)
         d2h = (a_band.nrows + 1) * 8 + res.c.nnz * 12
-        st = torch.tensor([te, h2d, d2h], dtype=torch.float64, device=dev)
+        st = torch.tensor([te, h2d, d2h], dtype=torch.float64, device=bdev)
         if ws > 1:
             t_max = st[:1].clone()
             dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -482,28 +559,37 @@ def run_gpu_arm(args):
             st[0] = t_max[0]
         te, h2d, d2h = st.tolist()
         e2e = {"value": flop / te, "unit": "mult/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": te * 1e3,
+               "rounds": int(res.report.get("nrounds", 1))}
 
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return 0
 
+    def hsum(i):  # recombine the summed halves of a 64-bit hash (mod 2^64)
+        return (int(hashes[i].item()) + (int(hashes[i + 1].item()) << 32)) % (1 << 64)
+
     peak, peak_src = peak_hbm()
-    b_exp, b_sort, b_tot = model_bytes(nnz_a, a_csr.nnz, flop, nnz_c)
-    # dominant kernel = the longer of expand and sort/merge (rank 0's own band)
-    my_b_exp, my_b_sort, _ = model_bytes(nnz_a_local, a_csr.nnz, flop_local, nnz_local)
+    b_exp, b_sort, b_tot = model_bytes(nnz_a, k_b, flop, nnz_c)
+    # dominant kernel = the longer of expand and sort/merge (rank 0's own band);
+    # the sort/merge phase includes the distinct-count pass that places its output
+    my_b_exp, my_b_sort, _ = model_bytes(nnz_a_local, k_b, flop_local, nnz_local)
+    t_sm_phase = t_sort + t_count
     kern = ("k_sortmerge", my_b_sort, t_sort) if t_sort >= t_exp else ("k_expand", my_b_exp, t_exp)
     achieved = kern[1] / kern[2] / 1e9
     traffic = None
     tf = ROOT / "profiles" / f"traffic_{args.config}.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(kern[0])
+            td = json.loads(tf.read_text())
+            traffic = td.get(kern[0])
+            traffic_src = td.get("source")
         except Exception:
-            traffic = None
+            traffic, traffic_src = None, None
     roofline = {"bound": "hbm", "kernel": kern[0], "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": traffic_src if traffic is not None else None,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": kern[1],
                 "avg_launch_s": kern[2],
@@ -511,37 +597,42 @@ def run_gpu_arm(args):
                     "expand": {"model_bytes": my_b_exp, "s": t_exp,
                                "GBps": my_b_exp / t_exp / 1e9 if t_exp else None,
                                "frac": my_b_exp / t_exp / 1e9 / peak if t_exp else None},
-                    "sort_merge": {"model_bytes": my_b_sort, "s": t_sort,
-                                   "GBps": my_b_sort / t_sort / 1e9 if t_sort else None,
-                                   "frac": my_b_sort / t_sort / 1e9 / peak if t_sort else None},
+                    "sort_merge": {"model_bytes": my_b_sort, "s": t_sm_phase,
+                                   "includes": "k_bincount (distinct count + offsets) + k_sortmerge",
+                                   "GBps": my_b_sort / t_sm_phase / 1e9 if t_sm_phase else None,
+                                   "frac": my_b_sort / t_sm_phase / 1e9 / peak if t_sm_phase else None},
+                    "sortmerge_kernel_alone": {"s": t_sort,
+                                               "frac": my_b_sort / t_sort / 1e9 / peak if t_sort else None},
                     "symbolic_s": t_sym, "bin_count_s": t_count}}
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
             rcfg = reference_config(args.config)
-            res = time_reference(rcfg, 3, 1, args.cpu_budget, os.cpu_count() or 1)
+            res_c = time_reference(rcfg, 3, 1, args.cpu_budget, os.cpu_count() or 1)
             rcfg.close()
-            cpu = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: res_c[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, not required
             cpu = {"value": None, "unit": "mult/s", "cores": 0, "kind": "reference",
                    "sample": f"failed: {e}"}
+    partition = ((f"weak: rank r multiplies its own {args.config}-sized row block A_r (seed 1+r) "
+                  f"of the row-stacked A by the shared B" if weak else
+                  f"strong: {ws} flop-balanced row bands (cut on the device), A and B broadcast "
+                  f"once over {backend} at setup ({t_bcast:.2f} s)")
+                 if ws > 1 else "single GPU")
+    if rounds > 1:
+        partition += f", {rounds} bounded-memory rounds per rank (device-side cuts and slabs)"
     line = {
         "metric": "SpGEMM mults/sec", "value": flop / t_step, "unit": "mult/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True,
-        "scaling": "strong" if (ws > 1 and not weak) else "weak", "vs_baseline": None,
+        "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64",
         "data": data_desc(),
         "config": {"workload": workload_name(args.config),
                    "n": n, "nnz_a": nnz_a, "flop": flop, "nnz_c": nnz_c,
                    "model_bytes": b_tot, "model_GBps": b_tot / t_step / 1e9,
                    "model_frac_of_peak_per_gpu": b_tot / t_step / 1e9 / (peak * ws),
-                   "l2": "inputs+tuples larger than L2 (tuples alone are 12 B x flop)",
-                   "partition": ((f"weak: rank r multiplies its own {args.config}-sized row block "
-                                  f"A_r (seed 1+r) of the row-stacked A by the shared B"
-                                  if weak else f"strong: {ws} flop-balanced row bands")
-                                 if ws > 1 else "single GPU") +
-                     (f", {rounds} bounded-memory rounds per rank" if rounds > 1 else "")},
+                   "l2": L2_NOTE, "partition": partition},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -549,7 +640,12 @@ def run_gpu_arm(args):
         "clocks": clocks,
         "phases_ms": {"symbolic": t_sym_max * 1e3, "expand": t_exp_max * 1e3,
                       "bin_count": t_count_max * 1e3, "sort_merge": t_sort_max * 1e3},
+        "c_checksum": {"nnz": nnz_c, "row_hash": hsum(0), "rowcol_hash": hsum(2)}
+        if rounds == 1 else None,
     }
+    if ws > 1:
+        line["per_rank_ms"] = [t * 1e3 for t in all_t]
+        line["band_nnz"] = band_nnz
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -569,8 +665,10 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=30.0)
     ap.add_argument("--ref-budget", type=float, default=240.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: per-GPU work fixed (weak, default) or total work fixed (strong)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: total work fixed, flop-balanced row bands of one A with A and B "
+                         "broadcast once (strong, default: SURVEY.md §8e) or per-GPU work fixed "
+                         "(weak, opt-in)")
     ap.add_argument("--max-round-tuples", type=int, default=0,
                     help="force bounded-memory rounds of at most this many mults")
     args = ap.parse_args()

@@ -203,13 +203,22 @@ int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg, uint64_t* per_
 uint32_t pbg_context_launches(pbg_context* ctx);
 
 /* ---- row bands on the device (pbg_bands.cuh) ----------- */
-/* Flop-balanced cuts of the rows of C = A*B into nbands bands (device-
- * resident A in CSC, B in CSR): cuts[0] = 0, cuts[nbands] = nrows(A), cut j
- * after the first row whose inclusive flop prefix reaches j/nbands of the
- * total (the reference's balanced_starts rule, pb_spgemm.cpp:58-82). *flop
- * (may be NULL) = flop of the whole product. Host destination for cuts. */
+/* Flop-balanced cuts of rows [r0, r1) of C = A*B into nbands bands
+ * (device-resident A in CSC, B in CSR): cuts[0] = r0, cuts[nbands] = r1,
+ * cut j after the first row whose inclusive flop prefix (from r0) reaches
+ * j/nbands of the range's flop — the reference's balanced_starts rule
+ * (pb_spgemm.cpp:58-82). *flop (may be NULL) = flop of rows [r0, r1).
+ * Host destination for cuts. */
 int pbg_band_cuts_device(pbg_context* ctx, const pbg_csx_view* a_csc, const pbg_csx_view* b_csr,
-                         uint32_t nbands, void* stream, uint32_t* cuts, uint64_t* flop);
+                         uint32_t r0, uint32_t r1, uint32_t nbands, void* stream, uint32_t* cuts,
+                         uint64_t* flop);
+/* The CSC row slab A(r0:r1, :) (rows renumbered from 0) built on the device
+ * into caller device arrays colptr[ncols+1], rowids/values[cap]; with
+ * colptr == NULL only *nnz is returned (size query). §8f f1: a device's row
+ * slab of A without a host pass. */
+int pbg_row_slab_device(pbg_context* ctx, const pbg_csx_view* a_csc, uint32_t r0, uint32_t r1,
+                        void* stream, uint64_t* colptr, uint32_t* rowids, double* values,
+                        uint64_t cap, uint64_t* nnz);
 /* C(r0:r1, :) = A(r0:r1, :) * B for device-resident A (the whole CSC) and B:
  * the row slab of A is extracted on the device, the product has r1 - r0 rows
  * (band-local rowptr) and is read with pbg_context_result like a

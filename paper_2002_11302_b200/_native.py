@@ -81,7 +81,8 @@ PBG_EXPORTS = {
     "pbg_context_result": (C.c_int, [vp, P(vp), P(vp), P(vp)]),
     "pbg_context_symbolic": (C.c_int, [vp, P(Config), vp, vp, vp]),
     "pbg_context_launches": (u32, [vp]),
-    "pbg_band_cuts_device": (C.c_int, [vp, P(CsxView), P(CsxView), u32, vp, vp, P(u64)]),
+    "pbg_band_cuts_device": (C.c_int, [vp, P(CsxView), P(CsxView), u32, u32, u32, vp, vp, P(u64)]),
+    "pbg_row_slab_device": (C.c_int, [vp, P(CsxView), u32, u32, vp, vp, vp, vp, u64, P(u64)]),
     "pbg_multiply_device_band": (C.c_int, [vp, P(CsxView), P(CsxView), u32, u32, P(Config), vp,
                                            P(u64), P(Report)]),
     "pbg_context_checksum": (C.c_int, [vp, u64, vp, vp, P(f64)]),

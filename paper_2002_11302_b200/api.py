@@ -327,17 +327,41 @@ class DeviceContext:
             _raise(rc)
         return nnz.value, rep.as_dict()
 
-    def band_cuts(self, a_view, b_view, nbands: int, stream: int = 0):
-        """Flop-balanced row cuts of A*B into nbands bands, computed on the
-        device (balanced_starts rule, pb_spgemm.cpp:58-82): (cuts, flop)."""
+    def band_cuts(self, a_view, b_view, nbands: int, stream: int = 0, rows=None):
+        """Flop-balanced cuts of rows [r0, r1) (default: all) of A*B into
+        nbands bands, computed on the device (balanced_starts rule,
+        pb_spgemm.cpp:58-82): (cuts, flop of the rows)."""
+        r0, r1 = rows or (0, a_view.nrows)
         cuts = np.zeros(nbands + 1, np.uint32)
         flop = C.c_uint64(0)
-        rc = self._lib.pbg_band_cuts_device(self._ctx, C.byref(a_view), C.byref(b_view), nbands,
-                                            C.c_void_p(stream or None), cuts.ctypes.data,
+        rc = self._lib.pbg_band_cuts_device(self._ctx, C.byref(a_view), C.byref(b_view), r0, r1,
+                                            nbands, C.c_void_p(stream or None), cuts.ctypes.data,
                                             C.byref(flop))
         if rc:
             _raise(rc)
         return cuts, flop.value
+
+    def row_slab(self, a_view, r0: int, r1: int, stream: int = 0):
+        """A(r0:r1, :) as a CSC (rows renumbered) built on the device: torch
+        tensors (colptr int64, rowids int32, values float64) and its view."""
+        import torch
+        nnz = C.c_uint64(0)
+        s = C.c_void_p(stream or None)
+        rc = self._lib.pbg_row_slab_device(self._ctx, C.byref(a_view), r0, r1, s, None, None,
+                                           None, 0, C.byref(nnz))
+        if rc:
+            _raise(rc)
+        dev = torch.device("cuda", self.device)
+        k = nnz.value
+        cp = torch.empty(a_view.ncols + 1, dtype=torch.int64, device=dev)
+        ri = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+        vv = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+        rc = self._lib.pbg_row_slab_device(self._ctx, C.byref(a_view), r0, r1, s, cp.data_ptr(),
+                                           ri.data_ptr(), vv.data_ptr(), k, C.byref(nnz))
+        if rc:
+            _raise(rc)
+        ri, vv = ri[:k], vv[:k]
+        return (cp, ri, vv), self.view(r1 - r0, a_view.ncols, cp, ri, vv)
 
     def multiply_band(self, a_view, b_view, r0: int, r1: int, cfg: PbConfig | None = None,
                       stream: int = 0):

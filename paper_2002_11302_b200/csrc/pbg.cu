@@ -1981,18 +1981,44 @@ void pbg_release(pbg_handle* h) {
 }
 
 int pbg_band_cuts_device(pbg_context* ctx, const pbg_csx_view* a, const pbg_csx_view* b,
-                         uint32_t nbands, void* stream, uint32_t* cuts, uint64_t* flop) {
+                         uint32_t r0, uint32_t r1, uint32_t nbands, void* stream, uint32_t* cuts,
+                         uint64_t* flop) {
     if (!ctx || !cuts) return fail(PBG_ERR_ARG, "context / cuts is null");
     if (nbands == 0) return fail(PBG_ERR_ARG, "nbands must be positive");
     int rc;
     if ((rc = validate_view(a, "A")) || (rc = validate_view(b, "B"))) return rc;
     if (a->ncols != b->nrows) return fail(PBG_ERR_DIM, "dimension mismatch");
+    if (r0 > r1 || r1 > a->nrows) return fail(PBG_ERR_ARG, "row range outside A");
     CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     uint64_t f = 0;
     if ((rc = dev_row_prefix(ctx, *a, *b, st, &f))) return rc;
-    if ((rc = dev_cuts(ctx, 0, a->nrows, nbands, st, cuts, nullptr))) return rc;
-    if (flop) *flop = f;
+    std::vector<uint64_t> off(nbands + 1);
+    if ((rc = dev_cuts(ctx, r0, r1, nbands, st, cuts, off.data()))) return rc;
+    if (flop) *flop = off[nbands] - off[0];
+    return PBG_OK;
+}
+
+int pbg_row_slab_device(pbg_context* ctx, const pbg_csx_view* a, uint32_t r0, uint32_t r1,
+                        void* stream, uint64_t* colptr, uint32_t* rowids, double* values,
+                        uint64_t cap, uint64_t* nnz) {
+    if (!ctx || !nnz) return fail(PBG_ERR_ARG, "context / nnz is null");
+    int rc;
+    if ((rc = validate_view(a, "A"))) return rc;
+    if (r0 > r1 || r1 > a->nrows) return fail(PBG_ERR_ARG, "row range outside A");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pbg_csx_view slab;
+    if ((rc = dev_slab(ctx, *a, r0, r1, st, &slab))) return rc;
+    *nnz = slab.nnz;
+    if (!colptr) return PBG_OK;  // size query
+    if (slab.nnz > cap) return fail(PBG_ERR_ARG, "slab capacity below its nnz");
+    CUDA_TRY(cudaMemcpyAsync(colptr, slab.ptr, (uint64_t(a->ncols) + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    if (slab.nnz) {
+        CUDA_TRY(cudaMemcpyAsync(rowids, slab.idx, slab.nnz * 4, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(values, slab.val, slab.nnz * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
     return PBG_OK;
 }
 

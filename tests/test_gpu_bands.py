@@ -82,14 +82,15 @@ def test_multiply_into_caller_arrays(pinned):
         for mrt in (0, max(one.sym.flop // 6, 1)):
             out = (arr(a.nrows + 1, np.uint64, torch.int64), arr(k + 5, np.uint32, torch.int32),
                    arr(k + 5, np.float64, torch.float64))
-            r = gpu(a, b, max_round_tuples=mrt, out=out)
+            r = api.pb_multiply(a, b, api.PbConfig(device=0, max_round_tuples=mrt), out=out)
             _same(r, one)
             if mrt:
                 assert r.report["nrounds"] >= 6
         small = (np.empty(a.nrows + 1, np.uint64), np.empty(k // 2, np.uint32),
                  np.empty(k // 2, np.float64))
         with pytest.raises(api.DeviceError):
-            gpu(a, b, max_round_tuples=max(one.sym.flop // 4, 1), out=small)
+            api.pb_multiply(a, b, api.PbConfig(device=0, max_round_tuples=max(one.sym.flop // 4, 1)),
+                            out=small)
 
 
 def _upload(a, b):
