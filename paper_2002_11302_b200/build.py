@@ -4,7 +4,10 @@ repo snapshot):
 * ``libpbg.so``      — the sm_100a kernels + C-ABI (include/pbg.h), nvcc;
 * ``libpbg_host.so`` — host input preparation (include/pbg_host.h), g++/OpenMP;
 * ``libspgemm_b200.so`` — the C++ drop-in ``spgemm::pb_multiply`` over the
-  C-ABI (include/spgemm_b200/pb_spgemm.hpp).
+  C-ABI (include/spgemm_b200/pb_spgemm.hpp);
+* ``libpbg_checked.so`` — libpbg with PBG_CHECKED device bounds checks (trap
+  on an out-of-range store index), run by tests/test_gpu_checked.py in place
+  of compute-sanitizer memcheck, which the GPU pool does not run.
 """
 from __future__ import annotations
 
@@ -23,6 +26,7 @@ GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIBPBG = PKG / "libpbg.so"
 LIBHOST = PKG / "libpbg_host.so"
 LIBSHIM = PKG / "libspgemm_b200.so"
+LIBCHECKED = PKG / "libpbg_checked.so"
 
 
 def _newer(target: Path, deps) -> bool:
@@ -37,15 +41,23 @@ def _run(cmd):
     subprocess.run([str(c) for c in cmd], check=True)
 
 
-def build_pbg(force: bool = False) -> Path:
+def _build_cu(target: Path, defines, force: bool) -> Path:
     deps = [CSRC / "pbg.cu", *sorted(CSRC.glob("*.cuh")), INCLUDE / "pbg.h"]
-    if force or not _newer(LIBPBG, deps):
-        tmp = LIBPBG.with_suffix(".so.tmp")
+    if force or not _newer(target, deps):
+        tmp = target.with_suffix(".so.tmp")
         _run([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-Xcompiler", "-Wall", "-shared", "-I", INCLUDE, "-I", CSRC,
+              "-Xcompiler", "-Wall", "-shared", *defines, "-I", INCLUDE, "-I", CSRC,
               "-o", tmp, CSRC / "pbg.cu", "-lcudart"])
-        tmp.replace(LIBPBG)
-    return LIBPBG
+        tmp.replace(target)
+    return target
+
+
+def build_pbg(force: bool = False) -> Path:
+    return _build_cu(LIBPBG, [], force)
+
+
+def build_checked(force: bool = False) -> Path:
+    return _build_cu(LIBCHECKED, ["-DPBG_CHECKED"], force)
 
 
 def build_host(force: bool = False) -> Path:
@@ -71,9 +83,24 @@ def build_shim(force: bool = False) -> Path:
 
 
 def build_all(force: bool = False) -> None:
+    import threading
     build_host(force)
+    # the checked variant compiles alongside the product library
+    errs = []
+    t = threading.Thread(target=lambda: _catch(errs, build_checked, force))
+    t.start()
     build_pbg(force)
+    t.join()
+    if errs:
+        raise errs[0]
     build_shim(force)
+
+
+def _catch(errs, fn, *args):
+    try:
+        fn(*args)
+    except Exception as e:  # re-raised by the caller's thread
+        errs.append(e)
 
 
 if __name__ == "__main__":

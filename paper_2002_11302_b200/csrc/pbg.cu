@@ -55,6 +55,8 @@ struct DevBuf {
     }
 };
 
+size_t pool_trim();
+
 int grow(DevBuf& b, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (b.cap >= bytes) return PBG_OK;
@@ -64,6 +66,11 @@ int grow(DevBuf& b, size_t bytes) {
     if (e != cudaSuccess) {
         cudaGetLastError();
         e = cudaMalloc(&b.p, bytes);
+        if (e != cudaSuccess && pool_trim() > 0) {
+            // idle pooled contexts held the memory: they were released
+            cudaGetLastError();
+            e = cudaMalloc(&b.p, bytes);
+        }
         if (e != cudaSuccess) {
             cudaGetLastError();
             b.p = nullptr;
@@ -462,7 +469,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         const bool pack32 = nb < (1ull << (32 - lbits));
         if ((rc = grow(ctx->row_pack, (m + 1) * (pack32 ? 4 : 8)))) return rc;
         ExpandArgs ea{xa_colptr, xa_rowids, xa_vals, B.ptr, B.idx, B.val, kv, k, chunk_p0, nchunks,
-                      ctx->row_pack.p, lbits, cursor, keys, vals, cb};
+                      ctx->row_pack.p, lbits, cursor, keys, vals, cb, bin_off};
         if (pack32) {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
                                                          static_cast<uint32_t*>(ctx->row_pack.p));
@@ -640,14 +647,16 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         // rows (the stencil, > 512 products per output row on average) and
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
+        static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
         auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
-            static std::atomic<bool> attr_set[2][64] = {};  // [shape][device]
-            if (!attr_set[big_table][ctx->device & 63]) {
+            static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
+            const int shape = (cnt_v1 ? 2 : 0) + (big_table ? 1 : 0);
+            if (!attr_set[shape][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                               100));
-                attr_set[big_table][ctx->device & 63] = true;
+                attr_set[shape][ctx->device & 63] = true;
             }
             int per_sm = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem);
@@ -657,10 +666,16 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                    nt, smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
             return PBG_OK;
         };
-        if (big_table) {
-            if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
+        if (cnt_v1) {
+            if (big_table) {
+                if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
+            } else {
+                if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
+            }
+        } else if (big_table) {
+            if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
         } else {
-            if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
+            if ((rc = launch_count(k_bincount2<512, 16384>, 512, (16384 + 32) * 4))) return rc;
         }
         ++L;
         // wcap can exceed the m-sized status pool: give this scan its own words
@@ -697,6 +712,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         sa.cval = static_cast<double*>(ctx->cval.p);
         sa.rowptr = rowptr;
         sa.m = m;
+        sa.c_cap = flop;
         sa.col_bits = cb;
         sa.merged_total = sc + S_MERGED_TOTAL;
         sa.err = reinterpret_cast<unsigned int*>(sc + S_ERR);
@@ -796,6 +812,25 @@ pbg_context* pool_get(int dev) {
 void pool_put(pbg_context* c) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     g_pool.push_back(c);
+}
+
+// Frees every idle pooled context (their grow-only workspaces can hold many
+// GB after a large product); called when a cudaMalloc fails. Returns how
+// many were freed.
+size_t pool_trim() {
+    std::vector<pbg_context*> idle;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        idle.swap(g_pool);
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (pbg_context* c : idle) {
+        cudaSetDevice(c->device);
+        delete c;
+    }
+    cudaSetDevice(dev);
+    return idle.size();
 }
 
 int make_context(int device, pbg_context** out) {

@@ -4,10 +4,29 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 namespace pbg {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// PBG_CHECKED builds (libpbg_checked.so, tests/test_gpu_checked.py) trap on
+// an out-of-range shared or global index at the kernels' store sites — the
+// stand-in for compute-sanitizer memcheck, which the GPU pool does not run.
+#ifdef PBG_CHECKED
+#define PBG_DCHECK(cond)                                                                  \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("PBG_CHECKED failure %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define PBG_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 // Look-back status word: 2 flag bits + 62-bit value.
 constexpr uint64_t ST_AGG = 1ull << 62;
@@ -155,6 +174,25 @@ __device__ __forceinline__ uint64_t warp_last_le(const uint64_t* __restrict__ a,
         if (step == 1) break;
     }
     return lo;
+}
+
+// ---- shared-memory addresses and cp.async (global -> shared, L1-allocating)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace pbg

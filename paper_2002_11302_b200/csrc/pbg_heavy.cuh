@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, u
             const uint32_t q = tid + j * HV_NT;
             if (q < tl.m) {
                 const uint64_t dst = static_cast<uint64_t>(sm.gb[rb[j] >> 16]) + (rb[j] & 0xffffu);
+                PBG_DCHECK(dst < it.n[tl.i]);
                 DK[dst] = kk[j];
                 DV[dst] = vv[j];
             }
@@ -642,6 +643,175 @@ __global__ void __launch_bounds__(NT) k_bincount(const uint32_t* __restrict__ ke
         }
         par ^= 1;
         __syncthreads();
+    }
+}
+
+// Pipelined count k_bincount2 (same result as k_bincount, C2 1.15 -> 1.01
+// ms). The per-bin critical path of k_bincount held two dependent global
+// round trips (descriptor -> key address -> keys), every thread's probes ran
+// one after another behind a branch per key, and one thread summed the warp
+// counts serially. Here keys (16-byte vector loads) are in flight two bins
+// ahead and descriptors four; a thread issues the first-probe CAS of all its
+// keys back to back (a lane without a key CASes its own dummy slot, so no
+// CAS is predicated) and only collided keys probe on; every key's final slot
+// is reset unconditionally; warp counts go to one shared counter.
+struct CntDesc {
+    uint64_t off;
+    uint64_t merged;  // tuples of a merged item (already distinct), else ~0
+    uint32_t n;       // keys to count (0: merged / above capacity / past the end)
+    uint32_t flags;   // bit0 scratch buffer
+};
+
+__device__ __forceinline__ CntDesc cnt_desc(const WorkBins& w, uint64_t b, uint64_t nw, uint64_t cap) {
+    CntDesc d{0, ~0ull, 0, 0};
+    if (b >= nw) return d;
+    const uint32_t fl = w.flags[b];
+    const uint64_t nn = w.n[b];
+    d.off = w.off[b];
+    d.flags = fl;
+    d.merged = (fl & 2u) ? nn : ~0ull;
+    d.n = ((fl & 2u) || nn > cap) ? 0u : static_cast<uint32_t>(nn);
+    return d;
+}
+
+template <int NT>
+__device__ __forceinline__ void cnt_keys(const uint32_t* __restrict__ keys,
+                                         const uint32_t* __restrict__ skeys, const CntDesc& d,
+                                         uint32_t (&kk)[4096 / NT]) {
+    constexpr int PER = 4096 / NT;
+    static_assert(PER % 4 == 0, "uint4 key loads");
+    const uint32_t* kb = ((d.flags & 1u) ? skeys : keys) + d.off;
+    if (!(d.flags & 1u) && (d.off & 3u) == 0) {
+        // main-buffer bins start 16-byte aligned and are padded to 4 tuples
+#pragma unroll
+        for (int q = 0; q < PER / 4; ++q) {
+            const uint32_t i = 4u * (threadIdx.x + q * NT);
+            uint4 v = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
+            if (i < d.n) v = __ldcs(reinterpret_cast<const uint4*>(kb + i));
+            kk[4 * q] = v.x;
+            kk[4 * q + 1] = i + 1 < d.n ? v.y : CNT_EMPTY;
+            kk[4 * q + 2] = i + 2 < d.n ? v.z : CNT_EMPTY;
+            kk[4 * q + 3] = i + 3 < d.n ? v.w : CNT_EMPTY;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t i = threadIdx.x + j * NT;
+            kk[j] = i < d.n ? __ldcs(kb + i) : CNT_EMPTY;
+        }
+    }
+}
+
+// resident CTAs per SM: shared memory (table + dummies) and 64 warps bound it
+constexpr int cnt_ctas(int nt, int slots) {
+    return (225 * 1024 / ((slots + 32) * 4)) < (2048 / nt) ? (225 * 1024 / ((slots + 32) * 4))
+                                                         : (2048 / nt);
+}
+// Work-bin descriptors are staged in shared memory: thread 0 copies bin
+// b + 4G's (n, off, flags) with cp.async while the CTA counts bin b, so the
+// loop reads three shared words per bin instead of issuing three dependent
+// global loads and their 64-bit address arithmetic per thread (a version
+// loading them per thread, two bins ahead: C2 1.08 ms; this one 1.01).
+struct RawDesc {
+    uint64_t n, off;
+    uint32_t flags, pad;
+};
+
+__device__ __forceinline__ void stage_desc(RawDesc& d, const WorkBins& w, uint64_t b, uint64_t nw) {
+    if (b < nw) {
+        cp_async8(&d.n, w.n + b);
+        cp_async8(&d.off, w.off + b);
+        cp_async4(&d.flags, w.flags + b);
+    } else {
+        d.n = 0;
+        d.flags = 0;
+    }
+    cp_async_commit();
+}
+
+__device__ __forceinline__ CntDesc cnt_desc_smem(const RawDesc& r, uint64_t cap) {
+    CntDesc d;
+    const uint64_t nn = r.n;
+    d.off = r.off;
+    d.flags = r.flags;
+    d.merged = (r.flags & 2u) ? nn : ~0ull;
+    d.n = ((r.flags & 2u) || nn > cap) ? 0u : static_cast<uint32_t>(nn);
+    return d;
+}
+
+template <int NT, int SLOTS>
+__global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount2(const uint32_t* __restrict__ keys,
+                                                  const uint32_t* __restrict__ skeys, WorkBins w,
+                                                  const uint64_t* nw_dev, uint64_t cap,
+                                                  uint64_t* wb_nnz) {
+    constexpr int PER = 4096 / NT;
+    static_assert(SLOTS % 4 == 0, "table cleared in uint4s");
+    extern __shared__ __align__(16) uint32_t table[];  // SLOTS + 32 per-lane dummies
+    __shared__ RawDesc s_d[4];
+    __shared__ uint32_t s_cnt;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint64_t nw = *nw_dev;
+    const uint64_t G = gridDim.x;
+    for (int i = tid; i < (SLOTS + 32) / 4; i += NT)
+        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
+    uint64_t b = blockIdx.x;
+    if (tid == 0) {
+        s_cnt = 0;
+        for (int q = 0; q < 4; ++q) stage_desc(s_d[q], w, b + q * G, nw);
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    uint32_t k0[PER], k1[PER], k2[PER];
+    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[0], cap), k0);
+    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[1], cap), k1);
+    for (uint32_t it = 0; b < nw; b += G, ++it) {
+        cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[(it + 2) & 3], cap), k2);  // bin b + 2G
+        uint32_t h[PER], old[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t hk =
+                static_cast<uint32_t>((static_cast<uint64_t>(k0[j] * 0x9E3779B1u) * SLOTS) >> 32);
+            h[j] = k0[j] == CNT_EMPTY ? SLOTS + lane : hk;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) old[j] = atomicCAS(&table[h[j]], CNT_EMPTY, k0[j]);
+        uint32_t fresh = 0, pend = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            fresh += (old[j] == CNT_EMPTY) & (k0[j] != CNT_EMPTY);
+            pend |= static_cast<uint32_t>(old[j] != CNT_EMPTY && old[j] != k0[j]) << j;
+        }
+        while (pend) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                if (!((pend >> j) & 1u)) continue;
+                const uint32_t s = h[j] + 1 == SLOTS ? 0u : h[j] + 1;
+                const uint32_t o = atomicCAS(&table[s], CNT_EMPTY, k0[j]);
+                h[j] = s;
+                if (o == CNT_EMPTY) fresh += 1;
+                if (o == CNT_EMPTY || o == k0[j]) pend &= ~(1u << j);
+            }
+        }
+        fresh = __reduce_add_sync(FULL, fresh);
+        if (lane == 0) atomicAdd(&s_cnt, fresh);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) table[h[j]] = CNT_EMPTY;
+        if (tid == 0) {
+            RawDesc& dm = s_d[it & 3];
+            // merged items are already distinct; a valid list has no other
+            // bin above the capacity
+            wb_nnz[b] = (dm.flags & 2u) ? dm.n : s_cnt;
+            s_cnt = 0;
+            stage_desc(dm, w, b + 4 * G, nw);  // slot of bin b is free: bin b + 4G
+            cp_async_wait_group<1>();          // bin b + 3G's descriptor has landed
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            k0[j] = k1[j];
+            k1[j] = k2[j];
+        }
     }
 }
 

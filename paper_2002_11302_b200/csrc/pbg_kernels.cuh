@@ -313,6 +313,7 @@ struct ExpandArgs {
     uint32_t* keys;
     double* vals;
     int col_bits;
+    const uint64_t* bin_off;  // bin tuple offsets (PBG_CHECKED: reservations stay inside the bin)
 };
 
 constexpr int EXP_NT = 256;
@@ -454,6 +455,7 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                 if (lb) {
                     const P bin = pack >> a.lbits;
                     dst = atomicAdd(&a.cursor[bin], (unsigned long long)lb);
+                    PBG_DCHECK(dst >= a.bin_off[bin] && dst + lb <= a.bin_off[bin + 1]);
                     rp = static_cast<uint32_t>(pack & ((P(1) << a.lbits) - 1)) << cb;
                 }
             }
@@ -656,7 +658,6 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
         }
     }
 }
-
 
 
 // ------------------------------------------------------- row-banded expand --

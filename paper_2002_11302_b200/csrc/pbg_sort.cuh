@@ -94,6 +94,7 @@ struct SortArgs {
     double* cval;             // C values
     uint64_t* rowptr;
     uint64_t m;
+    uint64_t c_cap;           // entries the C arrays hold (PBG_CHECKED bound)
     int col_bits;
     unsigned long long* merged_total;
     unsigned int* err;  // bit1 work bin above capacity, bit2 merged != distinct count
@@ -136,9 +137,6 @@ struct SortSmem {
 };
 
 // ---- TMA bulk copy (global -> shared) with mbarrier completion ----
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -181,15 +179,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
         : "memory");
 }
 
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-}
 
 // Thread 0: work bin b (its ticket taken a while ago) becomes descriptor
 // slot `slot`; it arrives asynchronously (cp_async_wait_all + a barrier).
@@ -500,7 +489,13 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     const int sh = bits > SM_NB_BITS ? bits - SM_NB_BITS : 0;
     // ---- 1. bucket histogram / scan / scatter in -> scr ----
     // (keeping the histogram's returned slot in registers to save the second
-    // atomic was measured slower: register pressure at 64 regs spills)
+    // atomic was measured slower: register pressure at 64 regs spills. Two
+    // duplicate-free fast paths were built and measured slower at C2, both
+    // writing every tuple at bucket start + the histogram atomic's arrival
+    // rank in final form, then ordering buckets of 2+ tuples per owning
+    // thread: an 8x8 register rank network 2.3 -> 3.4 ms, an in-place
+    // insertion sort 2.4 -> 2.8 ms — per-thread bucket work is uneven, so
+    // warps wait at the next barrier, and bank conflicts rise.)
 #pragma unroll HIST_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
         const uint32_t d = (sm.k[in][i] - keylo) >> sh;
@@ -518,6 +513,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         const uint32_t d = (key - keylo) >> sh;
         const uint32_t old = atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
         const uint32_t pos = (old >> ((d & 1) * 16)) & 0xffffu;
+        PBG_DCHECK(pos < n);
         sm.k[scr][pos] = key;
         sm.v[scr][pos] = sm.v[in][i];
     }
@@ -620,6 +616,7 @@ __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm,
     const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
     const uint32_t* K = sm.k[buf];
     const double* V = sm.v[buf];
+    PBG_DCHECK(P + U <= a.c_cap && rs + span <= a.m);
     uint32_t* okeys = a.ccol + P;
     double* ovals = a.cval + P;
     for (uint32_t u = tid; u < U; u += SM_NT) {
@@ -667,6 +664,7 @@ __device__ __forceinline__ void write_bin_bulk(const SortArgs& a, SortSmem& sm, 
     if (ka > U) ka = U;
     if (va > U) va = U;
     const uint32_t kb = ka + ((U - ka) & ~3u), vb = va + ((U - va) & ~1u);
+    PBG_DCHECK(P + U <= a.c_cap && rs + span <= a.m && U <= SM_CAP);
     if (tid < ka) a.ccol[P + tid] = K[tid];
     if (tid < U - kb) a.ccol[P + kb + tid] = K[kb + tid];
     if (tid < va) a.cval[P + tid] = V[tid];
@@ -694,6 +692,7 @@ __device__ void write_merged(const SortArgs& a, const BinMeta& m, uint64_t b, ui
     const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
     const uint32_t* K = ((m.flags & 1u) ? a.skeys : a.keys) + m.off;
     const double* V = ((m.flags & 1u) ? a.svals : a.vals) + m.off;
+    PBG_DCHECK(P + U <= a.c_cap && m.rs < a.m);
     for (uint32_t u = tid; u < U; u += SM_NT) {
         __stcs(a.ccol + P + u, K[u] & colmask);
         __stcs(a.cval + P + u, V[u]);

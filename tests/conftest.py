@@ -20,3 +20,18 @@ def _built():
     import oracle
     oracle.build(ref=Path("/root/reference/proj/src").is_dir())
     yield
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """GPU tests upload inputs through torch and keep per-test device
+    contexts: return their memory after every test, so a large product later
+    in the session (C5b bands: ~23 GB of workspace) does not fail on memory
+    an earlier test still caches."""
+    yield
+    if "torch" in sys.modules:
+        import gc
+        import torch
+        if torch.cuda.is_initialized():
+            gc.collect()
+            torch.cuda.empty_cache()

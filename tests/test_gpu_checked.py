@@ -1,0 +1,122 @@
+"""Memory and race checking of every kernel family. The
+reference has no such tooling (proj/src/CMakeLists.txt:12, -Wall -Wextra
+only); the GPU path mixes generic-proxy shared stores with TMA bulk copies in
+both directions, mbarriers and shared-memory hash tables.
+
+tests/cpp/sanitize_driver.cpp calls the C-ABI on small inputs that reach:
+expand, count, sort+merge (TMA bulk loads/stores, the duplicate-free fast
+path), the duplicate pre-merge, the LSD fallback, heavy-row split + dense
+reduce, the column hash SpGEMM with hub columns, COO conversion, the device
+generators, bounded-memory rounds and multi-context row bands. It runs
+* against libpbg_checked.so (PBG_CHECKED: every store site of the expand,
+  sort+merge and heavy-split kernels traps on an index outside its bin, its
+  shared buffer or C), and the GPU parity subset runs on that library too;
+* under compute-sanitizer memcheck / racecheck / synccheck / initcheck where
+  the GPU pool allows it (this pool's wrapper refuses: the tests skip with
+  its message).
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SANITIZER = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+PKG = ROOT / "paper_2002_11302_b200"
+DRIVER_CASES = ["er", "rmat", "stencil", "lsd", "hash", "coo"]
+
+
+def _driver(tmp_path_factory, lib):
+    from paper_2002_11302_b200 import build
+    if not (PKG / lib).exists():
+        build.build_all()
+    exe = tmp_path_factory.mktemp("drv") / f"sanitize_driver_{lib.split('.')[0]}"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", str(ROOT / "include"),
+                    str(ROOT / "tests" / "cpp" / "sanitize_driver.cpp"), "-L", str(PKG),
+                    f"-l:{lib}", "-l:libpbg_host.so", f"-Wl,-rpath,{PKG}", "-o", str(exe)],
+                   check=True)
+    return exe
+
+
+@pytest.fixture(scope="module")
+def driver(tmp_path_factory):
+    return _driver(tmp_path_factory, "libpbg.so")
+
+
+@pytest.fixture(scope="module")
+def checked_driver(tmp_path_factory):
+    return _driver(tmp_path_factory, "libpbg_checked.so")
+
+
+def test_driver_runs_clean(driver):
+    r = subprocess.run([str(driver)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failure(s)" in r.stdout
+
+
+@pytest.mark.parametrize("case", DRIVER_CASES)
+def test_checked_build_driver(checked_driver, case):
+    """Every store index in range (a PBG_CHECKED trap kills the process with
+    the failing condition printed)."""
+    r = subprocess.run([str(checked_driver), case], capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert "PBG_CHECKED failure" not in out, out[-4000:]
+    assert r.returncode == 0 and "0 failure(s)" in r.stdout, out[-4000:]
+
+
+def test_checked_build_parity_subset():
+    """The GPU parity tests that reach every kernel path, on the checked
+    library (PBG_LIB selects it for the Python bindings)."""
+    import sys
+    env = dict(os.environ, PBG_LIB="libpbg_checked.so")
+    sel = ("golden or known_answers or identity or random_sweep or rectangular or "
+           "heavy or uniform_key or tiny_bin or duplicate_and_unsorted or empty_rows or "
+           "widest or coo_conversion or hash_multiply or bounded_memory or expand_row_bands")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests" / "test_gpu_parity.py"),
+                        "-m", "gpu and not slow", "-x", "-q", "-p", "no:cacheprovider", "-k", sel],
+                       capture_output=True, text=True, timeout=1500, env=env, cwd=str(ROOT))
+    out = r.stdout + r.stderr
+    assert "PBG_CHECKED failure" not in out, out[-4000:]
+    assert r.returncode == 0, out[-4000:]
+
+
+# (tool, cases, extra flags). racecheck / synccheck / initcheck replay every
+# shared-memory access, so they take the smaller cases one at a time.
+CASES = [
+    ("memcheck", "", []),
+    ("racecheck", "er", ["--racecheck-report", "all"]),
+    ("racecheck", "rmat", ["--racecheck-report", "all"]),
+    ("racecheck", "stencil", ["--racecheck-report", "all"]),
+    ("racecheck", "lsd", ["--racecheck-report", "all"]),
+    ("racecheck", "hash", ["--racecheck-report", "all"]),
+    ("synccheck", "", []),
+    ("initcheck", "er", []),
+    ("initcheck", "rmat", []),
+]
+
+
+@pytest.mark.parametrize("tool,case,extra", CASES, ids=[f"{t}-{c or 'all'}" for t, c, _ in CASES])
+def test_compute_sanitizer(driver, tool, case, extra):
+    if not os.path.exists(SANITIZER):
+        pytest.skip("compute-sanitizer not installed")
+    cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "99", *extra, str(driver)]
+    if case:
+        cmd.append(case)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (earlier
+        # runs left GPUs needing a reset); test_driver_runs_clean and the
+        # kernels' own bounds checks (PBG_CHECKED builds) stand in for it
+        pytest.skip("compute-sanitizer disabled on this GPU pool: " + out.strip().splitlines()[0][:120])
+    assert r.returncode == 0, out[-6000:]
+    assert "0 failure(s)" in r.stdout, out[-6000:]
+    # the sanitizer's summary line: "ERROR SUMMARY: 0 errors" (racecheck also
+    # prints "RACECHECK SUMMARY: 0 hazards displayed")
+    assert "ERROR SUMMARY: 0 errors" in out, out[-6000:]
