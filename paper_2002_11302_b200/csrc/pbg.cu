@@ -57,9 +57,14 @@ struct DevBuf {
 
 size_t pool_trim();
 
+// bumped on every reallocation: a captured pipeline graph whose pointers may
+// be stale is re-captured
+std::atomic<uint64_t> g_alloc_gen{1};
+
 int grow(DevBuf& b, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (b.cap >= bytes) return PBG_OK;
+    ++g_alloc_gen;
     b.release();
     const size_t want = bytes + bytes / 8;  // grow-only with headroom
     cudaError_t e = cudaMalloc(&b.p, want);
@@ -102,6 +107,7 @@ enum Scalar : int {
     S_HEAVY_PAD,       // padded tuples of heavy rows (scratch size)
     S_ITEMS,           // heavy-row items after a split pass
     S_NWORK,           // work bins
+    S_ABORT,           // speculative launch: the symbolic result differs from the plan
     S_COUNT
 };
 constexpr int kTickets = 32;  // one u32 ticket per single-pass scan / persistent kernel
@@ -139,6 +145,20 @@ struct pbg_context {
     // host path: tuple budget of a single pass (0 = no check); run_pipeline
     // returns kNeedsRounds after the symbolic phase when flop exceeds it
     uint64_t round_tuples = 0;
+    // speculative single-sync pipeline (run_pipeline): the symbolic scalars
+    // of the last synchronous multiply of this shape, and the pipeline
+    // captured as a CUDA graph
+    bool spec_valid = false;
+    uint64_t spec_key[10] = {};
+    unsigned long long spec_hs[S_COUNT] = {};
+    unsigned long long* hs_pinned = nullptr;  // S_COUNT scalars + nnz(C)
+    unsigned long long last_hs[S_COUNT] = {};  // symbolic scalars of the last synchronous multiply
+    uint32_t spec_bands = 1;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_stream = nullptr;  // graphs are captured here (never the legacy stream)
+    bool capturing = false;             // phase events become graph event-record nodes
+    uint64_t gkey[20] = {};
+    uint32_t g_launches = 0;
     ~pbg_context() {
         for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
                           &bin_off, &cursor, &bin_out, &chunk_p0, &keys, &vals, &ccol, &cval,
@@ -157,6 +177,9 @@ struct pbg_context {
             b->release();
         if (ev_ok)
             for (auto& e : ev) cudaEventDestroy(e);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (hs_pinned) cudaFreeHost(hs_pinned);
     }
 };
 
@@ -232,9 +255,32 @@ unsigned blocks_for(uint64_t n, unsigned nt) {
     return static_cast<unsigned>(std::max<uint64_t>(1, b));
 }
 
-// The pipeline on device-resident views.
-int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
-                 const pbg_config& cfg, cudaStream_t st) {
+// Speculative launch: the symbolic scalars that size the buffers and grids
+// must equal the plan's; otherwise the bin count is zeroed (every later
+// kernel reads it from device memory, so they all do nothing), the chunk
+// table is emptied (k_chunks) and the host reruns the multiply synchronously.
+__global__ void k_spec_check(unsigned long long* sc, uint64_t flop, uint64_t nb, uint64_t tcap) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const bool ok = sc[S_FLOP] == flop && sc[S_FLOP_LO] == flop && sc[S_FLOP_HI] == 0 &&
+                    sc[S_NBINS] == nb && sc[S_HEAVY] == 0 && sc[S_TUPLE_CAP] == tcap;
+    if (!ok) {
+        sc[S_ABORT] = 1;
+        sc[S_NBINS] = 0;
+    }
+}
+
+int pipeline_finish(pbg_context* ctx, const pbg_config& cfg, const unsigned long long* hs,
+                    uint64_t nnz, uint64_t flop, uint64_t m, int cb, uint32_t L);
+
+// The pipeline on device-resident views. `assumed` = null: the synchronous
+// pipeline (one host round trip after the symbolic phase sizes everything
+// that follows). `assumed` = the scalars of an earlier multiply of the same
+// shape: everything is launched without waiting (the k_spec_check guard
+// above), the scalars and nnz(C) land in ctx->hs_pinned, and the caller
+// syncs and calls pipeline_finish — so the whole multiply can be captured
+// as one CUDA graph.
+int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
+                      const pbg_config& cfg, cudaStream_t st, const unsigned long long* assumed) {
     using namespace pbg;
     const uint64_t m = A.nrows, k = A.ncols, n = B.ncols;
     const uint64_t nnz_a = A.nnz;
@@ -298,7 +344,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     auto* cursor = static_cast<unsigned long long*>(ctx->cursor.p);
     auto* rowptr = static_cast<uint64_t*>(ctx->rowptr.p);
 
-    CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[0], st, ctx->capturing ? cudaEventRecordExternal : 0));
     CUDA_TRY(cudaMemsetAsync(zb, 0, zero_bytes, st));
     uint32_t L = 0;
 
@@ -347,10 +393,17 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                     m, stat_m3, tickets + 3, sc + S_TUPLE_CAP, nullptr, st);
         ++L;
     }
-    CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[1], st, ctx->capturing ? cudaEventRecordExternal : 0));
     unsigned long long hs[S_COUNT];
-    CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    if (assumed) {
+        std::memcpy(hs, assumed, sizeof hs);
+        k_spec_check<<<1, 32, 0, st>>>(sc, hs[S_FLOP], hs[S_NBINS], hs[S_TUPLE_CAP]);
+        ++L;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::memcpy(ctx->last_hs, hs, sizeof hs);
+    }
     CUDA_TRY(cudaGetLastError());
 
     if (hs[S_FLOP_HI] != 0 || hs[S_FLOP_LO] > ST_VAL)
@@ -376,8 +429,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         } else {
             CUDA_TRY(cudaMemsetAsync(rowptr, 0, 8, st));
         }
-        CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
-        CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[2], st, ctx->capturing ? cudaEventRecordExternal : 0));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[3], st, ctx->capturing ? cudaEventRecordExternal : 0));
         ctx->rep.nbins = 0;
         ctx->nnz_c = 0;
     } else {
@@ -391,7 +444,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         // for nnz(C) before the sort kernel
         if ((rc = grow(ctx->ccol, flop * 4))) return rc;
         if ((rc = grow(ctx->cval, flop * 8))) return rc;
-        CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[5], st, ctx->capturing ? cudaEventRecordExternal : 0));
         auto* keys = static_cast<uint32_t*>(ctx->keys.p);
         auto* vals = static_cast<double*>(ctx->vals.p);
 
@@ -460,7 +513,8 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         if ((rc = grow(ctx->chunk_p0, (nchunks + 1) * 8))) return rc;
         auto* chunk_p0 = static_cast<uint64_t*>(ctx->chunk_p0.p);
         k_chunks<<<blocks_for(nchunks + 1, 256), 256, 0, st>>>(xcolflop, xa_colptr, B.ptr, kv, k,
-                                                              nnz_a, ch, nchunks, chunk_p0);
+                                                              nnz_a, ch, nchunks, chunk_p0,
+                                                              assumed ? sc + S_ABORT : nullptr);
         ++L;
         // bin cursors start at the bins' offsets (atomicAdd returns the slot)
         CUDA_TRY(cudaMemcpyAsync(cursor, bin_off, nb * 8, cudaMemcpyDeviceToDevice, st));
@@ -488,7 +542,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         CUDA_TRY(cudaStreamSynchronize(st));
         return fail(PBG_ERR_INTERNAL, "diagnostic build: stopped after the expand");
 #endif
-        CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[2], st, ctx->capturing ? cudaEventRecordExternal : 0));
 
         // ---- work bins: regular bins + the key-range pieces of heavy rows ----
         const uint64_t* nb_dev = reinterpret_cast<const uint64_t*>(sc + S_NBINS);
@@ -688,7 +742,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                         reinterpret_cast<unsigned int*>(hst), sc + S_NNZ, nullptr, st);
         }
         ++L;
-        CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[6], st, ctx->capturing ? cudaEventRecordExternal : 0));
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
         static std::atomic<bool> attr_set[64] = {};
         if (!attr_set[ctx->device & 63]) {
@@ -748,12 +802,31 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
             fprintf(stderr, " total=%.1f\n", tot);
         }
 #endif
-        CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[3], st, ctx->capturing ? cudaEventRecordExternal : 0));
+        if (assumed) {  // the caller syncs and finishes (pipeline_finish)
+            CUDA_TRY(cudaMemcpyAsync(ctx->hs_pinned, sc, S_COUNT * 8, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(ctx->hs_pinned + S_COUNT, rowptr + m, 8, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[4], st, ctx->capturing ? cudaEventRecordExternal : 0));
+            ctx->g_launches = L;
+            return PBG_OK;
+        }
         CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
         uint64_t nnz = 0;
         CUDA_TRY(cudaMemcpyAsync(&nnz, rowptr + m, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[4], st, ctx->capturing ? cudaEventRecordExternal : 0));
         CUDA_TRY(cudaStreamSynchronize(st));
         CUDA_TRY(cudaGetLastError());
+        return pipeline_finish(ctx, cfg, hs, nnz, flop, m, cb, L);
+    }
+    CUDA_TRY(cudaEventRecordWithFlags(ctx->ev[4], st, ctx->capturing ? cudaEventRecordExternal : 0));
+    return pipeline_finish(ctx, cfg, hs, 0, flop, m, cb, L);
+}
+
+// Conservation checks, phase times (CUDA events) and the report of a
+// multiply whose scalars hs and nnz(C) have reached the host.
+int pipeline_finish(pbg_context* ctx, const pbg_config& cfg, const unsigned long long* hs,
+                    uint64_t nnz, uint64_t flop, uint64_t m, int cb, uint32_t L) {
+    if (flop != 0 && m != 0) {
         ctx->nnz_c = nnz;
         ctx->rep.tuples_into_sort = hs[S_TUPLES_TOTAL];
         ctx->rep.merged_total = hs[S_MERGED_TOTAL];
@@ -769,7 +842,6 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         if (hs[S_MERGED_TOTAL] != nnz)
             return fail(PBG_ERR_INTERNAL, "compressed counts disagree with output nnz");
     }
-    CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
     CUDA_TRY(cudaEventSynchronize(ctx->ev[4]));
     float t_sym = 0, t_exp = 0, t_sort = 0, t_tot = 0;
     CUDA_TRY(cudaEventElapsedTime(&t_sym, ctx->ev[0], ctx->ev[1]));
@@ -793,6 +865,112 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
     ctx->launches = L;
     ctx->have_result = true;
     return PBG_OK;
+}
+
+// A multiply of the same shape as the context's last synchronous one (same
+// dimensions, nnz, configuration; no heavy rows) is launched speculatively
+// with that multiply's symbolic scalars (run_pipeline_impl with `assumed`),
+// captured once as a CUDA graph and replayed while the input pointers and
+// the workspace allocation are unchanged: one host round trip per multiply
+// instead of two, and one graph launch instead of ~25 kernel launches (the
+// latency floor of small products, C1). If the symbolic result differs, the
+// guard kernel has turned every later kernel into a no-op and the multiply
+// reruns synchronously, which also refreshes the plan.
+int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
+                 const pbg_config& cfg, cudaStream_t st) {
+    static const int spec_env = getenv("PBG_SPEC") ? atoi(getenv("PBG_SPEC")) : 2;  // 0 off, 1 no graph, 2 graph
+    const uint64_t key[10] = {A.nrows, A.ncols, A.nnz, B.nrows, B.ncols, B.nnz,
+                              cfg.bin_cap, cfg.reserved[1], ctx->round_tuples,
+                              static_cast<uint64_t>(ctx->device)};
+    int rc;
+    if (spec_env && ctx->spec_valid && std::memcmp(key, ctx->spec_key, sizeof key) == 0) {
+        if (!ctx->hs_pinned) CUDA_TRY(cudaMallocHost(&ctx->hs_pinned, (S_COUNT + 1) * 8));
+        if (!ctx->ev_ok) {
+            for (auto& e : ctx->ev) CUDA_TRY(cudaEventCreate(&e));
+            ctx->ev_ok = true;
+        }
+        const uint64_t gk[20] = {key[0], key[1], key[2], key[3], key[4], key[5], key[6], key[7], key[8], key[9],
+                                 reinterpret_cast<uint64_t>(A.ptr), reinterpret_cast<uint64_t>(A.idx),
+                                 reinterpret_cast<uint64_t>(A.val), reinterpret_cast<uint64_t>(B.ptr),
+                                 reinterpret_cast<uint64_t>(B.idx), reinterpret_cast<uint64_t>(B.val),
+                                 g_alloc_gen.load(), ctx->spec_hs[S_FLOP], ctx->spec_hs[S_NBINS],
+                                 ctx->spec_hs[S_TUPLE_CAP]};
+        bool launched = false;
+        if (spec_env >= 2) {
+            if (!ctx->gexec || std::memcmp(gk, ctx->gkey, sizeof gk) != 0) {
+                if (ctx->gexec) {
+                    cudaGraphExecDestroy(ctx->gexec);
+                    ctx->gexec = nullptr;
+                }
+                // grow() reallocations inside the capture bump g_alloc_gen:
+                // a first capture that allocated is run directly, the next
+                // call captures again on the now stable workspace
+                const uint64_t gen0 = g_alloc_gen.load();
+                if (!ctx->cap_stream)
+                    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+                cudaGraph_t graph = nullptr;
+                CUDA_TRY(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+                ctx->capturing = true;
+                rc = run_pipeline_impl(ctx, A, B, cfg, ctx->cap_stream, ctx->spec_hs);
+                ctx->capturing = false;
+                const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+                if (rc) {
+                    if (graph) cudaGraphDestroy(graph);
+                    return rc;
+                }
+                if (ce != cudaSuccess || !graph) {
+                    cudaGetLastError();
+                    return fail(PBG_ERR_CUDA, "pipeline graph capture failed");
+                }
+                const cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (ie != cudaSuccess) {
+                    cudaGetLastError();
+                    ctx->gexec = nullptr;
+                    return fail(PBG_ERR_CUDA, "pipeline graph instantiation failed");
+                }
+                if (g_alloc_gen.load() == gen0) std::memcpy(ctx->gkey, gk, sizeof gk);
+                else std::memset(ctx->gkey, 0, sizeof ctx->gkey);
+            }
+            CUDA_TRY(cudaGraphLaunch(ctx->gexec, st));
+            launched = true;
+        } else {
+            if ((rc = run_pipeline_impl(ctx, A, B, cfg, st, ctx->spec_hs))) return rc;
+            launched = true;
+        }
+        if (launched) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            CUDA_TRY(cudaGetLastError());
+            const unsigned long long* hs = ctx->hs_pinned;
+            if (!hs[S_ABORT]) {
+                ctx->m = A.nrows;
+                ctx->k = A.ncols;
+                ctx->n = B.ncols;
+                ctx->col_bits = ceil_log2_u64(B.ncols);
+                ctx->flop = hs[S_FLOP];
+                ctx->rep = pbg_report{};
+                ctx->rep.flop = hs[S_FLOP];
+                ctx->rep.nnz_a = A.nnz;
+                ctx->rep.nnz_b = B.nnz;
+                ctx->rep.gpu_bins = static_cast<uint32_t>(hs[S_NBINS]);
+                ctx->rep.heavy_bins = 0;
+                ctx->rep.bin_cap = static_cast<uint32_t>(cfg.bin_cap ? cfg.bin_cap : pbg::SM_CAP);
+                ctx->rep.tuple_bytes = hs[S_TUPLE_CAP] * 12;
+                ctx->rep.expand_bands = ctx->spec_bands;
+                return pipeline_finish(ctx, cfg, hs, hs[S_COUNT], hs[S_FLOP], A.nrows,
+                                       ctx->col_bits, ctx->g_launches);
+            }
+            // plan mismatch: fall through to the synchronous pipeline
+        }
+    }
+    rc = run_pipeline_impl(ctx, A, B, cfg, st, nullptr);
+    ctx->spec_valid = rc == PBG_OK && ctx->rep.heavy_bins == 0 && ctx->flop > 0 && A.nrows > 0;
+    if (ctx->spec_valid) {
+        std::memcpy(ctx->spec_key, key, sizeof key);
+        std::memcpy(ctx->spec_hs, ctx->last_hs, sizeof ctx->spec_hs);
+        ctx->spec_bands = ctx->rep.expand_bands;
+    }
+    return rc;
 }
 
 std::mutex g_pool_mu;

@@ -280,9 +280,14 @@ __global__ void k_binsizes(const uint32_t* __restrict__ bin_rs,
 __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
                          const uint64_t* __restrict__ a_colptr,
                          const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t kb,
-                         uint64_t nnz_a, uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0) {
+                         uint64_t nnz_a, uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0,
+                         const unsigned long long* abort) {
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (c > nchunks) return;
+    if (abort && *abort) {  // speculative launch rejected: every chunk empty
+        chunk_p0[c] = 0;
+        return;
+    }
     if (c == nchunks) {
         chunk_p0[c] = nnz_a;
         return;
