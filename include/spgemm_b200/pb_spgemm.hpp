@@ -23,6 +23,13 @@ struct PbConfig {
     std::uint64_t l2_bytes = 1 << 20;
     int nthreads = 0;                // no meaning on the GPU
     bool balanced_bins = false;
+    // B200 extension (after the reference's fields, so the reference's
+    // aggregate initialisations still compile): devices to split C's rows
+    // over as flop-balanced bands (pbg_config.ngpus; 0 = the
+    // SPGEMM_B200_NGPUS environment variable, else one; -1 = every visible
+    // device), and the first device (-1 = the current one).
+    int ngpus = 0;
+    int device = -1;
 };
 
 inline int ceil_log2(std::uint64_t x) { return x <= 1 ? 0 : std::bit_width(x - 1); }

@@ -1,6 +1,7 @@
 // pb_spgemm_shim.cpp — spgemm::pb_multiply re-implemented over the C-ABI
 // (include/pbg.h). The drop-in for reference proj/src/pb_spgemm.cpp:330-361:
 // same signature, same exception classes, GPU underneath, no CPU fallback.
+#include <cstdlib>
 #include <stdexcept>
 
 #include "pbg.h"
@@ -41,6 +42,10 @@ pbg_config to_c(const PbConfig& c) {
     o.l2_bytes = c.l2_bytes;
     o.nthreads = c.nthreads;
     o.balanced_bins = c.balanced_bins ? 1 : 0;
+    o.device = c.device;
+    o.ngpus = c.ngpus;
+    if (o.ngpus == 0)
+        if (const char* e = std::getenv("SPGEMM_B200_NGPUS")) o.ngpus = std::atoi(e);
     return o;
 }
 

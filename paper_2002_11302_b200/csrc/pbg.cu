@@ -119,7 +119,7 @@ struct pbg_context {
     bool rowflop32 = true;  // row_flop holds u32 counters (nnz(B) < 2^32)
     int num_sms = 148;
     DevBuf colflop_off, row_flop, row_off, flags, row_bin, bin_rs, bin_cnt, bin_off, cursor,
-        bin_out, chunk_p0, keys, vals, ccol, cval, rowptr, zero_block, in_a_ptr, in_a_idx,
+        bin_out, chunk_p0, chunk_col, keys, vals, ccol, cval, rowptr, zero_block, in_a_ptr, in_a_idx,
         in_a_val, in_b_ptr, in_b_idx, in_b_val;
     // heavy rows + work bins
     DevBuf heavy_excl, hpad_excl, bin_hidx, hbin, hoff, hhead, hcount, skeys, svals, child_cnt,
@@ -153,7 +153,7 @@ struct pbg_context {
     unsigned long long spec_hs[S_COUNT] = {};
     unsigned long long* hs_pinned = nullptr;  // S_COUNT scalars + nnz(C)
     unsigned long long last_hs[S_COUNT] = {};  // symbolic scalars of the last synchronous multiply
-    uint32_t spec_bands = 1;
+    uint32_t spec_bands = 1, spec_cap = 0;
     cudaGraphExec_t gexec = nullptr;
     cudaStream_t cap_stream = nullptr;  // graphs are captured here (never the legacy stream)
     bool capturing = false;             // phase events become graph event-record nodes
@@ -161,7 +161,7 @@ struct pbg_context {
     uint32_t g_launches = 0;
     ~pbg_context() {
         for (DevBuf* b : {&colflop_off, &row_flop, &row_off, &flags, &row_bin, &bin_rs, &bin_cnt,
-                          &bin_off, &cursor, &bin_out, &chunk_p0, &keys, &vals, &ccol, &cval,
+                          &bin_off, &cursor, &bin_out, &chunk_p0, &chunk_col, &keys, &vals, &ccol, &cval,
                           &rowptr, &zero_block, &in_a_ptr, &in_a_idx, &in_a_val, &in_b_ptr,
                           &in_b_idx, &in_b_val, &heavy_excl, &hpad_excl, &bin_hidx, &hbin, &hoff,
                           &hhead, &hcount, &skeys, &svals, &child_cnt, &child_pos, &hstat, &wcnt,
@@ -284,7 +284,20 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
     using namespace pbg;
     const uint64_t m = A.nrows, k = A.ncols, n = B.ncols;
     const uint64_t nnz_a = A.nnz;
-    const uint64_t cap = cfg.bin_cap ? cfg.bin_cap : SM_CAP;
+    // bin capacity: shared-memory sized (SM_CAP) unless the product is too
+    // small to give the count and sort kernels ~4 bins per SM — then smaller
+    // bins (from an estimate on the host: nnz(A) x mean nnz of B's rows; only
+    // the bin size depends on it, not the result)
+    uint64_t cap = cfg.bin_cap ? cfg.bin_cap : SM_CAP;
+    if (!cfg.bin_cap && A.ncols > 0) {
+        const double est = static_cast<double>(A.nnz) * static_cast<double>(B.nnz) / A.ncols;
+        const double want = est / (4.0 * ctx->num_sms);
+        uint64_t c2 = SM_CAP;
+        while (c2 > 512 && c2 > want) c2 >>= 1;
+        static const int cap_env = getenv("PBG_AUTO_CAP_MIN") ? atoi(getenv("PBG_AUTO_CAP_MIN")) : 1024;  // tuning hook
+        cap = std::max<uint64_t>(c2, static_cast<uint64_t>(std::max(cap_env, 16)));
+        cap = std::min<uint64_t>(cap, SM_CAP);
+    }
     const int cb = ceil_log2_u64(n);
     // rows per bin: local_row << col_bits | col must stay below 2^31 so keys
     // never collide with the hash-set sentinel 0xffffffff
@@ -511,9 +524,11 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         while (ch < 16384 && flop / ch > warps * 4) ch <<= 1;
         const uint64_t nchunks = (flop + ch - 1) / ch;
         if ((rc = grow(ctx->chunk_p0, (nchunks + 1) * 8))) return rc;
+        if ((rc = grow(ctx->chunk_col, (nchunks + 1) * 8))) return rc;
         auto* chunk_p0 = static_cast<uint64_t*>(ctx->chunk_p0.p);
+        auto* chunk_col = static_cast<uint64_t*>(ctx->chunk_col.p);
         k_chunks<<<blocks_for(nchunks + 1, 256), 256, 0, st>>>(xcolflop, xa_colptr, B.ptr, kv, k,
-                                                              nnz_a, ch, nchunks, chunk_p0,
+                                                              nnz_a, ch, nchunks, chunk_p0, chunk_col,
                                                               assumed ? sc + S_ABORT : nullptr);
         ++L;
         // bin cursors start at the bins' offsets (atomicAdd returns the slot)
@@ -522,7 +537,7 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         while ((1ull << lbits) < maxr) ++lbits;
         const bool pack32 = nb < (1ull << (32 - lbits));
         if ((rc = grow(ctx->row_pack, (m + 1) * (pack32 ? 4 : 8)))) return rc;
-        ExpandArgs ea{xa_colptr, xa_rowids, xa_vals, B.ptr, B.idx, B.val, kv, k, chunk_p0, nchunks,
+        ExpandArgs ea{xa_colptr, xa_rowids, xa_vals, B.ptr, B.idx, B.val, kv, k, chunk_p0, chunk_col, nchunks,
                       ctx->row_pack.p, lbits, cursor, keys, vals, cb, bin_off};
         if (pack32) {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
@@ -589,10 +604,12 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                         sc + S_HEAVY_PAD, nullptr, st);
             L += 2;
         }
-        k_heavy_init<<<blocks_for(m + 1, 256), 256, 0, st>>>(bin_cnt, nb_dev, heavy_excl,
-                                                            hpad_excl, cap, cb, hbin, hoff,
-                                                            bin_hidx, cur);
-        ++L;
+        if (H > 0) {
+            k_heavy_init<<<blocks_for(m + 1, 256), 256, 0, st>>>(bin_cnt, nb_dev, heavy_excl,
+                                                                hpad_excl, cap, cb, hbin, hoff,
+                                                                bin_hidx, cur);
+            ++L;
+        }
         if (H > 0) {
             CUDA_TRY(cudaMemcpyAsync(hs, sc, sizeof hs, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
@@ -655,8 +672,17 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                 nitems = nout;
                 sh -= d;
             }
-            k_hv_dense<<<static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms)), HV_NT,
-                         0, st>>>(hc, cur, nitems);
+            {
+                const size_t dsm = static_cast<size_t>(HV_DC) * HV_DENSE * 8 + HV_DENSE;
+                static std::atomic<bool> dn_attr[64] = {};
+                if (!dn_attr[ctx->device & 63]) {
+                    CUDA_TRY(cudaFuncSetAttribute(k_hv_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(dsm)));
+                    dn_attr[ctx->device & 63] = true;
+                }
+                k_hv_dense<<<static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms)),
+                             HV_NT, dsm, st>>>(hc, cur, nitems);
+            }
             ++L;
             CUDA_TRY(cudaMemsetAsync(hcount, 0, H * 4, st));
             k_heavy_heads<<<blocks_for(nitems, 256), 256, 0, st>>>(cur.h, nitems, hhead, hcount);
@@ -680,15 +706,22 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         auto* wpos = static_cast<uint64_t*>(ctx->wpos.p);
         auto* wb_nnz = static_cast<uint64_t*>(ctx->wb_nnz.p);
         auto* wb_out = static_cast<uint64_t*>(ctx->wb_out.p);
-        k_work_count<<<blocks_for(m + 1, 256), 256, 0, st>>>(
-            nb_dev, bin_hidx, hcount, cursor, bin_off, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
-            reinterpret_cast<unsigned int*>(sc + S_ERR));
-        launch_scan(ArrayIn{wcnt}, wpos, 0, nb_dev, m, stat_m7, tickets + 8, sc + S_NWORK,
-                    nullptr, st);
-        k_work_fill<<<blocks_for(m + 1, 256), 256, 0, st>>>(nb_dev, bin_rs, bin_cnt, bin_off,
-                                                           bin_hidx, wpos, hhead, hcount, hc,
-                                                           cur, cb, w);
-        L += 3;
+        if (H == 0) {  // work bins = bins: one launch
+            k_work_direct<<<blocks_for(m + 1, 256), 256, 0, st>>>(
+                nb_dev, bin_rs, bin_cnt, bin_off, cursor, cb, w, sc + S_NWORK, sc + S_TUPLES_TOTAL,
+                reinterpret_cast<unsigned int*>(sc + S_ERR));
+            ++L;
+        } else {
+            k_work_count<<<blocks_for(m + 1, 256), 256, 0, st>>>(
+                nb_dev, bin_hidx, hcount, cursor, bin_off, bin_cnt, wcnt, sc + S_TUPLES_TOTAL,
+                reinterpret_cast<unsigned int*>(sc + S_ERR));
+            launch_scan(ArrayIn{wcnt}, wpos, 0, nb_dev, m, stat_m7, tickets + 8, sc + S_NWORK,
+                        nullptr, st);
+            k_work_fill<<<blocks_for(m + 1, 256), 256, 0, st>>>(nb_dev, bin_rs, bin_cnt, bin_off,
+                                                               bin_hidx, wpos, hhead, hcount, hc,
+                                                               cur, cb, w);
+            L += 3;
+        }
         if (nitems) {
             k_work_fill_items<<<blocks_for(nitems, 256), 256, 0, st>>>(wpos, bin_rs, hhead, hc, cur,
                                                                        nitems, w);
@@ -702,9 +735,10 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
         static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
+        static const bool cnt_pair = getenv("PBG_CNT_PAIR") && atoi(getenv("PBG_CNT_PAIR")) != 0;  // A/B hook
         auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
-            static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
-            const int shape = (cnt_v1 ? 2 : 0) + (big_table ? 1 : 0);
+            static std::atomic<bool> attr_set[6][64] = {};  // [kernel x shape][device]
+            const int shape = (cnt_v1 ? 2 : cnt_pair ? 4 : 0) + (big_table ? 1 : 0);
             if (!attr_set[shape][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
@@ -725,6 +759,12 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                 if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
             } else {
                 if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
+            }
+        } else if (cnt_pair) {
+            if (big_table) {
+                if ((rc = launch_count(k_bincount_pair<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
+            } else {
+                if ((rc = launch_count(k_bincount_pair<512, 16384>, 512, (16384 + 32) * 4))) return rc;
             }
         } else if (big_table) {
             if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
@@ -954,7 +994,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
                 ctx->rep.nnz_b = B.nnz;
                 ctx->rep.gpu_bins = static_cast<uint32_t>(hs[S_NBINS]);
                 ctx->rep.heavy_bins = 0;
-                ctx->rep.bin_cap = static_cast<uint32_t>(cfg.bin_cap ? cfg.bin_cap : pbg::SM_CAP);
+                ctx->rep.bin_cap = ctx->spec_cap;
                 ctx->rep.tuple_bytes = hs[S_TUPLE_CAP] * 12;
                 ctx->rep.expand_bands = ctx->spec_bands;
                 return pipeline_finish(ctx, cfg, hs, hs[S_COUNT], hs[S_FLOP], A.nrows,
@@ -969,6 +1009,7 @@ int run_pipeline(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_view& B,
         std::memcpy(ctx->spec_key, key, sizeof key);
         std::memcpy(ctx->spec_hs, ctx->last_hs, sizeof ctx->spec_hs);
         ctx->spec_bands = ctx->rep.expand_bands;
+        ctx->spec_cap = ctx->rep.bin_cap;
     }
     return rc;
 }

@@ -152,6 +152,28 @@ __device__ __forceinline__ HvTile hv_tile(const Items& it, const uint64_t* tile_
     return r;
 }
 
+// Warp-aggregated shared-memory histogram increment. Lanes hold consecutive
+// tuples of a run-ordered stream (a B row's columns are sorted), so equal
+// buckets come in runs of adjacent lanes: the first lane of each run adds
+// the run's length once and the others derive their rank from its old
+// count. RMAT's skewed columns made the one-atomic-per-tuple version
+// serialise on a few hot buckets (ncu: 2.6 G shared bank conflicts in
+// k_hv_scatter for 3.8 G tuples). Returns the tuple's rank in its bucket.
+__device__ __forceinline__ uint32_t warp_bucket_rank(uint32_t* cnt, uint32_t bk, bool valid) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t prev = __shfl_up_sync(FULL, bk, 1);
+    const uint32_t vm = __ballot_sync(FULL, valid);
+    const uint32_t heads = __ballot_sync(FULL, valid && (lane == 0 || bk != prev));
+    const uint32_t upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+    const uint32_t above = heads & ~upto;
+    const int end = above ? __ffs(above) - 1 : 32 - __clz(vm);  // one past this run
+    uint32_t base = 0;
+    if (valid && ((heads >> lane) & 1u)) base = atomicAdd(&cnt[bk], static_cast<uint32_t>(end - lane));
+    const int head = 31 - __clz(heads & upto);
+    const uint32_t hb = __shfl_sync(FULL, base, head < 0 ? 0 : head);
+    return hb + static_cast<uint32_t>(lane - head);
+}
+
 __global__ void __launch_bounds__(HV_NT) k_hv_hist(HeavyCtx c, Items it, uint64_t nitems,
                                                    const uint64_t* __restrict__ tile_pos,
                                                    const uint32_t* __restrict__ tile_item,
@@ -160,14 +182,25 @@ __global__ void __launch_bounds__(HV_NT) k_hv_hist(HeavyCtx c, Items it, uint64_
     const int tid = threadIdx.x;
     const uint64_t ntiles = tile_pos[nitems];
     const uint32_t nbk = 1u << d, s2 = sh - d, mask = nbk - 1u;
+    constexpr int TPT = HV_TILE / HV_NT;  // 8 keys per thread, all loads in flight together
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const HvTile tl = hv_tile(it, tile_pos, tile_item, t);
         const uint32_t buf = it.buf[tl.i];
         const uint32_t* K = (buf ? c.skeys : c.keys) + item_base(c, it.h[tl.i], buf) +
                             it.loc[tl.i] + tl.start;
+        uint32_t kk[TPT];
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const uint32_t q = tid + j * HV_NT;
+            kk[j] = q < tl.m ? __ldcs(K + q) : 0u;
+        }
         for (uint32_t q = tid; q < nbk; q += HV_NT) cnt[q] = 0;
         __syncthreads();
-        for (uint32_t q = tid; q < tl.m; q += HV_NT) atomicAdd(&cnt[(__ldcs(K + q) >> s2) & mask], 1u);
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const uint32_t q = tid + j * HV_NT;
+            warp_bucket_rank(cnt, (kk[j] >> s2) & mask, q < tl.m);
+        }
         __syncthreads();
         uint32_t* h = hist + static_cast<uint64_t>(tl.i) * nbk;
         for (uint32_t q = tid; q < nbk; q += HV_NT)
@@ -295,10 +328,9 @@ __global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, u
 #pragma unroll
         for (int j = 0; j < TPT; ++j) {
             const uint32_t q = tid + j * HV_NT;
-            if (q < tl.m) {
-                const uint32_t bk = (kk[j] >> s2) & mask;
-                rb[j] = atomicAdd(&sm.cnt[bk], 1u) | (bk << 16);
-            }
+            const uint32_t bk = (kk[j] >> s2) & mask;
+            const uint32_t r = warp_bucket_rank(sm.cnt, bk, q < tl.m);
+            rb[j] = r | (bk << 16);
         }
         __syncthreads();
         {  // one global reservation per non-empty bucket
@@ -395,12 +427,20 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
 // measured 1.5x slower: these items are popular columns, and L2 atomics
 // serialise per address.)
 constexpr int HV_DENSE = 1 << HV_DENSE_BITS;
+#ifndef PBG_DENSE_COPIES
+#define PBG_DENSE_COPIES 1
+#endif
+// DC accumulator copies, warp w adding into copy w % DC (fewer warps contend
+// for a popular column's slot); summed into copy 0 before the write-back
+constexpr int HV_DC = PBG_DENSE_COPIES;
 __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64_t nitems) {
-    __shared__ double acc[HV_DENSE];
-    __shared__ uint8_t seen[HV_DENSE];
+    extern __shared__ __align__(16) unsigned char dn_raw[];
+    double* acc_all = reinterpret_cast<double*>(dn_raw);                       // HV_DC x HV_DENSE
+    uint8_t* seen = reinterpret_cast<uint8_t*>(acc_all + HV_DC * HV_DENSE);    // HV_DENSE
     __shared__ uint32_t s_warp[HV_NT / 32 + 1];
     constexpr int PER = HV_DENSE / HV_NT;  // 8
     const int tid = threadIdx.x;
+    double* acc = acc_all + ((tid >> 5) % HV_DC) * HV_DENSE;
     for (uint64_t i = blockIdx.x; i < nitems; i += gridDim.x) {
         if (it.kind[i] != IT_DENSE) continue;
         const uint32_t buf = it.buf[i];
@@ -409,10 +449,10 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
         double* V = (buf ? c.svals : c.vals) + base;
         const uint64_t n = it.n[i];
         const uint32_t keylo = it.keylo[i];
-        for (int q = tid; q < HV_DENSE; q += HV_NT) {
-            acc[q] = 0.0;
-            seen[q] = 0;
-        }
+        // -0.0 is the exact additive identity: a column whose only product is
+        // -0.0 keeps its sign, as the reference's first-insert does
+        for (int q = tid; q < HV_DC * HV_DENSE; q += HV_NT) acc_all[q] = -0.0;
+        for (int q = tid; q < HV_DENSE; q += HV_NT) seen[q] = 0;
         __syncthreads();
         // 8 tuples per thread in flight: the loads of a batch are issued
         // before its shared-memory adds
@@ -435,6 +475,15 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
             }
         }
         __syncthreads();
+        if (HV_DC > 1) {
+            for (int q = tid; q < HV_DENSE; q += HV_NT) {
+                double sum = acc_all[q];
+#pragma unroll
+                for (int cpy = 1; cpy < HV_DC; ++cpy) sum += acc_all[cpy * HV_DENSE + q];
+                acc_all[q] = sum;
+            }
+            __syncthreads();
+        }
         uint32_t cnt = 0;
 #pragma unroll
         for (int j = 0; j < PER; ++j) cnt += seen[tid * PER + j];
@@ -445,7 +494,7 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
             const uint32_t slot = tid * PER + j;
             if (seen[slot]) {
                 K[o] = keylo + slot;
-                V[o] = acc[slot];
+                V[o] = acc_all[slot];
                 ++o;
             }
         }
@@ -523,6 +572,37 @@ __global__ void k_work_fill(const uint64_t* nb_dev, const uint32_t* __restrict__
         return;
     }
     // heavy row: its items are filled by k_work_fill_items (one thread each)
+}
+
+// No heavy rows: every bin is one work bin (work bin b = bin b). Replaces
+// k_heavy_init + k_work_count + scan + k_work_fill (four launches, the
+// latency floor of small products) with one; also the expand conservation
+// check and the tuples_into_sort total.
+__global__ void k_work_direct(const uint64_t* nb_dev, const uint32_t* __restrict__ bin_rs,
+                              const uint64_t* __restrict__ bin_cnt,
+                              const uint64_t* __restrict__ bin_off,
+                              const unsigned long long* __restrict__ cursor, int col_bits,
+                              WorkBins w, unsigned long long* nw_out,
+                              unsigned long long* tuples_total, unsigned int* err) {
+    const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nb = *nb_dev;
+    if (b == 0) *nw_out = nb;
+    uint64_t cur = 0;
+    if (b < nb) {
+        const uint32_t rs = bin_rs[b], span = bin_rs[b + 1] - rs;
+        const uint64_t off = bin_off[b], n = bin_cnt[b];
+        w.off[b] = off;
+        w.n[b] = n;
+        w.rs[b] = rs;
+        w.span[b] = span;
+        w.keylo[b] = 0;
+        w.keybits[b] = (span > 1 ? 32 - __clz(span - 1) : 0) + col_bits;
+        w.flags[b] = 0;
+        cur = cursor[b] - off;  // cursors start at the bin's offset
+        if (cur != n) atomicOr(err, 1u);
+    }
+    cur = warp_sum(cur);
+    if ((threadIdx.x & 31) == 0 && cur) atomicAdd(tuples_total, (unsigned long long)cur);
 }
 
 // Work bins of heavy-row items: item `it` of row h lands at wpos[bin] + (it - head[h]).
@@ -714,7 +794,7 @@ constexpr int cnt_ctas(int nt, int slots) {
 // loading them per thread, two bins ahead: C2 1.08 ms; this one 1.01).
 struct RawDesc {
     uint64_t n, off;
-    uint32_t flags, pad;
+    uint32_t flags, keybits;
 };
 
 __device__ __forceinline__ void stage_desc(RawDesc& d, const WorkBins& w, uint64_t b, uint64_t nw) {
@@ -722,9 +802,11 @@ __device__ __forceinline__ void stage_desc(RawDesc& d, const WorkBins& w, uint64
         cp_async8(&d.n, w.n + b);
         cp_async8(&d.off, w.off + b);
         cp_async4(&d.flags, w.flags + b);
+        cp_async4(&d.keybits, w.keybits + b);
     } else {
         d.n = 0;
         d.flags = 0;
+        d.keybits = 0;
     }
     cp_async_commit();
 }
@@ -811,6 +893,123 @@ __global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount2(const uin
         for (int j = 0; j < PER; ++j) {
             k0[j] = k1[j];
             k1[j] = k2[j];
+        }
+    }
+}
+
+// Two work bins per iteration in one table: bin B's keys carry bit 31 (both
+// bins' keys fit 30 bits, so a tagged key never equals the empty marker), so
+// the per-iteration costs — descriptor reads, key-load issue, two barriers,
+// the count reductions — are paid once per pair. A pair whose keys need 31
+// bits is counted as two rounds.
+template <int NT, int SLOTS>
+__global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount_pair(const uint32_t* __restrict__ keys,
+                                                      const uint32_t* __restrict__ skeys, WorkBins w,
+                                                      const uint64_t* nw_dev, uint64_t cap,
+                                                      uint64_t* wb_nnz) {
+    constexpr int PER = 4096 / NT;
+    extern __shared__ __align__(16) uint32_t table[];  // SLOTS + 32 per-lane dummies
+    __shared__ RawDesc s_d[8];                          // bin v of this CTA -> slot v % 8
+    __shared__ uint32_t s_cnt[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint64_t nw = *nw_dev;
+    const uint64_t G = gridDim.x;
+    for (int i = tid; i < (SLOTS + 32) / 4; i += NT)
+        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
+    const uint64_t b0 = blockIdx.x;
+    if (tid == 0) {
+        s_cnt[0] = s_cnt[1] = 0;
+        for (int q = 0; q < 8; ++q) stage_desc(s_d[q], w, b0 + q * G, nw);
+        cp_async_wait_all();
+    }
+    __syncthreads();
+    // insert PER keys of one bin (tag already applied); returns fresh count
+    auto insert = [&](const uint32_t (&kk)[PER], uint32_t (&h)[PER]) -> uint32_t {
+        uint32_t old[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t hk =
+                static_cast<uint32_t>((static_cast<uint64_t>(kk[j] * 0x9E3779B1u) * SLOTS) >> 32);
+            h[j] = kk[j] == CNT_EMPTY ? SLOTS + lane : hk;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) old[j] = atomicCAS(&table[h[j]], CNT_EMPTY, kk[j]);
+        uint32_t fresh = 0, pend = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            fresh += (old[j] == CNT_EMPTY) & (kk[j] != CNT_EMPTY);
+            pend |= static_cast<uint32_t>(old[j] != CNT_EMPTY && old[j] != kk[j]) << j;
+        }
+        while (pend) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                if (!((pend >> j) & 1u)) continue;
+                const uint32_t s = h[j] + 1 == SLOTS ? 0u : h[j] + 1;
+                const uint32_t o = atomicCAS(&table[s], CNT_EMPTY, kk[j]);
+                h[j] = s;
+                if (o == CNT_EMPTY) fresh += 1;
+                if (o == CNT_EMPTY || o == kk[j]) pend &= ~(1u << j);
+            }
+        }
+        return fresh;
+    };
+    uint32_t kA[PER], kB[PER], nA[PER], nB[PER];
+    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[0], cap), kA);
+    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[1], cap), kB);
+    for (uint32_t it = 0; b0 + 2ull * it * G < nw; ++it) {
+        const uint32_t v = 2 * it;  // this pair: bins v and v + 1 of this CTA
+        const uint64_t bA = b0 + v * G, bB = bA + G;
+        // next pair's keys in flight
+        cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[(v + 2) & 7], cap), nA);
+        cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[(v + 3) & 7], cap), nB);
+        const bool tag = s_d[v & 7].keybits <= 30 && s_d[(v + 1) & 7].keybits <= 30;
+        uint32_t hA[PER], hB[PER];
+        if (tag) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+                if (kB[j] != CNT_EMPTY) kB[j] |= 0x80000000u;
+            const uint32_t fa = insert(kA, hA), fb = insert(kB, hB);
+            const uint32_t ra = __reduce_add_sync(FULL, fa), rb = __reduce_add_sync(FULL, fb);
+            if (lane == 0) {
+                atomicAdd(&s_cnt[0], ra);
+                atomicAdd(&s_cnt[1], rb);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                table[hA[j]] = CNT_EMPTY;
+                table[hB[j]] = CNT_EMPTY;
+            }
+        } else {  // two rounds: bin A, then bin B
+            const uint32_t ra = __reduce_add_sync(FULL, insert(kA, hA));
+            if (lane == 0) atomicAdd(&s_cnt[0], ra);
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PER; ++j) table[hA[j]] = CNT_EMPTY;
+            __syncthreads();
+            const uint32_t rb = __reduce_add_sync(FULL, insert(kB, hB));
+            if (lane == 0) atomicAdd(&s_cnt[1], rb);
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PER; ++j) table[hB[j]] = CNT_EMPTY;
+        }
+        if (tid == 0) {
+            // merged items are already distinct; a valid list has no other
+            // bin above the capacity
+            const RawDesc& da = s_d[v & 7];
+            const RawDesc& db = s_d[(v + 1) & 7];
+            if (bA < nw) wb_nnz[bA] = (da.flags & 2u) ? da.n : s_cnt[0];
+            if (bB < nw) wb_nnz[bB] = (db.flags & 2u) ? db.n : s_cnt[1];
+            s_cnt[0] = s_cnt[1] = 0;
+            stage_desc(s_d[v & 7], w, b0 + (v + 8) * G, nw);  // slots of this pair are free
+            stage_desc(s_d[(v + 1) & 7], w, b0 + (v + 9) * G, nw);
+            cp_async_wait_group<2>();  // the pair after next has landed
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            kA[j] = nA[j];
+            kB[j] = nB[j];
         }
     }
 }

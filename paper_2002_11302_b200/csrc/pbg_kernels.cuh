@@ -281,7 +281,7 @@ __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
                          const uint64_t* __restrict__ a_colptr,
                          const uint64_t* __restrict__ b_rowptr, uint64_t k, uint64_t kb,
                          uint64_t nnz_a, uint64_t ch, uint64_t nchunks, uint64_t* chunk_p0,
-                         const unsigned long long* abort) {
+                         uint64_t* chunk_col, const unsigned long long* abort) {
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (c > nchunks) return;
     if (abort && *abort) {  // speculative launch rejected: every chunk empty
@@ -290,6 +290,7 @@ __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
     }
     if (c == nchunks) {
         chunk_p0[c] = nnz_a;
+        chunk_col[c] = k;
         return;
     }
     const uint64_t t0 = c * ch;
@@ -299,6 +300,10 @@ __global__ void k_chunks(const uint64_t* __restrict__ colflop_off,
     const uint64_t rel = t0 - colflop_off[col];
     const uint64_t i = (rel + lb - 1) / lb;
     chunk_p0[c] = a_colptr[col] + i;
+    // a lower bound on the column of run chunk_p0[c] (the expand starts its
+    // column search there instead of searching colptr from 0: C1 expand
+    // 0.053 -> 0.029 ms)
+    chunk_col[c] = i < a_colptr[col + 1] - a_colptr[col] ? col : col + 1;
 }
 
 struct ExpandArgs {
@@ -311,6 +316,7 @@ struct ExpandArgs {
     uint64_t a_ncols;   // (virtual) columns of A
     uint64_t b_rows;    // real columns of A = rows of B (virtual column v reads B row v % b_rows)
     const uint64_t* chunk_p0;
+    const uint64_t* chunk_col;  // lower bound on the column of each chunk's first run
     uint64_t nchunks;
     const void* row_pack;          // per row: bin << lbits | (row - bin row start), u32 or u64
     int lbits;
@@ -405,7 +411,9 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
 #endif
         const uint64_t pend = a.chunk_p0[c + 1];
         if (p >= pend) continue;
-        uint64_t kcur = warp_last_le(a.a_colptr, 0, a.a_ncols, p);
+        // the column of run p: at most a few columns past the chunk's bound
+        uint64_t kcur = a.chunk_col[c];
+        if (a.a_colptr[kcur + 1] <= p) kcur = warp_last_le(a.a_colptr, kcur, a.a_ncols, p);
         // Software pipeline over batches of 32 runs: batch t+1's loads (row
         // id, value, column window, then packed bin and B row bounds) are
         // issued while batch t's tuples stream out, so only the bin-cursor
