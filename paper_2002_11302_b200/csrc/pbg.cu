@@ -735,10 +735,9 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
         static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
-        static const bool cnt_pair = getenv("PBG_CNT_PAIR") && atoi(getenv("PBG_CNT_PAIR")) != 0;  // A/B hook
         auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
-            static std::atomic<bool> attr_set[6][64] = {};  // [kernel x shape][device]
-            const int shape = (cnt_v1 ? 2 : cnt_pair ? 4 : 0) + (big_table ? 1 : 0);
+            static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
+            const int shape = (cnt_v1 ? 2 : 0) + (big_table ? 1 : 0);
             if (!attr_set[shape][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
@@ -759,12 +758,6 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                 if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
             } else {
                 if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
-            }
-        } else if (cnt_pair) {
-            if (big_table) {
-                if ((rc = launch_count(k_bincount_pair<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
-            } else {
-                if ((rc = launch_count(k_bincount_pair<512, 16384>, 512, (16384 + 32) * 4))) return rc;
             }
         } else if (big_table) {
             if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;

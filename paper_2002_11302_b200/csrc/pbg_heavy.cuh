@@ -897,121 +897,4 @@ __global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount2(const uin
     }
 }
 
-// Two work bins per iteration in one table: bin B's keys carry bit 31 (both
-// bins' keys fit 30 bits, so a tagged key never equals the empty marker), so
-// the per-iteration costs — descriptor reads, key-load issue, two barriers,
-// the count reductions — are paid once per pair. A pair whose keys need 31
-// bits is counted as two rounds.
-template <int NT, int SLOTS>
-__global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount_pair(const uint32_t* __restrict__ keys,
-                                                      const uint32_t* __restrict__ skeys, WorkBins w,
-                                                      const uint64_t* nw_dev, uint64_t cap,
-                                                      uint64_t* wb_nnz) {
-    constexpr int PER = 4096 / NT;
-    extern __shared__ __align__(16) uint32_t table[];  // SLOTS + 32 per-lane dummies
-    __shared__ RawDesc s_d[8];                          // bin v of this CTA -> slot v % 8
-    __shared__ uint32_t s_cnt[2];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const uint64_t nw = *nw_dev;
-    const uint64_t G = gridDim.x;
-    for (int i = tid; i < (SLOTS + 32) / 4; i += NT)
-        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
-    const uint64_t b0 = blockIdx.x;
-    if (tid == 0) {
-        s_cnt[0] = s_cnt[1] = 0;
-        for (int q = 0; q < 8; ++q) stage_desc(s_d[q], w, b0 + q * G, nw);
-        cp_async_wait_all();
-    }
-    __syncthreads();
-    // insert PER keys of one bin (tag already applied); returns fresh count
-    auto insert = [&](const uint32_t (&kk)[PER], uint32_t (&h)[PER]) -> uint32_t {
-        uint32_t old[PER];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const uint32_t hk =
-                static_cast<uint32_t>((static_cast<uint64_t>(kk[j] * 0x9E3779B1u) * SLOTS) >> 32);
-            h[j] = kk[j] == CNT_EMPTY ? SLOTS + lane : hk;
-        }
-#pragma unroll
-        for (int j = 0; j < PER; ++j) old[j] = atomicCAS(&table[h[j]], CNT_EMPTY, kk[j]);
-        uint32_t fresh = 0, pend = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            fresh += (old[j] == CNT_EMPTY) & (kk[j] != CNT_EMPTY);
-            pend |= static_cast<uint32_t>(old[j] != CNT_EMPTY && old[j] != kk[j]) << j;
-        }
-        while (pend) {
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                if (!((pend >> j) & 1u)) continue;
-                const uint32_t s = h[j] + 1 == SLOTS ? 0u : h[j] + 1;
-                const uint32_t o = atomicCAS(&table[s], CNT_EMPTY, kk[j]);
-                h[j] = s;
-                if (o == CNT_EMPTY) fresh += 1;
-                if (o == CNT_EMPTY || o == kk[j]) pend &= ~(1u << j);
-            }
-        }
-        return fresh;
-    };
-    uint32_t kA[PER], kB[PER], nA[PER], nB[PER];
-    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[0], cap), kA);
-    cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[1], cap), kB);
-    for (uint32_t it = 0; b0 + 2ull * it * G < nw; ++it) {
-        const uint32_t v = 2 * it;  // this pair: bins v and v + 1 of this CTA
-        const uint64_t bA = b0 + v * G, bB = bA + G;
-        // next pair's keys in flight
-        cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[(v + 2) & 7], cap), nA);
-        cnt_keys<NT>(keys, skeys, cnt_desc_smem(s_d[(v + 3) & 7], cap), nB);
-        const bool tag = s_d[v & 7].keybits <= 30 && s_d[(v + 1) & 7].keybits <= 30;
-        uint32_t hA[PER], hB[PER];
-        if (tag) {
-#pragma unroll
-            for (int j = 0; j < PER; ++j)
-                if (kB[j] != CNT_EMPTY) kB[j] |= 0x80000000u;
-            const uint32_t fa = insert(kA, hA), fb = insert(kB, hB);
-            const uint32_t ra = __reduce_add_sync(FULL, fa), rb = __reduce_add_sync(FULL, fb);
-            if (lane == 0) {
-                atomicAdd(&s_cnt[0], ra);
-                atomicAdd(&s_cnt[1], rb);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                table[hA[j]] = CNT_EMPTY;
-                table[hB[j]] = CNT_EMPTY;
-            }
-        } else {  // two rounds: bin A, then bin B
-            const uint32_t ra = __reduce_add_sync(FULL, insert(kA, hA));
-            if (lane == 0) atomicAdd(&s_cnt[0], ra);
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < PER; ++j) table[hA[j]] = CNT_EMPTY;
-            __syncthreads();
-            const uint32_t rb = __reduce_add_sync(FULL, insert(kB, hB));
-            if (lane == 0) atomicAdd(&s_cnt[1], rb);
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < PER; ++j) table[hB[j]] = CNT_EMPTY;
-        }
-        if (tid == 0) {
-            // merged items are already distinct; a valid list has no other
-            // bin above the capacity
-            const RawDesc& da = s_d[v & 7];
-            const RawDesc& db = s_d[(v + 1) & 7];
-            if (bA < nw) wb_nnz[bA] = (da.flags & 2u) ? da.n : s_cnt[0];
-            if (bB < nw) wb_nnz[bB] = (db.flags & 2u) ? db.n : s_cnt[1];
-            s_cnt[0] = s_cnt[1] = 0;
-            stage_desc(s_d[v & 7], w, b0 + (v + 8) * G, nw);  // slots of this pair are free
-            stage_desc(s_d[(v + 1) & 7], w, b0 + (v + 9) * G, nw);
-            cp_async_wait_group<2>();  // the pair after next has landed
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            kA[j] = nA[j];
-            kB[j] = nB[j];
-        }
-    }
-}
-
 }  // namespace pbg

@@ -530,10 +530,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         __syncthreads();
         *res = scr;
         *rshift = 0;  // row starts from the bucket ends if nothing merges
-        bool dupz = false;
-        if (distinct < n)
-            for (uint32_t i = tid + 1; i < n; i += SM_NT) dupz |= sm.k[scr][i] == sm.k[scr][i - 1];
-        if (distinct < n && __syncthreads_or(dupz)) {
+        if (distinct < n) {  // exact count: duplicates present
             *res = in;
             *rshift = -1;
             return merge_dups(sm, scr, in, n);
@@ -592,11 +589,12 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         sorted = in;
         other = scr;
     }
-    // ---- 3. merge duplicates (none when the count kernel saw n distinct keys)
-    bool dup = false;
-    if (distinct < n)
-        for (uint32_t i = tid + 1; i < n; i += SM_NT) dup |= sm.k[sorted][i] == sm.k[sorted][i - 1];
-    if (distinct < n && __syncthreads_or(dup)) {
+    // ---- 3. merge duplicates. The count kernel's distinct count is exact:
+    // fewer distinct keys than tuples means there are duplicates, so no
+    // adjacent-key check pass is needed to find out (a third of C2's bins
+    // hold one duplicate pair)
+    if (distinct < n) {
+        __syncthreads();  // the rank pass's writes of `sorted`
         *res = other;
         return merge_dups(sm, sorted, other, n);
     }
