@@ -735,7 +735,6 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
         static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
-        static const bool cnt_tma = getenv("PBG_CNT_TMA") && atoi(getenv("PBG_CNT_TMA")) != 0;  // A/B hook
         auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
             static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
             const int shape = (cnt_v1 ? 2 : 0) + (big_table ? 1 : 0);
@@ -760,23 +759,6 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
             } else {
                 if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
             }
-        } else if (big_table && cnt_tma) {
-            // k_bincount3 has no skeys parameter: wrap it (main-buffer bins only)
-            constexpr int S3 = 19456;  // 2 CTAs per SM: 2 x (76 KB table + 32 KB ring)
-            const size_t smem3 = (S3 + 32 + 2 * 4096) * 4;
-            static std::atomic<bool> a3[64] = {};
-            if (!a3[ctx->device & 63]) {
-                CUDA_TRY(cudaFuncSetAttribute(k_bincount3<S3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(smem3)));
-                CUDA_TRY(cudaFuncSetAttribute(k_bincount3<S3>,
-                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                a3[ctx->device & 63] = true;
-            }
-            int per_sm = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bincount3<S3>, 1024, smem3);
-            k_bincount3<S3><<<static_cast<unsigned>(std::min<uint64_t>(
-                                  wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms)),
-                              1024, smem3, st>>>(keys, w, nw_dev, cap, wb_nnz);
         } else if (big_table) {
             if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
         } else {

@@ -897,109 +897,4 @@ __global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount2(const uin
     }
 }
 
-// k_bincount2 with the keys staged by TMA: thread 0 copies bin b + 2G's
-// keys into a 2-stage shared ring (cp.async.bulk, mbarrier completion)
-// while the CTA counts bin b, so a thread's key load is one LDS.128 instead
-// of a predicated global vector load with its address arithmetic and
-// masking (~50 of the ~160 instructions per thread and bin). The table
-// shrinks to fit the ring at 2 CTAs per SM. Main-buffer bins only (they
-// start 16-byte aligned and are padded to 4 tuples): the big-table shape,
-// used when no bin is a heavy row.
-template <int SLOTS>
-__global__ void __launch_bounds__(1024, 2) k_bincount3(const uint32_t* __restrict__ keys, WorkBins w,
-                                                       const uint64_t* nw_dev, uint64_t cap,
-                                                       uint64_t* wb_nnz) {
-    constexpr int NT = 1024, PER = 4;
-    extern __shared__ __align__(16) uint32_t table[];  // SLOTS + 32 dummies, then ring[2][4096]
-    uint32_t* ring = table + SLOTS + 32;
-    __shared__ RawDesc s_d[4];
-    __shared__ __align__(8) unsigned long long mbar[2];
-    __shared__ uint32_t s_cnt;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const uint64_t nw = *nw_dev;
-    const uint64_t G = gridDim.x;
-    for (int i = tid; i < (SLOTS + 32) / 4; i += NT)
-        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
-    const uint64_t b0 = blockIdx.x;
-    auto issue = [&](const RawDesc& d, int r) {  // thread 0: keys of a bin into ring r
-        const CntDesc c = cnt_desc_smem(d, cap);
-        if (c.n == 0) return;
-        const uint32_t bytes = (c.n * 4u + 15u) & ~15u;
-        fence_proxy_async_smem();
-        mbar_expect_tx(&mbar[r], bytes);
-        bulk_g2s(ring + r * 4096, keys + c.off, bytes, &mbar[r]);
-    };
-    if (tid == 0) {
-        s_cnt = 0;
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
-        for (int q = 0; q < 4; ++q) stage_desc(s_d[q], w, b0 + q * G, nw);
-        cp_async_wait_all();
-        issue(s_d[0], 0);
-        issue(s_d[1], 1);
-    }
-    __syncthreads();
-    uint32_t par = 0;  // bit r: phase of ring r's mbarrier
-    for (uint32_t v = 0; b0 + static_cast<uint64_t>(v) * G < nw; ++v) {
-        const uint64_t b = b0 + static_cast<uint64_t>(v) * G;
-        const int r = v & 1;
-        const CntDesc d = cnt_desc_smem(s_d[v & 3], cap);
-        uint32_t kk[PER];
-        if (d.n) {
-            mbar_wait(&mbar[r], (par >> r) & 1u);
-            par ^= 1u << r;
-            const uint32_t i = 4u * tid;
-            uint4 q = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
-            if (i < d.n) q = reinterpret_cast<const uint4*>(ring + r * 4096)[tid];
-            kk[0] = q.x;
-            kk[1] = i + 1 < d.n ? q.y : CNT_EMPTY;
-            kk[2] = i + 2 < d.n ? q.z : CNT_EMPTY;
-            kk[3] = i + 3 < d.n ? q.w : CNT_EMPTY;
-        } else {
-#pragma unroll
-            for (int j = 0; j < PER; ++j) kk[j] = CNT_EMPTY;
-        }
-        uint32_t h[PER], old[PER];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const uint32_t hk =
-                static_cast<uint32_t>((static_cast<uint64_t>(kk[j] * 0x9E3779B1u) * SLOTS) >> 32);
-            h[j] = kk[j] == CNT_EMPTY ? SLOTS + lane : hk;
-        }
-#pragma unroll
-        for (int j = 0; j < PER; ++j) old[j] = atomicCAS(&table[h[j]], CNT_EMPTY, kk[j]);
-        uint32_t fresh = 0, pend = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            fresh += (old[j] == CNT_EMPTY) & (kk[j] != CNT_EMPTY);
-            pend |= static_cast<uint32_t>(old[j] != CNT_EMPTY && old[j] != kk[j]) << j;
-        }
-        while (pend) {
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                if (!((pend >> j) & 1u)) continue;
-                const uint32_t s = h[j] + 1 == SLOTS ? 0u : h[j] + 1;
-                const uint32_t o = atomicCAS(&table[s], CNT_EMPTY, kk[j]);
-                h[j] = s;
-                if (o == CNT_EMPTY) fresh += 1;
-                if (o == CNT_EMPTY || o == kk[j]) pend &= ~(1u << j);
-            }
-        }
-        fresh = __reduce_add_sync(FULL, fresh);
-        if (lane == 0) atomicAdd(&s_cnt, fresh);
-        __syncthreads();  // ring r read, all inserts done
-#pragma unroll
-        for (int j = 0; j < PER; ++j) table[h[j]] = CNT_EMPTY;
-        if (tid == 0) {
-            RawDesc& dm = s_d[v & 3];
-            wb_nnz[b] = (dm.flags & 2u) ? dm.n : s_cnt;
-            s_cnt = 0;
-            stage_desc(dm, w, b0 + (v + 4) * G, nw);  // slot of bin v is free: bin v + 4
-            cp_async_wait_group<2>();                  // bin v + 2's descriptor has landed
-            issue(s_d[(v + 2) & 3], r);                // its keys into the ring just read
-        }
-        __syncthreads();
-    }
-}
-
 }  // namespace pbg
