@@ -1503,6 +1503,35 @@ int pbg_context_symbolic(pbg_context* ctx, const pbg_config* cfg_in, uint64_t* p
         for (uint64_t i = 0; i < k; ++i) per_column_flop[i] = off[i + 1] - off[i];
     }
     if (!per_bin_flop && !bin_row_starts) return PBG_OK;
+    // uniform layout (always the first step; the final one unless balanced
+    // bins are asked for and a bin exceeds the L2 budget): on the device,
+    // from the row-flop prefix — no pass over m on the host
+    const uint32_t nb = ctx->rep.nbins ? ctx->rep.nbins : 1;
+    const uint64_t rpb = m ? (m + nb - 1) / nb : 0;
+    if (m && ctx->flop) {
+        DevBuf& tmp = ctx->ck;  // small scratch: nb + 1 starts, nb flop
+        int rc = grow(tmp, (nb + 1) * 4 + nb * 8 + 16);
+        if (rc) return rc;
+        auto* dstarts = static_cast<uint32_t*>(tmp.p);
+        auto* dpbf = reinterpret_cast<uint64_t*>(static_cast<char*>(tmp.p) + (((nb + 1) * 4 + 7) & ~size_t(7)));
+        pbg::k_ref_layout_uniform<<<blocks_for(nb + 1, 256), 256>>>(static_cast<const uint64_t*>(ctx->row_off.p),
+                                                              m, nb, rpb, dstarts, dpbf);
+        std::vector<uint32_t> starts(nb + 1);
+        std::vector<uint64_t> pbf(nb);
+        CUDA_TRY(cudaMemcpy(starts.data(), dstarts, (nb + 1) * 4, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(pbf.data(), dpbf, nb * 8, cudaMemcpyDeviceToHost));
+        bool uniform_final = !cfg.balanced_bins;
+        if (!uniform_final) {
+            const uint32_t tb = ceil_log2_u64(rpb) + ctx->col_bits <= 32 ? 12 : 16;
+            const uint64_t maxb = *std::max_element(pbf.begin(), pbf.end());
+            uniform_final = !(maxb * tb > cfg.l2_bytes);
+        }
+        if (uniform_final) {
+            if (per_bin_flop) std::memcpy(per_bin_flop, pbf.data(), nb * 8);
+            if (bin_row_starts) std::memcpy(bin_row_starts, starts.data(), (nb + 1) * 4);
+            return PBG_OK;
+        }
+    }
     std::vector<uint64_t> rf(m);
     if (m && ctx->flop) {
         if (ctx->rowflop32) {

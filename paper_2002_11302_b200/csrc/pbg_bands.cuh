@@ -65,6 +65,22 @@ __global__ void k_colflop_each(const uint64_t* __restrict__ a_colptr,
     if (i < k) out[i] = (a_colptr[i + 1] - a_colptr[i]) * (b_rowptr[i + 1] - b_rowptr[i]);
 }
 
+// The reference's uniform bin layout (pb_spgemm.cpp:107-137: nbins ranges
+// of ceil(m / nbins) rows) from the row-flop prefix the symbolic phase keeps
+// on the device: starts[b] = min(b * rpb, m), per_bin_flop[b] = prefix
+// difference. Replaces a host pass over all m row counters per report.
+__global__ void k_ref_layout_uniform(const uint64_t* __restrict__ row_off, uint64_t m, uint32_t nb,
+                                     uint64_t rpb, uint32_t* starts, uint64_t* pbf) {
+    const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (b > nb) return;
+    const uint64_t s = b * rpb < m ? b * rpb : m;
+    starts[b] = static_cast<uint32_t>(s);
+    if (b < nb) {
+        const uint64_t e = (b + 1) * rpb < m ? (b + 1) * rpb : m;
+        pbf[b] = row_off[e] - row_off[s];
+    }
+}
+
 constexpr uint64_t SLAB_LONG = 64;  // columns longer than this are walked by a warp
 
 // cnt[j] = #{p in column j : r0 <= rowids[p] < r1}
