@@ -234,6 +234,14 @@ int pbg_multiply_device_band(pbg_context* ctx, const pbg_csx_view* a_csc, const 
 int pbg_context_checksum(pbg_context* ctx, uint64_t row_base, void* stream, uint64_t* out,
                          double* vsum);
 
+/* Development aid (no reference counterpart): the work bins of the context's
+ * last product -- the sort kernel's units of work (GPU bins and the key-range
+ * pieces of heavy rows): tuples, key bits, flags (bit0 scratch buffer, bit1
+ * merged, bit2 heavy sub-bin) and distinct keys of the first min(cap, *nw)
+ * work bins; any output array may be NULL. */
+int pbg_context_workbins(pbg_context* ctx, uint64_t cap, uint64_t* nw, uint64_t* n,
+                         uint32_t* keybits, uint32_t* flags, uint64_t* nnz);
+
 /* ---- reference helpers with no device work --------------------------- */
 /* choose_nbins (pb_spgemm.cpp:10-18) */
 uint32_t pbg_choose_nbins(uint64_t flop, uint32_t nrows, uint64_t l2_bytes, uint32_t tuple_bytes);

@@ -86,6 +86,7 @@ PBG_EXPORTS = {
     "pbg_multiply_device_band": (C.c_int, [vp, P(CsxView), P(CsxView), u32, u32, P(Config), vp,
                                            P(u64), P(Report)]),
     "pbg_context_checksum": (C.c_int, [vp, u64, vp, vp, P(f64)]),
+    "pbg_context_workbins": (C.c_int, [vp, u64, vp, vp, vp, vp, vp]),
     "pbg_choose_nbins": (u32, [u64, u32, u64, u32]),
 }
 

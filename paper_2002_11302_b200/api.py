@@ -390,6 +390,22 @@ class DeviceContext:
             _raise(rc)
         return int(out[0]), int(out[1]), int(out[2]), vs.value
 
+    def workbins(self):
+        """Development aid: (tuples, key bits, flags, distinct keys) arrays of
+        the last product's work bins (the sort kernel's units of work)."""
+        nw = C.c_uint64(0)
+        rc = self._lib.pbg_context_workbins(self._ctx, 0, C.byref(nw), None, None, None, None)
+        if rc:
+            _raise(rc)
+        c = nw.value
+        n, nnz = np.zeros(c, np.uint64), np.zeros(c, np.uint64)
+        kb, fl = np.zeros(c, np.uint32), np.zeros(c, np.uint32)
+        rc = self._lib.pbg_context_workbins(self._ctx, c, C.byref(nw), n.ctypes.data, kb.ctypes.data,
+                                            fl.ctypes.data, nnz.ctypes.data)
+        if rc:
+            _raise(rc)
+        return n, kb, fl, nnz
+
     def result_pointers(self):
         rp, ci, va = C.c_void_p(), C.c_void_p(), C.c_void_p()
         rc = self._lib.pbg_context_result(self._ctx, C.byref(rp), C.byref(ci), C.byref(va))

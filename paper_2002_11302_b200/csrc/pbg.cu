@@ -619,7 +619,12 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
             hc.svals = static_cast<double*>(ctx->svals.p);
             nitems = H;
             static std::atomic<bool> hv_attr[64] = {};  // per device; a concurrent double set is benign
+            static const bool hv_v1 = getenv("PBG_HV_SCATTER_V1") && atoi(getenv("PBG_HV_SCATTER_V1")) != 0;  // A/B hook
             if (!hv_attr[ctx->device & 63]) {
+                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(sizeof(HvScatter2Smem))));
+                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter2,
+                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(sizeof(HvScatterSmem))));
                 CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter,
@@ -663,8 +668,15 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                 const uint64_t nout = hs[S_ITEMS];
                 Items nxt{};
                 if ((rc = items_of(curset ^ 1, nout, &nxt))) return rc;
-                k_hv_scatter<<<gt, HV_NT, sizeof(HvScatterSmem), st>>>(hc, cur, nitems, tpos, titem,
-                                                                      sh, d, hist);
+                if (hv_v1) {
+                    k_hv_scatter<<<gt, HV_NT, sizeof(HvScatterSmem), st>>>(hc, cur, nitems, tpos, titem,
+                                                                          sh, d, hist);
+                } else {
+                    const unsigned g2 = static_cast<unsigned>(
+                        std::min<uint64_t>(ntiles, (HV_TILE <= 4096 ? 2ull : 1ull) * ctx->num_sms));
+                    k_hv_scatter2<<<g2, HV2_NT, sizeof(HvScatter2Smem), st>>>(hc, cur, nitems, tpos,
+                                                                             titem, sh, d, hist);
+                }
                 k_hv_children<<<gi, HV_PT, 0, st>>>(hc, cur, nitems, sh, d, hist, cpos, nxt);
                 L += 7;
                 cur = nxt;
@@ -2339,6 +2351,23 @@ int pbg_context_checksum(pbg_context* ctx, uint64_t row_base, void* stream, uint
     out[1] = hs[1];
     out[2] = hs[2];
     if (vsum) std::memcpy(vsum, &hs[3], 8);
+    return PBG_OK;
+}
+
+int pbg_context_workbins(pbg_context* ctx, uint64_t cap, uint64_t* nw_out, uint64_t* n,
+                         uint32_t* keybits, uint32_t* flags, uint64_t* nnz) {
+    if (!ctx || !ctx->have_result || !nw_out) return fail(PBG_ERR_ARG, "no product in this context");
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    unsigned long long nw = 0;
+    CUDA_TRY(cudaMemcpy(&nw, static_cast<unsigned long long*>(ctx->zero_block.p) + S_NWORK, 8,
+                        cudaMemcpyDeviceToHost));
+    *nw_out = nw;
+    const uint64_t c = std::min<uint64_t>(cap, nw);
+    if (c && n) CUDA_TRY(cudaMemcpy(n, ctx->wb[1].p, c * 8, cudaMemcpyDeviceToHost));
+    if (c && keybits) CUDA_TRY(cudaMemcpy(keybits, ctx->wb[5].p, c * 4, cudaMemcpyDeviceToHost));
+    if (c && flags) CUDA_TRY(cudaMemcpy(flags, ctx->wb[6].p, c * 4, cudaMemcpyDeviceToHost));
+    if (c && nnz) CUDA_TRY(cudaMemcpy(nnz, ctx->wb_nnz.p, c * 8, cudaMemcpyDeviceToHost));
     return PBG_OK;
 }
 

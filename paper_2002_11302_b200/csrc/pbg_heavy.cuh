@@ -32,9 +32,18 @@
 namespace pbg {
 
 constexpr int HV_NT = 512;
-constexpr int HV_TILE = 4096;        // tuples per split tile
+#ifndef PBG_HV_TILE
+#define PBG_HV_TILE 4096
+#endif
+constexpr int HV_TILE = PBG_HV_TILE; // tuples per split tile (4096 or 8192)
 constexpr int HV_DENSE_BITS = 12;    // key range of a dense-reduced item (4096 columns)
 constexpr int HV_MAXD = 10;          // digit bits per split pass (<= 1024 buckets)
+#ifndef PBG_HV_GREEDY
+#define PBG_HV_GREEDY 0              // tuning hook, see hv_plan_item
+#endif
+#ifndef PBG_DENSE_MIN
+#define PBG_DENSE_MIN 0              // tuning hook, see k_hv_children
+#endif
 
 // SORT: <= cap tuples, a work bin of the sort kernel. SPLIT: split on the
 // next key bits. DENSE: > cap tuples in a key range <= 2^HV_DENSE_BITS,
@@ -174,6 +183,16 @@ __device__ __forceinline__ uint32_t warp_bucket_rank(uint32_t* cnt, uint32_t bk,
     return hb + static_cast<uint32_t>(lane - head);
 }
 
+// Tile histograms. A CTA takes a contiguous range of tiles, so consecutive
+// tiles mostly belong to the same item: their counts pile up in shared memory
+// and reach the item's global counters once per item and CTA (one global
+// atomic per bucket and TILE serialised on the few hundred counters of the
+// heaviest rows), with no barrier between tiles of one item. A thread takes 8
+// CONSECUTIVE keys per 4096-key chunk (two 16-byte loads from the 16-byte
+// boundary below the tile; the stream is run-ordered, so they mostly share a
+// bucket) and adds each run of equal buckets once. (The lane-striped version
+// with warp_bucket_rank spent ~45 instructions per tuple on ballots and
+// shuffles and ran issue-bound at 2.1 TB/s.)
 __global__ void __launch_bounds__(HV_NT) k_hv_hist(HeavyCtx c, Items it, uint64_t nitems,
                                                    const uint64_t* __restrict__ tile_pos,
                                                    const uint32_t* __restrict__ tile_item,
@@ -182,30 +201,74 @@ __global__ void __launch_bounds__(HV_NT) k_hv_hist(HeavyCtx c, Items it, uint64_
     const int tid = threadIdx.x;
     const uint64_t ntiles = tile_pos[nitems];
     const uint32_t nbk = 1u << d, s2 = sh - d, mask = nbk - 1u;
-    constexpr int TPT = HV_TILE / HV_NT;  // 8 keys per thread, all loads in flight together
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    constexpr int CHUNKS = HV_TILE / (8 * HV_NT);  // 4096-key chunks per tile
+    static_assert(CHUNKS >= 1 && CHUNKS * 8 * HV_NT == HV_TILE, "8 keys per thread and chunk");
+    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = blockIdx.x * per;
+    const uint64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
+    if (t0 >= t1) return;
+    for (uint32_t q = tid; q < nbk; q += HV_NT) cnt[q] = 0;
+    uint32_t item = tile_item[t0];
+    __syncthreads();
+    for (uint64_t t = t0; t < t1; ++t) {
         const HvTile tl = hv_tile(it, tile_pos, tile_item, t);
+        if (tl.i != item) {  // (CTA-uniform) flush the finished item's counts
+            __syncthreads();
+            uint32_t* h = hist + static_cast<uint64_t>(item) * nbk;
+            for (uint32_t q = tid; q < nbk; q += HV_NT) {
+                const uint32_t v = cnt[q];
+                if (v) atomicAdd(h + q, v);
+                cnt[q] = 0;
+            }
+            item = tl.i;
+            __syncthreads();
+        }
         const uint32_t buf = it.buf[tl.i];
-        const uint32_t* K = (buf ? c.skeys : c.keys) + item_base(c, it.h[tl.i], buf) +
-                            it.loc[tl.i] + tl.start;
-        uint32_t kk[TPT];
+        const uint64_t abs0 = item_base(c, it.h[tl.i], buf) + it.loc[tl.i] + tl.start;
+        const uint32_t sk = static_cast<uint32_t>(abs0 & 3u);
+        const uint32_t* K = (buf ? c.skeys : c.keys) + (abs0 - sk);  // 16-byte aligned
+        const uint32_t end = sk + tl.m;                               // valid: [sk, end)
+        uint4 q0[CHUNKS], q1[CHUNKS];
 #pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const uint32_t q = tid + j * HV_NT;
-            kk[j] = q < tl.m ? __ldcs(K + q) : 0u;
+        for (int ch = 0; ch < CHUNKS; ++ch) {
+            const uint32_t e0 = 8u * (tid + ch * HV_NT);
+            q0[ch] = make_uint4(0, 0, 0, 0);
+            q1[ch] = q0[ch];
+            if (e0 < end) q0[ch] = __ldcs(reinterpret_cast<const uint4*>(K + e0));
+            if (e0 + 4 < end) q1[ch] = __ldcs(reinterpret_cast<const uint4*>(K + e0 + 4));
         }
-        for (uint32_t q = tid; q < nbk; q += HV_NT) cnt[q] = 0;
-        __syncthreads();
+        // the shift can push up to 3 keys past the HV_TILE covered above
+        uint32_t xk = 0;
+        const bool xv = tid < 3 && HV_TILE + tid < end;
+        if (xv) xk = __ldcs(K + HV_TILE + tid);
 #pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const uint32_t q = tid + j * HV_NT;
-            warp_bucket_rank(cnt, (kk[j] >> s2) & mask, q < tl.m);
+        for (int ch = 0; ch < CHUNKS; ++ch) {
+            const uint32_t e0 = 8u * (tid + ch * HV_NT);
+            const uint32_t kk[8] = {q0[ch].x, q0[ch].y, q0[ch].z, q0[ch].w,
+                                    q1[ch].x, q1[ch].y, q1[ch].z, q1[ch].w};
+            uint32_t cur = 0xffffffffu, len = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t e = e0 + j;
+                const bool valid = e >= sk && e < end;
+                const uint32_t bk = (kk[j] >> s2) & mask;
+                if (valid && bk == cur) {
+                    ++len;
+                } else {
+                    if (len) atomicAdd(&cnt[cur], len);
+                    cur = valid ? bk : 0xffffffffu;
+                    len = valid ? 1u : 0u;
+                }
+            }
+            if (len) atomicAdd(&cnt[cur], len);
         }
-        __syncthreads();
-        uint32_t* h = hist + static_cast<uint64_t>(tl.i) * nbk;
-        for (uint32_t q = tid; q < nbk; q += HV_NT)
-            if (cnt[q]) atomicAdd(h + q, cnt[q]);
-        __syncthreads();
+        if (xv) atomicAdd(&cnt[(xk >> s2) & mask], 1u);
+    }
+    __syncthreads();
+    uint32_t* h = hist + static_cast<uint64_t>(item) * nbk;
+    for (uint32_t q = tid; q < nbk; q += HV_NT) {
+        const uint32_t v = cnt[q];
+        if (v) atomicAdd(h + q, v);
     }
 }
 
@@ -238,6 +301,36 @@ __device__ uint32_t hv_plan_item(PlanSmem& sm, const uint32_t* cnt_g, uint32_t n
     }
     if (tid == 0) sm.st[nbk] = tot;
     __syncthreads();
+#if PBG_HV_GREEDY
+    // greedy grouping by one thread: a child takes consecutive buckets while
+    // their sum stays <= cap (children ~cap/2 on average under the window
+    // rule below; fuller children mean fewer work bins for the count and
+    // sort kernels). <= 1024 buckets per item: microseconds.
+    if (tid == 0) {
+        uint32_t run = 0, ci = 0;
+        bool open = false;
+        for (uint32_t q = 0; q < nbk; ++q) {
+            const uint32_t vq = sm.st[q + 1] - sm.st[q];
+            uint32_t f = 0;
+            if (vq) {
+                if (!open || run + static_cast<uint64_t>(vq) > cap) {
+                    f = 1;
+                    run = vq;
+                    open = true;
+                } else {
+                    run += vq;
+                }
+            }
+            sm.fl[q] = (ci << 1) | f;
+            ci += f;
+        }
+        sm.s_warp[0] = ci;
+    }
+    __syncthreads();
+    const uint32_t nchild = sm.s_warp[0];
+    __syncthreads();
+    return nchild;
+#else
     const uint32_t T = static_cast<uint32_t>(cap / 2);
     uint32_t starts = 0, f[HV_PB];
 #pragma unroll
@@ -265,6 +358,7 @@ __device__ uint32_t hv_plan_item(PlanSmem& sm, const uint32_t* cnt_g, uint32_t n
     }
     __syncthreads();
     return nchild;
+#endif
 }
 
 // per item: bucket counts -> scatter cursors (bucket starts), child count
@@ -358,6 +452,129 @@ __global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, u
     }
 }
 
+// k_hv_scatter2: the same split with the tiles staged by TMA. A producer warp
+// (warp HV_NT/32, one elected lane) walks the CTA's tiles one ahead of the 512
+// consumer threads: it resolves the tile descriptor (tile -> item -> buffer
+// addresses: three dependent global round trips that every thread of
+// k_hv_scatter paid per tile), publishes it in shared memory and starts two
+// bulk copies (keys, values; from the 16-byte boundary below the tile) into
+// the free one of two buffers, completion on that buffer's `full` mbarrier.
+// Consumers rank the tile's keys from shared memory (no tuple registers held
+// across the reservation round trip), reserve, store, and hand the buffer
+// back through its `empty` mbarrier. ncu on a C3 round had k_hv_scatter at
+// 50 % long-scoreboard stalls, 28 % issue, 3.1 TB/s.
+struct HvDesc {
+    uint32_t* dk;      // destination of the item's tuples (other buffer)
+    double* dv;
+    uint32_t* cursor;  // the item's bucket cursors
+    uint64_t n;        // tuples of the item (PBG_CHECKED bound)
+    uint32_t m;        // tuples in the tile
+    uint32_t sk, sv;   // the tile starts sk keys / sv values into the buffer
+    uint32_t pad;
+};
+struct HvScatter2Smem {
+    uint32_t k[2][HV_TILE + 4];
+    double v[2][HV_TILE + 2];
+    uint32_t cnt[1 << HV_MAXD];
+    uint32_t gb[1 << HV_MAXD];
+    HvDesc desc[2];
+    unsigned long long full[2], empty[2];
+};
+constexpr int HV2_NC = HV_TILE <= 4096 ? HV_TILE / 8 : 960;  // consumer threads (a CTA holds <= 1024)
+constexpr int HV2_NT = HV2_NC + 32;  // consumers + the producer warp
+
+__global__ void __launch_bounds__(HV2_NT, HV_TILE <= 4096 ? 2 : 1) k_hv_scatter2(HeavyCtx c, Items it, uint64_t nitems,
+                                                           const uint64_t* __restrict__ tile_pos,
+                                                           const uint32_t* __restrict__ tile_item,
+                                                           uint32_t sh, uint32_t d, uint32_t* cursor) {
+    extern __shared__ __align__(16) unsigned char hv2_raw[];
+    HvScatter2Smem& sm = *reinterpret_cast<HvScatter2Smem*>(hv2_raw);
+    const int tid = threadIdx.x;
+    const uint64_t ntiles = tile_pos[nitems];
+    const uint32_t nbk = 1u << d, s2 = sh - d, mask = nbk - 1u;
+    if (tid == 0) {
+        mbar_init(&sm.full[0], 1);
+        mbar_init(&sm.full[1], 1);
+        mbar_init(&sm.empty[0], 1);
+        mbar_init(&sm.empty[1], 1);
+    }
+    __syncthreads();
+    if (tid >= HV2_NC) {  // ---- producer warp
+        if (tid != HV2_NC) return;
+        uint32_t i = 0;
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+            const int s = i & 1;
+            if (i >= 2) mbar_wait(&sm.empty[s], ((i >> 1) - 1) & 1);
+            const HvTile tl = hv_tile(it, tile_pos, tile_item, t);
+            const uint32_t buf = it.buf[tl.i], h = it.h[tl.i];
+            const uint64_t loc = it.loc[tl.i];
+            const uint64_t sbase = item_base(c, h, buf) + loc + tl.start;
+            const uint64_t dbase = item_base(c, h, buf ^ 1u) + loc;
+            const uint64_t sk = sbase & 3u, sv = sbase & 1u;
+            HvDesc& D = sm.desc[s];
+            D.dk = (buf ? c.keys : c.skeys) + dbase;
+            D.dv = (buf ? c.vals : c.svals) + dbase;
+            D.cursor = cursor + static_cast<uint64_t>(tl.i) * nbk;
+            D.n = it.n[tl.i];
+            D.m = tl.m;
+            D.sk = static_cast<uint32_t>(sk);
+            D.sv = static_cast<uint32_t>(sv);
+            const uint32_t kb = static_cast<uint32_t>(((tl.m + sk) * 4 + 15) & ~15ull);
+            const uint32_t vb = static_cast<uint32_t>(((tl.m + sv) * 8 + 15) & ~15ull);
+            mbar_expect_tx(&sm.full[s], kb + vb);
+            bulk_g2s(sm.k[s], (buf ? c.skeys : c.keys) + (sbase - sk), kb, &sm.full[s]);
+            bulk_g2s(sm.v[s], (buf ? c.svals : c.vals) + (sbase - sv), vb, &sm.full[s]);
+        }
+        return;
+    }
+    // ---- consumers (threads 0 .. HV2_NC-1; barriers are named: the producer
+    // warp takes no part)
+    constexpr int TPT = (HV_TILE + HV2_NC - 1) / HV2_NC;  // 8 (9 for 8192-tuple tiles)
+    uint32_t i = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int s = i & 1;
+        for (uint32_t q = tid; q < nbk; q += HV2_NC) sm.cnt[q] = 0;
+        mbar_wait(&sm.full[s], (i >> 1) & 1);
+        named_barrier<1, HV2_NC>();
+        const HvDesc& D = sm.desc[s];
+        const uint32_t m = D.m;
+        const uint32_t* K = sm.k[s] + D.sk;
+        const double* V = sm.v[s] + D.sv;
+        uint32_t rb[TPT];
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const uint32_t q = tid + j * HV2_NC;
+            const bool valid = q < m;
+            const uint32_t bk = valid ? ((K[q] >> s2) & mask) : 0u;
+            const uint32_t r = warp_bucket_rank(sm.cnt, bk, valid);
+            rb[j] = r | (bk << 16);
+        }
+        named_barrier<1, HV2_NC>();
+        {  // one global reservation per non-empty bucket
+            uint32_t* cur = D.cursor;
+            for (uint32_t q = tid; q < nbk; q += HV2_NC) {
+                const uint32_t v = sm.cnt[q];
+                if (v) sm.gb[q] = atomicAdd(cur + q, v);
+            }
+        }
+        named_barrier<1, HV2_NC>();
+        uint32_t* DK = D.dk;
+        double* DV = D.dv;
+#pragma unroll
+        for (int j = 0; j < TPT; ++j) {
+            const uint32_t q = tid + j * HV2_NC;
+            if (q < m) {
+                const uint64_t dst = static_cast<uint64_t>(sm.gb[rb[j] >> 16]) + (rb[j] & 0xffffu);
+                PBG_DCHECK(dst < D.n);
+                DK[dst] = K[q];
+                DV[dst] = V[q];
+            }
+        }
+        named_barrier<1, HV2_NC>();  // buffer s, cnt and gb are free again
+        if (tid == 0) mbar_arrive(&sm.empty[s]);
+    }
+}
+
 // Child descriptors of every item at child_pos (non-SPLIT items are copied).
 // `starts` holds the bucket starts again after the scatter (cursor - count
 // is not needed: the plan is recomputed from the cursors' final values,
@@ -410,7 +627,11 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
             out.h[oo] = in.h[i];
             out.buf[oo] = in.buf[i] ^ 1u;
             out.sh[oo] = s2;
-            out.kind[oo] = cn <= c.cap ? IT_SORT : (s2 <= HV_DENSE_BITS ? IT_DENSE : IT_SPLIT);
+            // a single-bucket child within the dense key range is summed by
+            // k_hv_dense from PBG_DENSE_MIN tuples on (0 = only above cap)
+            const bool dense_ok = s2 <= HV_DENSE_BITS && nb == 1;
+            out.kind[oo] = cn <= c.cap ? ((PBG_DENSE_MIN && dense_ok && cn >= PBG_DENSE_MIN) ? IT_DENSE : IT_SORT)
+                                       : (s2 <= HV_DENSE_BITS ? IT_DENSE : IT_SPLIT);
             out.keylo[oo] = in.keylo[i] + (q << s2);
             out.keybits[oo] = rbits;
         }
@@ -427,11 +648,16 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
 // measured 1.5x slower: these items are popular columns, and L2 atomics
 // serialise per address.)
 constexpr int HV_DENSE = 1 << HV_DENSE_BITS;
+#ifndef PBG_DENSE_AGG
+#define PBG_DENSE_AGG 0  // 0 = off; else the smallest group of equal slots summed by shuffles
+#endif
 #ifndef PBG_DENSE_COPIES
 #define PBG_DENSE_COPIES 1
 #endif
-// DC accumulator copies, warp w adding into copy w % DC (fewer warps contend
-// for a popular column's slot); summed into copy 0 before the write-back
+// DC accumulator copies, lane l adding into copy l % DC (equal popular
+// columns in one instruction's lanes retry each other's CAS; copies per WARP
+// were measured useless: the contention is within the warp); summed into
+// copy 0 before the write-back
 constexpr int HV_DC = PBG_DENSE_COPIES;
 __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64_t nitems) {
     extern __shared__ __align__(16) unsigned char dn_raw[];
@@ -440,7 +666,7 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
     __shared__ uint32_t s_warp[HV_NT / 32 + 1];
     constexpr int PER = HV_DENSE / HV_NT;  // 8
     const int tid = threadIdx.x;
-    double* acc = acc_all + ((tid >> 5) % HV_DC) * HV_DENSE;
+    double* acc = acc_all + (tid % HV_DC) * HV_DENSE;
     for (uint64_t i = blockIdx.x; i < nitems; i += gridDim.x) {
         if (it.kind[i] != IT_DENSE) continue;
         const uint32_t buf = it.buf[i];
@@ -466,6 +692,36 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
                 ks[u] = q < n ? __ldcs(K + q) : 0xffffffffu;
                 vs[u] = q < n ? __ldcs(V + q) : 0.0;
             }
+#if PBG_DENSE_AGG
+            // Popular columns repeat inside one instruction's 32 tuples and an
+            // f64 shared-memory atomicAdd is a CAS loop: k equal slots cost k
+            // rounds. Groups of >= PBG_DENSE_AGG equal slots are summed by a
+            // shuffle butterfly first and added once by their first lane.
+            const int lane = tid & 31;
+#pragma unroll
+            for (int u = 0; u < DU; ++u) {
+                const bool valid = ks[u] != 0xffffffffu;
+                const uint32_t slot = valid ? ks[u] - keylo : 0x80000000u + lane;
+                const uint32_t peers = __match_any_sync(FULL, slot);
+                const bool first = (__ffs(peers) - 1) == lane;
+                const bool big = __popc(peers) >= PBG_DENSE_AGG;
+                uint32_t todo = __ballot_sync(FULL, valid && first && big);
+                double mine = vs[u];
+                while (todo) {
+                    const int L = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const uint32_t g = __shfl_sync(FULL, peers, L);
+                    double t = ((g >> lane) & 1u) ? vs[u] : -0.0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+                    if (lane == L) mine = t;
+                }
+                if (valid && (first || !big)) {
+                    atomicAdd(&acc[slot], mine);
+                    seen[slot] = 1;
+                }
+            }
+#else
 #pragma unroll
             for (int u = 0; u < DU; ++u) {
                 if (ks[u] == 0xffffffffu) continue;
@@ -473,6 +729,7 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
                 atomicAdd(&acc[slot], vs[u]);
                 seen[slot] = 1;
             }
+#endif
         }
         __syncthreads();
         if (HV_DC > 1) {

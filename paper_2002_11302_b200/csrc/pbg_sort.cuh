@@ -62,6 +62,13 @@ constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
 #define PBG_SM_BMAX 128
 #endif
 constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
+// hash pre-merge of a bin when distinct * NUM <= tuples * DEN (tuning hook)
+#ifndef PBG_PM_NUM
+#define PBG_PM_NUM 2
+#endif
+#ifndef PBG_PM_DEN
+#define PBG_PM_DEN 1
+#endif
 #ifndef PBG_RANK_UNROLL
 #define PBG_RANK_UNROLL 1
 #endif
@@ -154,11 +161,15 @@ __device__ __forceinline__ void meta_fetch(const SortArgs& a, SortSmem& sm, int 
     cp_async4(&m.span, a.w.span + b);
 }
 
-// How a work bin reaches shared memory: 1 = TMA bulk copy, 2 = plain loads
-// (unaligned heavy sub-bin), 0 = nothing to load (empty / merged / error).
+// How a work bin reaches shared memory: 1 = TMA bulk copy, 0 = nothing to
+// load (empty / merged / error). A heavy sub-bin may start at any tuple: its
+// copy starts at the 16-byte boundary below, so the bin sits (off & 3) keys /
+// (off & 1) values into the buffer (the buffers' slack covers the shift).
+// A MERGED sub-bin (k_hv_dense: sorted, duplicates summed, <= 4096 entries)
+// takes the same route and is written out unsorted-path-free.
 __device__ __forceinline__ uint32_t bin_kind(const BinMeta& m) {
-    if (m.n == 0 || m.n > SM_CAP || (m.flags & 2u)) return 0;
-    return (m.off & 3u) ? 2 : 1;
+    if (m.n == 0 || m.n > SM_CAP) return 0;
+    return 1;
 }
 
 // Thread 0: start the TMA copy of a kind-1 bin into buffer `buf` (generic-
@@ -167,12 +178,13 @@ __device__ __forceinline__ void issue_tma(const SortArgs& a, SortSmem& sm, int b
                                           const BinMeta& m) {
     const uint32_t* ks = (m.flags & 1u) ? a.skeys : a.keys;
     const double* vs = (m.flags & 1u) ? a.svals : a.vals;
-    const uint32_t kb = static_cast<uint32_t>((m.n * 4 + 15) & ~15ull);
-    const uint32_t vb = static_cast<uint32_t>((m.n * 8 + 15) & ~15ull);
+    const uint64_t sk = m.off & 3u, sv = m.off & 1u;
+    const uint32_t kb = static_cast<uint32_t>(((m.n + sk) * 4 + 15) & ~15ull);
+    const uint32_t vb = static_cast<uint32_t>(((m.n + sv) * 8 + 15) & ~15ull);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&sm.mbar, kb + vb);
-    bulk_g2s(sm.k[buf], ks + m.off, kb, &sm.mbar);
-    bulk_g2s(sm.v[buf], vs + m.off, vb, &sm.mbar);
+    bulk_g2s(sm.k[buf], ks + (m.off - sk), kb, &sm.mbar);
+    bulk_g2s(sm.v[buf], vs + (m.off - sv), vb, &sm.mbar);
 }
 
 // Exclusive scan of the SM_NB u16 counters in index order (8 per thread).
@@ -290,12 +302,18 @@ __device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits, uint32
 }
 
 // Sum equal-key runs of sorted buffer `x` into buffer `y`, compacted.
-// Warp w owns elements [w*PER_WARP, +PER_WARP), lane-striped.
+// Warp w owns elements [w*PER_WARP, +PER_WARP), lane-striped in windows of 32.
+// A warp-shuffle segmented reduction sums each run's part inside a window
+// into the window's first lane of that run (written back in place); the
+// thread of a run's head then adds the leading partial of every following
+// window the run covers: a key repeated r times costs its head r/32 adds
+// instead of r (RMAT's hot columns repeat hundreds of times; the serial
+// per-head loop was 29 % of the sort kernel on a C3 round).
 __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint32_t n) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
     const uint32_t* K = sm.k[x];
-    const double* V = sm.v[x];
+    double* V = sm.v[x];
     uint32_t* KO = sm.k[y];
     double* VO = sm.v[y];
     uint32_t masks[SM_ITEMS];
@@ -303,11 +321,24 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
 #pragma unroll
     for (int it = 0; it < SM_ITEMS; ++it) {
         const uint32_t i = w * SM_PER_WARP + it * 32 + lane;
-        const bool h = i < n && (i == 0 || K[i] != K[i - 1]);
+        const bool in = i < n;
+        const bool h = in && (i == 0 || K[i] != K[i - 1]);
         masks[it] = __ballot_sync(FULL, h);
         heads += __popc(masks[it]);
+        if (masks[it] == __ballot_sync(FULL, in)) continue;  // no duplicate inside this window
+        // segment starts of the window: run heads and lane 0
+        const uint32_t seg = masks[it] | 1u;
+        double v = in ? V[i] : 0.0;
+        const uint32_t above = seg >> 1 >> lane;  // bit j: lane + 1 + j starts a segment
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_down_sync(FULL, v, o);
+            if (lane + o < 32 && (above & ((1u << o) - 1u)) == 0) v += t;
+        }
+        if (in && ((seg >> lane) & 1u)) V[i] = v;
     }
     uint32_t tot;
+    // (the scan's barriers publish the windows' partial sums)
     uint32_t base = block_exclusive_scan<SM_NT>(lane == 0 ? heads : 0u, sm.s_warp32, tot);
     base = __shfl_sync(FULL, base, 0);
 #pragma unroll
@@ -317,7 +348,7 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
             const uint32_t u = base + __popc(masks[it] & lt);
             const uint32_t key = K[i];
             double s = V[i];
-            for (uint32_t e = i + 1; e < n && K[e] == key; ++e) s += V[e];
+            for (uint32_t e = (i | 31u) + 1; e < n && K[e] == key; e += 32) s += V[e];
             KO[u] = key;
             VO[u] = s;
         }
@@ -335,7 +366,7 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
 // turns the slot counts into group starts, values are scattered into their
 // groups and each group is summed by the thread owning its slot.
 __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
-                                  long long& prof_t) {
+                                  const uint32_t* Kin, const double* Vin, long long& prof_t) {
     const int tid = threadIdx.x;
     constexpr uint32_t EMPTY = 0xffffffffu;
     uint32_t* HK = sm.k[scr];
@@ -350,7 +381,7 @@ __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int s
         const uint32_t i = tid + j * SM_NT;
         hr[j] = EMPTY;
         if (i < n) {
-            const uint32_t key = sm.k[in][i];
+            const uint32_t key = Kin[i];
             uint32_t h = (key * 0x9E3779B1u) >> (32 - __builtin_ctz(SM_CAP));
             while (true) {
                 const uint32_t old = atomicCAS(&HK[h], EMPTY, key);
@@ -408,7 +439,7 @@ __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int s
 #pragma unroll
     for (int j = 0; j < SM_ITEMS; ++j) {
         if (hr[j] != EMPTY)
-            sm.v[scr][HK[hr[j] >> 16] + (hr[j] & 0xffffu)] = sm.v[in][tid + j * SM_NT];
+            sm.v[scr][HK[hr[j] >> 16] + (hr[j] & 0xffffu)] = Vin[tid + j * SM_NT];
     }
     __syncthreads();
     PROF_MARK(11);
@@ -429,14 +460,20 @@ __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int s
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
                                    int bits, uint32_t keylo, uint32_t distinct, int* res,
                                    int* rshift, uint64_t P, int* bulk,
-                                   int next_slot, uint64_t next_bin, long long& prof_t) {
+                                   int next_slot, uint64_t next_bin, uint32_t insk, uint32_t insv,
+                                   long long& prof_t) {
     const int tid = threadIdx.x;
     *bulk = 0;
+    // the bin as it arrived: insk keys / insv values into buffer `in`
+    const uint32_t* Kin = sm.k[in] + insk;
+    const double* Vin = sm.v[in] + insv;
     // the previous bin's bulk store reads buffer `scr`: done before it is written
     if (tid == 0) bulk_wait_read();
-    if (distinct * 2 <= n && n >= 64) {
+    if (distinct * PBG_PM_NUM <= n * PBG_PM_DEN && distinct <= SM_CAP / 2 && n >= 64) {
         __syncthreads();  // thread 0's bulk_wait_read before anyone writes `scr`
-        n = hash_premerge(a, sm, in, scr, n, prof_t);  // now n distinct keys, no duplicates
+        n = hash_premerge(a, sm, in, scr, n, Kin, Vin, prof_t);  // now n distinct keys, no duplicates
+        Kin = sm.k[in];  // the distinct pairs sit at the buffer's start
+        Vin = sm.v[in];
         zero_cnt(sm);
         __syncthreads();
         PROF_MARK(7);
@@ -454,7 +491,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     // warps wait at the next barrier, and bank conflicts rise.)
 #pragma unroll HIST_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
-        const uint32_t d = (sm.k[in][i] - keylo) >> sh;
+        const uint32_t d = (Kin[i] - keylo) >> sh;
         atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
     }
     __syncthreads();
@@ -465,13 +502,13 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     if (threadIdx.x == 0) meta_fetch(a, sm, next_slot, next_bin, *a.nw_dev);
 #pragma unroll SCAT_UNROLL
     for (uint32_t i = tid; i < n; i += SM_NT) {
-        const uint32_t key = sm.k[in][i];
+        const uint32_t key = Kin[i];
         const uint32_t d = (key - keylo) >> sh;
         const uint32_t old = atomicAdd(&cntw[d >> 1], 1u << ((d & 1) * 16));
         const uint32_t pos = (old >> ((d & 1) * 16)) & 0xffffu;
         PBG_DCHECK(pos < n);
         sm.k[scr][pos] = key;
-        sm.v[scr][pos] = sm.v[in][i];
+        sm.v[scr][pos] = Vin[i];
     }
     __syncthreads();
     PROF_MARK(2);
@@ -564,12 +601,13 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
 // Write a work bin: colids / values at P, rowptr of the rows it starts.
 __device__ __forceinline__ void write_bin(const SortArgs& a, const SortSmem& sm, int buf,
                                           uint64_t b, uint64_t nw, uint32_t rs, uint32_t span,
-                                          uint32_t U, uint64_t P, int rshift) {
+                                          uint32_t U, uint64_t P, int rshift, uint32_t kofs = 0,
+                                          uint32_t vofs = 0) {
     const int tid = threadIdx.x;
     const int cb = a.col_bits;
     const uint32_t colmask = cb >= 32 ? 0xffffffffu : ((1u << cb) - 1u);
-    const uint32_t* K = sm.k[buf];
-    const double* V = sm.v[buf];
+    const uint32_t* K = sm.k[buf] + kofs;
+    const double* V = sm.v[buf] + vofs;
     PBG_DCHECK(P + U <= a.c_cap && rs + span <= a.m);
     uint32_t* okeys = a.ccol + P;
     double* ovals = a.cval + P;
@@ -688,25 +726,26 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         int rshift = -1, bulk = 0;
         uint32_t U = 0;
         bool merged = false, fetched = false;
-        if (loaded) {
+        uint32_t wk = 0, wv = 0;  // where the output starts in buffer `res`
+        if (loaded && (M.flags & 2u)) {
+            // merged sub-bin: already sorted and distinct, copied as it arrived
+            mbar_wait(&sm.mbar, parity);
+            parity ^= 1;
+            U = static_cast<uint32_t>(M.n);
+            wk = static_cast<uint32_t>(M.off & 3u);
+            wv = static_cast<uint32_t>(M.off & 1u);
+            PROF_MARK(0);
+        } else if (loaded) {
             const uint32_t n = static_cast<uint32_t>(M.n);
             zero_cnt(sm);
-            if (loaded == 1) {
-                mbar_wait(&sm.mbar, parity);
-                parity ^= 1;
-            } else {  // unaligned heavy sub-bin: plain coalesced loads
-                const uint32_t* ks = ((M.flags & 1u) ? a.skeys : a.keys) + M.off;
-                const double* vs = ((M.flags & 1u) ? a.svals : a.vals) + M.off;
-                for (uint32_t i = tid; i < n; i += SM_NT) {
-                    sm.k[inb][i] = ks[i];
-                    sm.v[inb][i] = vs[i];
-                }
-            }
+            mbar_wait(&sm.mbar, parity);
+            parity ^= 1;
             __syncthreads();
             PROF_MARK(0);
             U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(M.keybits), M.keylo,
                                static_cast<uint32_t>(M.nnz), &res, &rshift, M.out, &bulk, mc ^ 1,
-                               tk, prof_t);
+                               tk, static_cast<uint32_t>(M.off & 3u),
+                               static_cast<uint32_t>(M.off & 1u), prof_t);
             fetched = true;
 #ifdef PBG_SORT_PROF
             __syncthreads();
@@ -730,7 +769,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         }
         if (merged) write_merged(a, M, b, nw, M.out, U);
         else if (bulk) write_bin_bulk(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift);
-        else write_bin(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift);
+        else write_bin(a, sm, res, b, nw, M.rs, M.span, U, M.out, rshift, wk, wv);
         PROF_MARK(5);
         inb = res ^ 1;
         mc ^= 1;
