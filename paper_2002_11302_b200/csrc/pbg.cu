@@ -619,15 +619,10 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
             hc.svals = static_cast<double*>(ctx->svals.p);
             nitems = H;
             static std::atomic<bool> hv_attr[64] = {};  // per device; a concurrent double set is benign
-            static const bool hv_v1 = getenv("PBG_HV_SCATTER_V1") && atoi(getenv("PBG_HV_SCATTER_V1")) != 0;  // A/B hook
             if (!hv_attr[ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(sizeof(HvScatter2Smem))));
                 CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter2,
-                                              cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(sizeof(HvScatterSmem))));
-                CUDA_TRY(cudaFuncSetAttribute(k_hv_scatter,
                                               cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 hv_attr[ctx->device & 63] = true;
             }
@@ -668,15 +663,10 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                 const uint64_t nout = hs[S_ITEMS];
                 Items nxt{};
                 if ((rc = items_of(curset ^ 1, nout, &nxt))) return rc;
-                if (hv_v1) {
-                    k_hv_scatter<<<gt, HV_NT, sizeof(HvScatterSmem), st>>>(hc, cur, nitems, tpos, titem,
-                                                                          sh, d, hist);
-                } else {
-                    const unsigned g2 = static_cast<unsigned>(
-                        std::min<uint64_t>(ntiles, (HV_TILE <= 4096 ? 2ull : 1ull) * ctx->num_sms));
-                    k_hv_scatter2<<<g2, HV2_NT, sizeof(HvScatter2Smem), st>>>(hc, cur, nitems, tpos,
-                                                                             titem, sh, d, hist);
-                }
+                const unsigned g2 = static_cast<unsigned>(
+                    std::min<uint64_t>(ntiles, (HV_TILE <= 4096 ? 2ull : 1ull) * ctx->num_sms));
+                k_hv_scatter2<<<g2, HV2_NT, sizeof(HvScatter2Smem), st>>>(hc, cur, nitems, tpos, titem,
+                                                                         sh, d, hist);
                 k_hv_children<<<gi, HV_PT, 0, st>>>(hc, cur, nitems, sh, d, hist, cpos, nxt);
                 L += 7;
                 cur = nxt;
@@ -791,10 +781,11 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // ---- sort + merge + CSR (pb_spgemm.cpp:260-328) ----
         static std::atomic<bool> attr_set[64] = {};
         if (!attr_set[ctx->device & 63]) {
-            CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(sizeof(SortSmem))));
-            CUDA_TRY(cudaFuncSetAttribute(k_sortmerge, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          100));
+            for (auto kern : {k_sortmerge<false>, k_sortmerge<true>}) {
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(sizeof(SortSmem))));
+                CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            }
             attr_set[ctx->device & 63] = true;
         }
         SortArgs sa{};
@@ -817,7 +808,7 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         sa.err = reinterpret_cast<unsigned int*>(sc + S_ERR);
         sa.fallbacks = sc + S_FALLBACKS;
         int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge, SM_NT, sizeof(SortSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sortmerge<false>, SM_NT, sizeof(SortSmem));
         if (const char* e = getenv("PBG_SORT_PER_SM")) per_sm = atoi(e);  // tuning hook
         const unsigned sm_blocks = static_cast<unsigned>(
             std::min<uint64_t>(wcap, static_cast<uint64_t>(std::max(per_sm, 1)) * ctx->num_sms));
@@ -827,7 +818,9 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         CUDA_TRY(cudaMemsetAsync(prof, 0, 16 * 8, st));
         sa.prof = prof;
 #endif
-        k_sortmerge<<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
+        // heavy rows: unaligned / merged sub-bins and hot duplicate keys
+        if (H > 0) k_sortmerge<true><<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
+        else k_sortmerge<false><<<sm_blocks, SM_NT, sizeof(SortSmem), st>>>(sa);
         ++L;
 #ifdef PBG_SORT_PROF
         {

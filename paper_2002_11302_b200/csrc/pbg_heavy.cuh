@@ -33,13 +33,13 @@ namespace pbg {
 
 constexpr int HV_NT = 512;
 #ifndef PBG_HV_TILE
-#define PBG_HV_TILE 4096
+#define PBG_HV_TILE 8192
 #endif
 constexpr int HV_TILE = PBG_HV_TILE; // tuples per split tile (4096 or 8192)
 constexpr int HV_DENSE_BITS = 12;    // key range of a dense-reduced item (4096 columns)
 constexpr int HV_MAXD = 10;          // digit bits per split pass (<= 1024 buckets)
 #ifndef PBG_HV_GREEDY
-#define PBG_HV_GREEDY 0              // tuning hook, see hv_plan_item
+#define PBG_HV_GREEDY 1              // child grouping rule, see hv_plan_item
 #endif
 #ifndef PBG_DENSE_MIN
 #define PBG_DENSE_MIN 0              // tuning hook, see k_hv_children
@@ -122,9 +122,20 @@ __global__ void k_heavy_init(const uint64_t* __restrict__ bin_cnt, const uint64_
 //   k_hv_children child descriptors at the scanned positions
 // A child above cap is one bucket; if its key range is <= 2^HV_DENSE_BITS
 // it is reduced by k_hv_dense, else split again on the next level.
+// The remaining sh - 12 bits are cut into the fewest levels of at most 8 bits,
+// evenly: 2^24 columns split 6 + 6 bits, not 10 + 2. A tile's tuples spread
+// over 2^d bucket segments, and the L2 serves short scattered segments at a
+// fixed rate of line requests (~8.5 G key+value segment pairs/s whatever
+// their length), so two passes with 128-tuple segments cost
+// less than one with 8-tuple segments.
 __host__ __device__ inline int hv_digit(int sh) {
-    const int d = sh - HV_DENSE_BITS;
-    return d < 1 ? 1 : (d > HV_MAXD ? HV_MAXD : d);
+    const int rem = sh - HV_DENSE_BITS;
+    if (rem < 1) return 1;
+#ifdef PBG_HV_DIGIT_MAX  // A/B hook: as many bits as fit per level (10 + 2 for 2^24 columns)
+    return rem > HV_MAXD ? HV_MAXD : rem;
+#endif
+    const int levels = (rem + 7) / 8;
+    return (rem + levels - 1) / levels;
 }
 
 // tile counts of SPLIT items (scan input)
@@ -380,83 +391,11 @@ __global__ void __launch_bounds__(HV_PT) k_hv_plan(Items it, uint64_t nitems, ui
     }
 }
 
-struct HvScatterSmem {
-    uint32_t cnt[1 << HV_MAXD];   // tile histogram
-    uint32_t gb[1 << HV_MAXD];    // reserved global start of the tile's bucket segment
-};
-
-__global__ void __launch_bounds__(HV_NT, 2) k_hv_scatter(HeavyCtx c, Items it, uint64_t nitems,
-                                                         const uint64_t* __restrict__ tile_pos,
-                                                         const uint32_t* __restrict__ tile_item,
-                                                         uint32_t sh, uint32_t d, uint32_t* cursor) {
-    extern __shared__ __align__(16) unsigned char hv_raw[];
-    HvScatterSmem& sm = *reinterpret_cast<HvScatterSmem*>(hv_raw);
-    const int tid = threadIdx.x;
-    const uint64_t ntiles = tile_pos[nitems];
-    const uint32_t nbk = 1u << d, s2 = sh - d, mask = nbk - 1u;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const HvTile tl = hv_tile(it, tile_pos, tile_item, t);
-        const uint32_t buf = it.buf[tl.i], h = it.h[tl.i];
-        const uint64_t loc = it.loc[tl.i];
-        const uint64_t sbase = item_base(c, h, buf) + loc + tl.start;
-        const uint64_t dbase = item_base(c, h, buf ^ 1u) + loc;
-        const uint32_t* SK = (buf ? c.skeys : c.keys) + sbase;
-        const double* SV = (buf ? c.svals : c.vals) + sbase;
-        uint32_t* DK = (buf ? c.keys : c.skeys) + dbase;
-        double* DV = (buf ? c.vals : c.svals) + dbase;
-        for (uint32_t q = tid; q < nbk; q += HV_NT) sm.cnt[q] = 0;
-        __syncthreads();
-        // tuples in registers; the histogram atomic's return value is the
-        // tuple's rank inside its bucket (one shared atomic per tuple)
-        constexpr int TPT = HV_TILE / HV_NT;  // 8
-        uint32_t kk[TPT], rb[TPT];
-        double vv[TPT];
-#pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const uint32_t q = tid + j * HV_NT;
-            if (q < tl.m) {
-                kk[j] = __ldcs(SK + q);
-                vv[j] = __ldcs(SV + q);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const uint32_t q = tid + j * HV_NT;
-            const uint32_t bk = (kk[j] >> s2) & mask;
-            const uint32_t r = warp_bucket_rank(sm.cnt, bk, q < tl.m);
-            rb[j] = r | (bk << 16);
-        }
-        __syncthreads();
-        {  // one global reservation per non-empty bucket
-            uint32_t* cur = cursor + static_cast<uint64_t>(tl.i) * nbk;
-            for (uint32_t q = tid; q < nbk; q += HV_NT) {
-                const uint32_t v = sm.cnt[q];
-                if (v) sm.gb[q] = atomicAdd(cur + q, v);
-            }
-        }
-        __syncthreads();
-        // straight from registers to the reserved global segment: lanes of a
-        // store hit different buckets, but each segment is completed by this
-        // CTA within microseconds, so L2 assembles full lines
-#pragma unroll
-        for (int j = 0; j < TPT; ++j) {
-            const uint32_t q = tid + j * HV_NT;
-            if (q < tl.m) {
-                const uint64_t dst = static_cast<uint64_t>(sm.gb[rb[j] >> 16]) + (rb[j] & 0xffffu);
-                PBG_DCHECK(dst < it.n[tl.i]);
-                DK[dst] = kk[j];
-                DV[dst] = vv[j];
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// k_hv_scatter2: the same split with the tiles staged by TMA. A producer warp
+// k_hv_scatter2: the split pass with its tiles staged by TMA. A producer warp
 // (warp HV_NT/32, one elected lane) walks the CTA's tiles one ahead of the 512
 // consumer threads: it resolves the tile descriptor (tile -> item -> buffer
-// addresses: three dependent global round trips that every thread of
-// k_hv_scatter paid per tile), publishes it in shared memory and starts two
+// addresses: three dependent global round trips that every thread of the
+// first version, k_hv_scatter, paid per tile), publishes it in shared memory and starts two
 // bulk copies (keys, values; from the 16-byte boundary below the tile) into
 // the free one of two buffers, completion on that buffer's `full` mbarrier.
 // Consumers rank the tile's keys from shared memory (no tuple registers held
@@ -648,11 +587,8 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
 // measured 1.5x slower: these items are popular columns, and L2 atomics
 // serialise per address.)
 constexpr int HV_DENSE = 1 << HV_DENSE_BITS;
-#ifndef PBG_DENSE_AGG
-#define PBG_DENSE_AGG 0  // 0 = off; else the smallest group of equal slots summed by shuffles
-#endif
 #ifndef PBG_DENSE_COPIES
-#define PBG_DENSE_COPIES 1
+#define PBG_DENSE_COPIES 2
 #endif
 // DC accumulator copies, lane l adding into copy l % DC (equal popular
 // columns in one instruction's lanes retry each other's CAS; copies per WARP
@@ -692,36 +628,6 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
                 ks[u] = q < n ? __ldcs(K + q) : 0xffffffffu;
                 vs[u] = q < n ? __ldcs(V + q) : 0.0;
             }
-#if PBG_DENSE_AGG
-            // Popular columns repeat inside one instruction's 32 tuples and an
-            // f64 shared-memory atomicAdd is a CAS loop: k equal slots cost k
-            // rounds. Groups of >= PBG_DENSE_AGG equal slots are summed by a
-            // shuffle butterfly first and added once by their first lane.
-            const int lane = tid & 31;
-#pragma unroll
-            for (int u = 0; u < DU; ++u) {
-                const bool valid = ks[u] != 0xffffffffu;
-                const uint32_t slot = valid ? ks[u] - keylo : 0x80000000u + lane;
-                const uint32_t peers = __match_any_sync(FULL, slot);
-                const bool first = (__ffs(peers) - 1) == lane;
-                const bool big = __popc(peers) >= PBG_DENSE_AGG;
-                uint32_t todo = __ballot_sync(FULL, valid && first && big);
-                double mine = vs[u];
-                while (todo) {
-                    const int L = __ffs(todo) - 1;
-                    todo &= todo - 1;
-                    const uint32_t g = __shfl_sync(FULL, peers, L);
-                    double t = ((g >> lane) & 1u) ? vs[u] : -0.0;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-                    if (lane == L) mine = t;
-                }
-                if (valid && (first || !big)) {
-                    atomicAdd(&acc[slot], mine);
-                    seen[slot] = 1;
-                }
-            }
-#else
 #pragma unroll
             for (int u = 0; u < DU; ++u) {
                 if (ks[u] == 0xffffffffu) continue;
@@ -729,7 +635,6 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
                 atomicAdd(&acc[slot], vs[u]);
                 seen[slot] = 1;
             }
-#endif
         }
         __syncthreads();
         if (HV_DC > 1) {

@@ -487,6 +487,46 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                 bnd_n = bi <= a.a_ncols ? a.a_colptr[bi] : ~0ull;
             }
             staged = false;
+            // Long runs (RMAT hub rows of B): the warp streams one run at a
+            // time, 32 consecutive tuples per step, with none of the flat
+            // stream's per-step run lookup (85 warp instructions per 32 tuples
+            // on a C3 round, 61 % issue-active). Only with the long-run
+            // register budget (MINB >= 4): short-run inputs never take it.
+            if (MINB >= 4) {
+                constexpr uint64_t EXP_LONG = 256;
+                uint32_t longm = __ballot_sync(FULL, lb >= EXP_LONG);
+                const bool is_long = lb >= EXP_LONG;
+                while (longm) {
+                    const int L = __ffs(longm) - 1;
+                    longm &= longm - 1;
+                    const uint64_t n0 = __shfl_sync(FULL, lb, L);
+                    const uint32_t* bc = a.b_colids + __shfl_sync(FULL, bst, L);
+                    const double* bv = a.b_vals + __shfl_sync(FULL, bst, L);
+                    uint32_t* kd = a.keys + __shfl_sync(FULL, dst, L);
+                    double* vd = a.vals + __shfl_sync(FULL, dst, L);
+                    const double a0 = __shfl_sync(FULL, av, L);
+                    const uint32_t r0 = __shfl_sync(FULL, rp, L);
+                    for (uint64_t q0 = 0; q0 < n0; q0 += 32 * 4) {
+                        uint32_t kq[4];
+                        double vq[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint64_t q = q0 + 32 * u + lane;
+                            kq[u] = q < n0 ? __ldg(bc + q) : 0u;
+                            vq[u] = q < n0 ? __ldg(bv + q) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint64_t q = q0 + 32 * u + lane;
+                            if (q < n0) {
+                                st_tuple_key(kd + q, r0 | kq[u], pol);
+                                st_tuple_val(vd + q, a0 * vq[u], pol);
+                            }
+                        }
+                    }
+                }
+                if (is_long) lb = 0;  // done: not part of the flat stream below
+            }
             const bool ne = lb != 0;
             const uint32_t nemask = __ballot_sync(FULL, ne);
             const int rank = __popc(nemask & lt);

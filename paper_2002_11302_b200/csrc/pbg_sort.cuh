@@ -64,10 +64,10 @@ constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
 constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
 // hash pre-merge of a bin when distinct * NUM <= tuples * DEN (tuning hook)
 #ifndef PBG_PM_NUM
-#define PBG_PM_NUM 2
+#define PBG_PM_NUM 4
 #endif
 #ifndef PBG_PM_DEN
-#define PBG_PM_DEN 1
+#define PBG_PM_DEN 3
 #endif
 #ifndef PBG_RANK_UNROLL
 #define PBG_RANK_UNROLL 1
@@ -309,6 +309,9 @@ __device__ int lsd_sort(SortSmem& sm, int x, int y, uint32_t n, int bits, uint32
 // window the run covers: a key repeated r times costs its head r/32 adds
 // instead of r (RMAT's hot columns repeat hundreds of times; the serial
 // per-head loop was 29 % of the sort kernel on a C3 round).
+// HV = false (no heavy rows in the product: duplicates are rare and short)
+// keeps the plain per-head loop.
+template <bool HV>
 __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint32_t n) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt = lanemask_lt();
@@ -325,6 +328,7 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
         const bool h = in && (i == 0 || K[i] != K[i - 1]);
         masks[it] = __ballot_sync(FULL, h);
         heads += __popc(masks[it]);
+        if (!HV) continue;
         if (masks[it] == __ballot_sync(FULL, in)) continue;  // no duplicate inside this window
         // segment starts of the window: run heads and lane 0
         const uint32_t seg = masks[it] | 1u;
@@ -348,7 +352,11 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
             const uint32_t u = base + __popc(masks[it] & lt);
             const uint32_t key = K[i];
             double s = V[i];
-            for (uint32_t e = (i | 31u) + 1; e < n && K[e] == key; e += 32) s += V[e];
+            if (HV) {
+                for (uint32_t e = (i | 31u) + 1; e < n && K[e] == key; e += 32) s += V[e];
+            } else {
+                for (uint32_t e = i + 1; e < n && K[e] == key; ++e) s += V[e];
+            }
             KO[u] = key;
             VO[u] = s;
         }
@@ -365,6 +373,7 @@ __device__ __forceinline__ uint32_t merge_dups(SortSmem& sm, int x, int y, uint3
 // loop): a tuple takes a rank in its slot with a u16 counter add, a scan
 // turns the slot counts into group starts, values are scattered into their
 // groups and each group is summed by the thread owning its slot.
+template <bool HV>
 __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
                                   const uint32_t* Kin, const double* Vin, long long& prof_t) {
     const int tid = threadIdx.x;
@@ -443,20 +452,59 @@ __device__ uint32_t hash_premerge(const SortArgs& a, SortSmem& sm, int in, int s
     }
     __syncthreads();
     PROF_MARK(11);
-    // one thread per distinct key sums its group
     const uint32_t D = tot >> 16;
+    if (!HV) {
+        // one thread per distinct key sums its group
+        for (uint32_t d = tid; d < D; d += SM_NT) {
+            const uint32_t g = grp[d], p = g >> 16, c = g & 0xffffu;
+            double s = sm.v[scr][p];
+            for (uint32_t t = 1; t < c; ++t) s += sm.v[scr][p + t];
+            sm.v[in][d] = s;
+        }
+        __syncthreads();
+        return D;
+    }
+    // heavy rows: a group of PM_BIG or more (RMAT's hot columns repeat
+    // hundreds of times in a bin, and the thread owning one kept the whole
+    // CTA waiting) is queued and summed by a warp afterwards
+    constexpr uint32_t PM_BIG = 64;
+    uint32_t* bigq = sm.k[scr];  // the hash keys are dead: queue of big groups (index d)
+    if (tid == 0) sm.s_warp32[0] = 0;
+    __syncthreads();
     for (uint32_t d = tid; d < D; d += SM_NT) {
         const uint32_t g = grp[d], p = g >> 16, c = g & 0xffffu;
+        if (c >= PM_BIG) {
+            bigq[atomicAdd(&sm.s_warp32[0], 1u)] = d;
+            continue;
+        }
         double s = sm.v[scr][p];
         for (uint32_t t = 1; t < c; ++t) s += sm.v[scr][p + t];
         sm.v[in][d] = s;
     }
     __syncthreads();
+    const uint32_t nbig = sm.s_warp32[0];
+    for (uint32_t q = tid >> 5; q < nbig; q += SM_NW) {
+        const uint32_t d = bigq[q];
+        const uint32_t g = grp[d], p = g >> 16, c = g & 0xffffu;
+        double s = -0.0;
+        for (uint32_t t = tid & 31; t < c; t += 32) s += sm.v[scr][p + t];
+        s = warp_sum(s);
+        if ((tid & 31) == 0) sm.v[in][d] = s;
+    }
+    __syncthreads();
     return tot >> 16;
+}
+
+// (out of line: inlined, its queue pass pushed k_sortmerge<true> into spills)
+__device__ __noinline__ uint32_t hash_premerge_heavy(const SortArgs& a, SortSmem& sm, int in, int scr,
+                                                     uint32_t n, const uint32_t* Kin, const double* Vin,
+                                                     long long& prof_t) {
+    return hash_premerge<true>(a, sm, in, scr, n, Kin, Vin, prof_t);
 }
 
 // Sort + merge the bin in buffer `in` using scratch buffer `scr`. Returns the
 // merged count; *res gets the buffer holding the merged output.
+template <bool HV>
 __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int scr, uint32_t n,
                                    int bits, uint32_t keylo, uint32_t distinct, int* res,
                                    int* rshift, uint64_t P, int* bulk,
@@ -465,13 +513,20 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     const int tid = threadIdx.x;
     *bulk = 0;
     // the bin as it arrived: insk keys / insv values into buffer `in`
-    const uint32_t* Kin = sm.k[in] + insk;
-    const double* Vin = sm.v[in] + insv;
+    // (heavy sub-bins only: bins of the main buffer are 16-byte aligned)
+    const uint32_t* Kin = sm.k[in] + (HV ? insk : 0u);
+    const double* Vin = sm.v[in] + (HV ? insv : 0u);
     // the previous bin's bulk store reads buffer `scr`: done before it is written
     if (tid == 0) bulk_wait_read();
-    if (distinct * PBG_PM_NUM <= n * PBG_PM_DEN && distinct <= SM_CAP / 2 && n >= 64) {
+    // pre-merge threshold: distinct <= n/2 (the stencil: cf 5.8); heavy rows'
+    // sub-bins (cf ~1.9, hot keys) gain from distinct <= 3n/4 (C3 sort -8 %)
+    const bool premerge = HV ? (distinct * PBG_PM_NUM <= n * PBG_PM_DEN && distinct <= SM_CAP / 2)
+                             : (distinct * 2 <= n);
+    if (premerge && n >= 64) {
         __syncthreads();  // thread 0's bulk_wait_read before anyone writes `scr`
-        n = hash_premerge(a, sm, in, scr, n, Kin, Vin, prof_t);  // now n distinct keys, no duplicates
+        // now n distinct keys, no duplicates
+        n = HV ? hash_premerge_heavy(a, sm, in, scr, n, Kin, Vin, prof_t)
+               : hash_premerge<false>(a, sm, in, scr, n, Kin, Vin, prof_t);
         Kin = sm.k[in];  // the distinct pairs sit at the buffer's start
         Vin = sm.v[in];
         zero_cnt(sm);
@@ -526,7 +581,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         if (distinct < n) {  // exact count: duplicates present
             *res = in;
             *rshift = -1;
-            return merge_dups(sm, scr, in, n);
+            return merge_dups<HV>(sm, scr, in, n);
         }
         return n;
     }
@@ -589,7 +644,7 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
     if (distinct < n) {
         __syncthreads();  // the rank pass's writes of `sorted`
         *res = other;
-        return merge_dups(sm, sorted, other, n);
+        return merge_dups<HV>(sm, sorted, other, n);
     }
     *res = sorted;
     *rshift = any_big ? -1 : sh;  // sorted positions = bucket ends: row starts from them
@@ -695,6 +750,10 @@ __device__ void write_merged(const SortArgs& a, const BinMeta& m, uint64_t b, ui
     }
 }
 
+// HV: the product has heavy rows (work bins may be unaligned heavy sub-bins or
+// merged pieces, duplicates are frequent and hot). HV = false is the plain
+// path of ER / stencil products.
+template <bool HV>
 __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
@@ -727,7 +786,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
         uint32_t U = 0;
         bool merged = false, fetched = false;
         uint32_t wk = 0, wv = 0;  // where the output starts in buffer `res`
-        if (loaded && (M.flags & 2u)) {
+        if (HV && loaded && (M.flags & 2u)) {
             // merged sub-bin: already sorted and distinct, copied as it arrived
             mbar_wait(&sm.mbar, parity);
             parity ^= 1;
@@ -742,7 +801,7 @@ __global__ void __launch_bounds__(SM_NT, 1024 / SM_NT) k_sortmerge(SortArgs a) {
             parity ^= 1;
             __syncthreads();
             PROF_MARK(0);
-            U = sort_merge_bin(a, sm, inb, inb ^ 1, n, static_cast<int>(M.keybits), M.keylo,
+            U = sort_merge_bin<HV>(a, sm, inb, inb ^ 1, n, static_cast<int>(M.keybits), M.keylo,
                                static_cast<uint32_t>(M.nnz), &res, &rshift, M.out, &bulk, mc ^ 1,
                                tk, static_cast<uint32_t>(M.off & 3u),
                                static_cast<uint32_t>(M.off & 1u), prof_t);
