@@ -539,15 +539,19 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         if ((rc = grow(ctx->row_pack, (m + 1) * (pack32 ? 4 : 8)))) return rc;
         ExpandArgs ea{xa_colptr, xa_rowids, xa_vals, B.ptr, B.idx, B.val, kv, k, chunk_p0, chunk_col, nchunks,
                       ctx->row_pack.p, lbits, cursor, keys, vals, cb, bin_off};
+        // very short runs (<= 12 tuples on average): 8 tuple steps in flight
+        const bool tiny_runs = !long_runs && flop <= 12 * nnz_a;
         if (pack32) {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
                                                          static_cast<uint32_t*>(ctx->row_pack.p));
             if (long_runs) k_expand<uint32_t, 4><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            else if (tiny_runs) k_expand<uint32_t, PBG_EXP_MINB, 8><<<exp_blocks, EXP_NT, 0, st>>>(ea);
             else k_expand<uint32_t, PBG_EXP_MINB><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         } else {
             k_rowpack<<<blocks_for(m, 256), 256, 0, st>>>(row_bin, bin_rs, m, lbits,
                                                          static_cast<uint64_t*>(ctx->row_pack.p));
             if (long_runs) k_expand<uint64_t, 4><<<exp_blocks, EXP_NT, 0, st>>>(ea);
+            else if (tiny_runs) k_expand<uint64_t, PBG_EXP_MINB, 8><<<exp_blocks, EXP_NT, 0, st>>>(ea);
             else k_expand<uint64_t, PBG_EXP_MINB><<<exp_blocks, EXP_NT, 0, st>>>(ea);
         }
         L += 2;
@@ -737,9 +741,8 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
         static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
-        auto launch_count = [&](auto kern, int nt, size_t smem) -> int {
+        auto launch_count = [&](auto kern, int nt, size_t smem, int shape) -> int {
             static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
-            const int shape = (cnt_v1 ? 2 : 0) + (big_table ? 1 : 0);
             if (!attr_set[shape][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
@@ -757,14 +760,14 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         };
         if (cnt_v1) {
             if (big_table) {
-                if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4))) return rc;
+                if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4, 3))) return rc;
             } else {
-                if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4))) return rc;
+                if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4, 2))) return rc;
             }
         } else if (big_table) {
-            if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4))) return rc;
+            if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4, 1))) return rc;
         } else {
-            if ((rc = launch_count(k_bincount2<512, 16384>, 512, (16384 + 32) * 4))) return rc;
+            if ((rc = launch_count(k_bincount2<512, 16384>, 512, (16384 + 32) * 4, 0))) return rc;
         }
         ++L;
         // wcap can exceed the m-sized status pool: give this scan its own words

@@ -1059,4 +1059,5 @@ __global__ void __launch_bounds__(NT, cnt_ctas(NT, SLOTS)) k_bincount2(const uin
     }
 }
 
+
 }  // namespace pbg

@@ -334,7 +334,6 @@ constexpr int EXP_NT = 256;
 #ifndef PBG_EXP_EVICT_LAST
 #define PBG_EXP_EVICT_LAST 1
 #endif
-constexpr int EXP_U = PBG_EXP_U;  // tuple steps in flight per lane
 
 // Tuple stores. With PBG_EXP_EVICT_LAST the lines carry an L2 evict_last
 // policy: a bin's partially written frontier line then survives the
@@ -387,7 +386,10 @@ constexpr int EXP_NW = EXP_NT / 32;
 // MINB: resident CTAs per SM the register budget is sized for — 2 for short
 // runs (ER, stencil: 128 registers, deeper batch pipeline), 4 for long runs
 // (RMAT: more warps streaming B rows).
-template <typename P, int MINB>
+// EXP_U: tuple steps of 32 a lane keeps in flight (loads issued before their
+// stores): 8 for very short runs (C5a's 8-tuple runs: expand 16.3 -> 15.1 ms),
+// 4 otherwise (C4 loses 2 % with 8).
+template <typename P, int MINB, int EXP_U = PBG_EXP_U>
 __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
     __shared__ uint64_t s_dst[EXP_NW][32];
     __shared__ uint64_t s_bst[EXP_NW][32];

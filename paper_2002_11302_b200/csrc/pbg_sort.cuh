@@ -599,8 +599,18 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         }
         uint32_t r = 0;
         if (distinct < n) {
+            uint32_t j = lo;
+            if (HV) {  // heavy sub-bins: clustered hot columns make long buckets
 #pragma unroll 1
-            for (uint32_t j = lo; j < hi; ++j) {
+                for (; j + 4 <= hi; j += 4) {
+                    const uint32_t k0 = sm.k[scr][j], k1 = sm.k[scr][j + 1], k2 = sm.k[scr][j + 2],
+                                   k3 = sm.k[scr][j + 3];
+                    r += ((k0 < key) | ((k0 == key) & (j < i))) + ((k1 < key) | ((k1 == key) & (j + 1 < i))) +
+                         ((k2 < key) | ((k2 == key) & (j + 2 < i))) + ((k3 < key) | ((k3 == key) & (j + 3 < i)));
+                }
+            }
+#pragma unroll 1
+            for (; j < hi; ++j) {
                 const uint32_t kj = sm.k[scr][j];
                 r += (kj < key) | ((kj == key) & (j < i));
             }

@@ -9,7 +9,7 @@ constexpr int NT = 512, ITERS = 8192, SLOTS = 8192;
 template <int MODE>
 __global__ void k(uint32_t* out, uint32_t seed, long long* cyc) {
     __shared__ uint32_t t[SLOTS];
-    for (int i = threadIdx.x; i < SLOTS; i += NT) t[i] = 0xffffffffu * (MODE == 2);
+    for (int i = threadIdx.x; i < SLOTS; i += NT) t[i] = 0xffffffffu * (MODE == 2 || MODE == 8);
     __syncthreads();
     uint32_t x = seed ^ (threadIdx.x * 0x9E3779B1u) ^ (blockIdx.x * 0x85ebca6bu), acc = 0;
     long long c0 = clock64();
@@ -26,6 +26,24 @@ __global__ void k(uint32_t* out, uint32_t seed, long long* cyc) {
         else if (MODE == 6) atomicAdd(&t[h >> 1], 1u << ((h & 1) * 16));  // variable add, no return (histogram)
         else if (MODE == 7) acc += atomicAdd(&t[h >> 1], 1u << ((h & 1) * 16));  // variable add with return (scatter)
         else if (MODE == 8) acc += atomicCAS(&t[h], 0xffffffffu, x) == 0xffffffffu;  // CAS, insert-style
+        else if (MODE == 9) atomicAdd(reinterpret_cast<double*>(t) + (h >> 1), 1.0 + x);  // f64 add (CAS loop), 4096 slots
+        else if (MODE == 10) {  // f64 add through per-slot 32-bit locks (2048 slots + 2048 locks)
+            const uint32_t sl = h >> 2;
+            double* a = reinterpret_cast<double*>(t) + sl;  // doubles in t[0..4096)
+            uint32_t* lock = t + 4096 + sl;
+            bool done = false;
+            while (!done) {
+                if (atomicExch(lock, 1u) == 0u) {
+                    *reinterpret_cast<volatile double*>(a) += 1.0 + x;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile uint32_t*>(lock) = 0u;
+                    done = true;
+                }
+            }
+        }
+        else if (MODE == 11) {  // f64 add as two u32 halves? no: 64-bit integer atomicAdd (native?)
+            atomicAdd(reinterpret_cast<unsigned long long*>(t) + (h >> 1), (unsigned long long)x);
+        }
     }
     __syncthreads();
     long long c1 = clock64();
@@ -64,6 +82,9 @@ int main() {
         run<6>("ATOMS var add, no return", b);
         run<7>("ATOMS var add, return", b);
         run<8>("ATOMS.CAS insert", b);
+        run<9>("f64 atomicAdd (CAS loop)", b);
+        run<10>("f64 add under u32 lock", b);
+        run<11>("u64 atomicAdd", b);
     }
     return 0;
 }

@@ -390,6 +390,32 @@ def test_uniform_key_reduction():
     check_vs(gpu(ac, b), oracle.multiply(ac, b))
 
 
+def test_distinct_count_paths_on_structured_duplicates():
+    """The count-kernel shape is picked from the flop per row: a 2D 9-point
+    stencil squared falls in the distinct-key class (81 products per row) yet
+    every bin is duplicate-heavy (25 distinct of 81), and a sparse banded
+    product has a few duplicates per bin: both must count exactly."""
+    g = 96
+    ii, jj = np.meshgrid(np.arange(g), np.arange(g), indexing="ij")
+    rows, cols = [], []
+    for di in (-1, 0, 1):
+        for dj in (-1, 0, 1):
+            ok = (ii + di >= 0) & (ii + di < g) & (jj + dj >= 0) & (jj + dj < g)
+            rows.append((ii * g + jj)[ok])
+            cols.append(((ii + di) * g + (jj + dj))[ok])
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    rng = np.random.default_rng(5)
+    s9 = M.coo_to_csr(g * g, g * g, rows, cols, rng.uniform(0.5, 1.5, rows.size))
+    a = M.csr_to_csc(s9)
+    check_vs(gpu(a, s9), oracle.multiply(a, s9))
+    n = 1 << 14  # 4 random entries per row within a band of 256 columns
+    r = np.repeat(np.arange(n), 4)
+    c = (r + rng.integers(0, 256, r.size)) % n
+    bnd = M.coo_to_csr(n, n, r, c, rng.uniform(0.5, 1.5, r.size))
+    a = M.csr_to_csc(bnd)
+    check_vs(gpu(a, bnd), oracle.multiply(a, bnd))
+
+
 def test_tiny_bin_capacity_forces_heavy_split():
     csr = M.make_matrix("er", 11, 8, seed=3)
     a = M.csr_to_csc(csr)
