@@ -686,8 +686,8 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                                                   static_cast<int>(dsm)));
                     dn_attr[ctx->device & 63] = true;
                 }
-                k_hv_dense<<<static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms)),
-                             HV_NT, dsm, st>>>(hc, cur, nitems);
+                const unsigned gd = static_cast<unsigned>(std::min<uint64_t>(nitems, 8ull * ctx->num_sms));
+                k_hv_dense<<<gd, HV_NT, dsm, st>>>(hc, cur, nitems);
             }
             ++L;
             CUDA_TRY(cudaMemsetAsync(hcount, 0, H * 4, st));

@@ -109,25 +109,25 @@ __global__ void k_heavy_init(const uint64_t* __restrict__ bin_cnt, const uint64_
 // d = hv_digit(sh) key bits below bit sh become 2^d buckets per item.
 // Tiles of HV_TILE tuples are the unit of work, so one heavy row is spread
 // over many CTAs:
-//   k_hv_hist    tile histograms, added into the item's bucket counters
+//   k_hv_hist    tile histograms, piled up in shared memory over a CTA's
+//                contiguous tiles and added to the item's bucket counters
 //   k_hv_plan    per item: bucket starts (-> scatter cursors) and children
-//                (consecutive buckets grouped to <= cap tuples, window rule
-//                as k_binflags); child counts are scanned on the host side
-//   k_hv_scatter tile: ranks by bucket (one shared atomic per tuple), one
-//                global reservation per (tile, bucket), tuples written from
-//                registers into their bucket segment of the other buffer (a
-//                segment is finished by one CTA within microseconds, so L2
-//                assembles whole lines; staging the tile in bucket order in
-//                shared memory first was measured 4 % slower)
+//                (consecutive buckets grouped greedily to <= cap tuples);
+//                child counts are scanned on the host side
+//   k_hv_scatter2 tile (staged by a TMA producer warp): ranks by bucket (one
+//                warp-aggregated shared atomic per run of equal buckets), one
+//                global reservation per (tile, bucket), tuples written into
+//                their bucket segment of the other buffer
 //   k_hv_children child descriptors at the scanned positions
 // A child above cap is one bucket; if its key range is <= 2^HV_DENSE_BITS
 // it is reduced by k_hv_dense, else split again on the next level.
 // The remaining sh - 12 bits are cut into the fewest levels of at most 8 bits,
 // evenly: 2^24 columns split 6 + 6 bits, not 10 + 2. A tile's tuples spread
-// over 2^d bucket segments, and the L2 serves short scattered segments at a
-// fixed rate of line requests (~8.5 G key+value segment pairs/s whatever
-// their length), so two passes with 128-tuple segments cost
-// less than one with 8-tuple segments.
+// over 2^d bucket segments that start at any tuple: short unaligned segments
+// leave partly written sectors behind (DRAM read-modify-write;
+// scripts/micro/scatter_segments.cu: 8-tuple segments 0.74 TB/s, 128-tuple
+// 2.3 TB/s, aligned or L2-resident 5.1 TB/s), so two passes with 128-tuple
+// segments cost no more than one with 8-tuple segments (C5b band: -3 %).
 __host__ __device__ inline int hv_digit(int sh) {
     const int rem = sh - HV_DENSE_BITS;
     if (rem < 1) return 1;
@@ -585,7 +585,11 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
 // count and sort kernels just copy. Exact-zero sums are kept (presence
 // flags). (A global-memory accumulator with native L2 f64 reductions was
 // measured 1.5x slower: these items are popular columns, and L2 atomics
-// serialise per address.)
+// serialise per address. An atomic-free version — 32-bit rank atomics per
+// slot, a scan, values grouped in shared memory, a warp-shuffle segmented sum
+// and owner threads keeping their 8 slots' sums in registers — was built,
+// parity-green, and measured slower: 20.2 vs 13.1 ms on a C3 round, eight
+// barriers per 4096-tuple batch against none here.)
 constexpr int HV_DENSE = 1 << HV_DENSE_BITS;
 #ifndef PBG_DENSE_COPIES
 #define PBG_DENSE_COPIES 2

@@ -20,6 +20,15 @@ PBG_SPEC=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log
 # full sections of the three top kernels (second multiply)
 ncu --set full --clock-control none --import-source on -k regex:"k_expand|k_bincount|k_sortmerge" \
   -s 3 -c 3 -o $O/full_C2 python scripts/profile_step.py --config C2 --steps 1 > /dev/null 2>&1
+# one bounded-memory round of C3 (the first 1.5 % of the rows: 3.0e9 tuples,
+# 12.5 K heavy rows): launch list and full sections of the heavy-row kernels
+timeout 600 python scripts/profile_step.py --config C3 --row-band 0.015 --steps 2 > $O/c3_round_phases.txt 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file $O/launches_C3round.csv python scripts/profile_step.py --config C3 --row-band 0.015 --steps 1 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_expand|k_hv_hist|k_hv_scatter2|k_hv_dense|k_bincount|k_sortmerge" \
+  -s 6 -c 6 -o $O/full_C3round python scripts/profile_step.py --config C3 --row-band 0.015 --steps 1 > /dev/null 2>&1
+timeout 300 ./scripts/micro/scatter_segments > $O/scatter_segments_micro.txt 2>&1
+timeout 300 ./scripts/micro/smem_atomics > $O/smem_ops_micro.txt 2>&1
 # the N>1 bench control flow with two ranks on this one device (gloo; a
 # correctness check of the strong row-band path, not a measurement)
 PBG_BENCH_DEVICE=0 PBG_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 \
