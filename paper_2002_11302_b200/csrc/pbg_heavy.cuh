@@ -401,7 +401,18 @@ __global__ void __launch_bounds__(HV_PT) k_hv_plan(Items it, uint64_t nitems, ui
 // Consumers rank the tile's keys from shared memory (no tuple registers held
 // across the reservation round trip), reserve, store, and hand the buffer
 // back through its `empty` mbarrier. ncu on a C3 round had k_hv_scatter at
-// 50 % long-scoreboard stalls, 28 % issue, 3.1 TB/s.
+// 50 % long-scoreboard stalls, 28 % issue, 3.1 TB/s. Measured and not kept:
+// two consumer groups of 480 threads, each bound to one buffer and working on
+// every other tile out of phase (+1.8 ms per C3 round: a group's buffer is
+// refilled only after the group releases it); segment starts from per-tile
+// bucket counts and a scan over each item's tiles instead of reservations
+// (deterministic, no returning atomics, one barrier less per tile): the split
+// kernel took 24.3 ms with grid-strided tiles and 20.9 ms with a contiguous
+// tile range per CTA against 18.1 ms — the atomics hand out a bucket's
+// positions in ARRIVAL order, so concurrently written segments are neighbours
+// and their partly written sectors meet in L2; precomputed positions scatter
+// them — and the per-tile histogram (4.1 vs 2.8 ms) and the scan (1.2 ms)
+// come on top.
 struct HvDesc {
     uint32_t* dk;      // destination of the item's tuples (other buffer)
     double* dv;

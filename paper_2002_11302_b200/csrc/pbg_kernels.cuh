@@ -331,6 +331,9 @@ constexpr int EXP_NT = 256;
 #ifndef PBG_EXP_U
 #define PBG_EXP_U 4
 #endif
+#ifndef PBG_EXP_LONG_U
+#define PBG_EXP_LONG_U 8  // long-run fast path: tuple steps in flight (4: C5b band expand 15.9 vs 15.0 ms)
+#endif
 #ifndef PBG_EXP_EVICT_LAST
 #define PBG_EXP_EVICT_LAST 1
 #endif
@@ -508,17 +511,18 @@ __global__ void __launch_bounds__(EXP_NT, MINB) k_expand(ExpandArgs a) {
                     double* vd = a.vals + __shfl_sync(FULL, dst, L);
                     const double a0 = __shfl_sync(FULL, av, L);
                     const uint32_t r0 = __shfl_sync(FULL, rp, L);
-                    for (uint64_t q0 = 0; q0 < n0; q0 += 32 * 4) {
-                        uint32_t kq[4];
-                        double vq[4];
+                    constexpr int LU = PBG_EXP_LONG_U;  // steps of 32 tuples in flight
+                    for (uint64_t q0 = 0; q0 < n0; q0 += 32 * LU) {
+                        uint32_t kq[LU];
+                        double vq[LU];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < LU; ++u) {
                             const uint64_t q = q0 + 32 * u + lane;
                             kq[u] = q < n0 ? __ldg(bc + q) : 0u;
                             vq[u] = q < n0 ? __ldg(bv + q) : 0.0;
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < LU; ++u) {
                             const uint64_t q = q0 + 32 * u + lane;
                             if (q < n0) {
                                 st_tuple_key(kd + q, r0 | kq[u], pol);

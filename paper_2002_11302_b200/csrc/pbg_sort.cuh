@@ -599,20 +599,29 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
         }
         uint32_t r = 0;
         if (distinct < n) {
+            // duplicates present: ties by position. Four keys per trip (heavy
+            // sub-bins' clustered hot columns make long buckets), then a
+            // predicated tail of 0..3 keys
             uint32_t j = lo;
-            if (HV) {  // heavy sub-bins: clustered hot columns make long buckets
 #pragma unroll 1
-                for (; j + 4 <= hi; j += 4) {
-                    const uint32_t k0 = sm.k[scr][j], k1 = sm.k[scr][j + 1], k2 = sm.k[scr][j + 2],
-                                   k3 = sm.k[scr][j + 3];
-                    r += ((k0 < key) | ((k0 == key) & (j < i))) + ((k1 < key) | ((k1 == key) & (j + 1 < i))) +
-                         ((k2 < key) | ((k2 == key) & (j + 2 < i))) + ((k3 < key) | ((k3 == key) & (j + 3 < i)));
-                }
+            for (; j + 4 <= hi; j += 4) {
+                const uint32_t k0 = sm.k[scr][j], k1 = sm.k[scr][j + 1], k2 = sm.k[scr][j + 2],
+                               k3 = sm.k[scr][j + 3];
+                r += ((k0 < key) | ((k0 == key) & (j < i))) + ((k1 < key) | ((k1 == key) & (j + 1 < i))) +
+                     ((k2 < key) | ((k2 == key) & (j + 2 < i))) + ((k3 < key) | ((k3 == key) & (j + 3 < i)));
             }
-#pragma unroll 1
-            for (; j < hi; ++j) {
+            const uint32_t left = hi - j;
+            if (left > 0) {
                 const uint32_t kj = sm.k[scr][j];
                 r += (kj < key) | ((kj == key) & (j < i));
+            }
+            if (left > 1) {
+                const uint32_t kj = sm.k[scr][j + 1];
+                r += (kj < key) | ((kj == key) & (j + 1 < i));
+            }
+            if (left > 2) {
+                const uint32_t kj = sm.k[scr][j + 2];
+                r += (kj < key) | ((kj == key) & (j + 2 < i));
             }
         } else {  // all keys distinct
             // clustered keys (the stencil after its premerge: ~25 per bucket)
@@ -624,8 +633,12 @@ __device__ uint32_t sort_merge_bin(const SortArgs& a, SortSmem& sm, int in, int 
                                k3 = sm.k[scr][j + 3];
                 r += (k0 < key) + (k1 < key) + (k2 < key) + (k3 < key);
             }
-#pragma unroll 1
-            for (; j < hi; ++j) r += sm.k[scr][j] < key;
+            // 0..3 keys left: predicated, no loop (the scalar tail loop was the
+            // kernel's hottest line at C2: 12.5 % of its instructions)
+            const uint32_t left = hi - j;
+            if (left > 0) r += sm.k[scr][j] < key;
+            if (left > 1) r += sm.k[scr][j + 1] < key;
+            if (left > 2) r += sm.k[scr][j + 2] < key;
         }
         if (nodup) {  // final form: masked column ids, C-aligned offsets
             sm.k[in][lo + r + shK] = key & colmask;
