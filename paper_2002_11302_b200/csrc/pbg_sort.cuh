@@ -59,9 +59,13 @@ constexpr int SM_NB = PBG_SM_NB;              // buckets of the MSD pass (u16 co
 constexpr int SM_CQ = SM_NB * 2 / 16 / SM_NT; // uint4s of counters per thread
 constexpr int SM_NB_BITS = __builtin_ctz(SM_NB);
 #ifndef PBG_SM_BMAX
-#define PBG_SM_BMAX 128
+#define PBG_SM_BMAX 512
 #endif
-constexpr int SM_BMAX = PBG_SM_BMAX;          // largest bucket ranked in place
+// largest bucket ranked in place (its rank loop is quadratic; beyond it the bin
+// takes the LSD radix, whose match.any ranking is far slower per key: with 128
+// a C5b band sent 30.8 K heavy sub-bins there — hot columns repeated > 128
+// times — and its sort took 27.4 instead of 26.2 ms)
+constexpr int SM_BMAX = PBG_SM_BMAX;
 // hash pre-merge of a bin when distinct * NUM <= tuples * DEN (tuning hook)
 #ifndef PBG_PM_NUM
 #define PBG_PM_NUM 4

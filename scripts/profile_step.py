@@ -12,6 +12,7 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--bin-cap", type=int, default=0)
 ap.add_argument("--rmat", type=int, nargs=2, metavar=("SCALE", "EF"), default=None,
                 help="C = A*A for a seeded RMAT matrix instead of a config (single pass)")
+ap.add_argument("--row-from", type=float, default=0.0, help="first row of the band, as a fraction of the rows")
 ap.add_argument("--row-band", type=float, default=1.0,
                 help="multiply only the first fraction of A's rows (one bounded round)")
 args = ap.parse_args()
@@ -21,7 +22,8 @@ if args.rmat:
 else:
     a, b = M.make_config(args.config)
 if args.row_band < 1.0:
-    a = M.row_band(a, 0, int(a.nrows * args.row_band))
+    r0 = int(a.nrows * args.row_from)
+    a = M.row_band(a, r0, min(a.nrows, r0 + int(a.nrows * args.row_band)))
 dev = torch.device("cuda", 0)
 t = lambda x, dt: torch.from_numpy(x.view(dt)).to(dev)
 A = (t(a.colptr, np.int64), t(a.rowids, np.int32), t(a.values, np.float64))

@@ -11,6 +11,7 @@ from paper_2002_11302_b200 import api, matrices as M
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--rmat", type=int, nargs=2, default=None)
+ap.add_argument("--row-from", type=float, default=0.0, help="first row of the band, as a fraction of the rows")
 ap.add_argument("--row-band", type=float, default=1.0)
 args = ap.parse_args()
 if args.rmat:
@@ -19,7 +20,8 @@ if args.rmat:
 else:
     a, b = M.make_config(args.config)
 if args.row_band < 1.0:
-    a = M.row_band(a, 0, int(a.nrows * args.row_band))
+    r0 = int(a.nrows * args.row_from)
+    a = M.row_band(a, r0, min(a.nrows, r0 + int(a.nrows * args.row_band)))
 dev = torch.device("cuda", 0)
 t = lambda x, dt: torch.from_numpy(x.view(dt)).to(dev)
 A = (t(a.colptr, np.int64), t(a.rowids, np.int32), t(a.values, np.float64))

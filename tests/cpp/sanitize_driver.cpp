@@ -140,19 +140,21 @@ int main(int argc, char** argv) {
         CHECK(pbgh_stencil27(10, 10, 10, s.ptr.data(), s.idx.data(), s.val.data(), &nnz) == 0);
         multiply("stencil 10^3", csr_to_csc(s), s, 0);
     }
-    if (want("lsd")) {  // one row of 300 clustered columns: MSD bucket > 128 -> LSD
+    if (want("lsd")) {
+        // 5 rows of 700 clustered columns in one bin: 23 key bits, MSD buckets of
+        // 2048 columns, 700 keys in a bucket > SM_BMAX (512) -> LSD radix
         Csx a, b;
         a.nrows = b.ncols = 1u << 20;
         a.ncols = b.nrows = 1;
-        a.ptr = {0, 1};
-        a.idx = {0};
-        a.val = {2.0};
-        b.ptr = {0, 300};
-        for (uint32_t j = 0; j < 300; ++j) {
-            b.idx.push_back(299 - j);
+        a.ptr = {0, 5};
+        a.idx = {0, 1, 2, 3, 4};
+        a.val = {2.0, 3.0, 4.0, 5.0, 6.0};
+        b.ptr = {0, 700};
+        for (uint32_t j = 0; j < 700; ++j) {
+            b.idx.push_back(699 - j);
             b.val.push_back(j + 1.0);
         }
-        multiply("clustered row (LSD)", a, b, 0);
+        multiply("clustered rows (LSD)", a, b, 0);
     }
     if (want("hash")) {
         const Csx a = generate(1, 12, 8, 1);

@@ -416,6 +416,23 @@ def test_distinct_count_paths_on_structured_duplicates():
     check_vs(gpu(a, bnd), oracle.multiply(a, bnd))
 
 
+def test_clustered_keys_rank_in_place_and_lsd_fallback():
+    """One output row whose first 256 columns (one MSD bucket: 20 key bits,
+    256 columns per bucket) receive `copies` tuples each, plus 600 single
+    columns so that the bin is not pre-merged: 512 keys in the bucket are
+    ranked in place (SM_BMAX = 512), 768 switch the bin to the LSD radix."""
+    n = 1 << 20
+    for copies, lsd in ((2, False), (3, True)):
+        k = copies + 1
+        a = M.coo_to_csc(n, k, np.zeros(k, int), np.arange(k), np.arange(2.0, 2.0 + k))
+        rows = np.r_[np.repeat(np.arange(copies), 256), np.full(600, copies)]
+        cols = np.r_[np.tile(np.arange(256), copies), 1000 + np.arange(600)]
+        b = M.coo_to_csr(k, n, rows, cols, np.linspace(1.0, 2.0, rows.size))
+        res = gpu(a, b, bin_cap=4096)  # (small products default to smaller bins)
+        check_vs(res, oracle.multiply(a, b))
+        assert (res.report["sort_fallbacks"] > 0) == lsd, res.report["sort_fallbacks"]
+
+
 def test_tiny_bin_capacity_forces_heavy_split():
     csr = M.make_matrix("er", 11, 8, seed=3)
     a = M.csr_to_csc(csr)
