@@ -378,6 +378,19 @@ def test_rmat_heavy_rows_vs_oracle():
         check_vs(res, oracle.multiply(a, csr))
 
 
+@pytest.mark.parametrize("scale", [13, 15, 17])
+@pytest.mark.parametrize("cap", [64, 1024, 0])
+def test_heavy_split_digits_and_bin_caps(scale, cap):
+    """Heavy-row split over column spaces of 2^13 / 2^15 / 2^17 (split digits
+    of 1, 3 and 5 bits above the 4096-column dense range) and bin capacities
+    from 64 tuples (nearly every row heavy, tiny unaligned sub-bins) up."""
+    csr = M.make_matrix("rmat", scale, 6, seed=100 + scale)
+    a = M.csr_to_csc(csr)
+    res = gpu(a, csr, bin_cap=cap)
+    check_vs(res, oracle.multiply(a, csr))
+    assert_valid_csr(res.c)
+
+
 def test_uniform_key_reduction():
     """One output entry receiving more tuples than a bin holds (6000 > 2048)."""
     K, n = 6000, 512
