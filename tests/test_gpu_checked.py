@@ -77,7 +77,8 @@ def test_checked_build_parity_subset():
     env = dict(os.environ, PBG_LIB="libpbg_checked.so")
     sel = ("golden or known_answers or identity or random_sweep or rectangular or "
            "heavy or uniform_key or tiny_bin or duplicate_and_unsorted or empty_rows or "
-           "widest or coo_conversion or hash_multiply or bounded_memory or expand_row_bands")
+           "widest or coo_conversion or hash_multiply or bounded_memory or expand_row_bands or "
+           "clustered or distinct_count")
     r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests" / "test_gpu_parity.py"),
                         "-m", "gpu and not slow", "-x", "-q", "-p", "no:cacheprovider", "-k", sel],
                        capture_output=True, text=True, timeout=1500, env=env, cwd=str(ROOT))
