@@ -130,7 +130,7 @@ struct pbg_context {
     DevBuf wb[7];
     // row bands (pbg_bands.cuh): row-flop prefix / per-column flop of the
     // whole product, cuts, the current slab of A, checksum words
-    DevBuf bd_zero, bd_rowflop, bd_rowoff, bd_colflop, bd_cuts, sl_cnt, sl_colptr, sl_rowids,
+    DevBuf bd_zero, bd_rowflop, bd_rowoff, bd_colflop, bd_cuts, sl_cnt, sl_wpre, sl_colptr, sl_rowids,
         sl_vals, ck;
     DevBuf alt_rowptr, alt_ccol, alt_cval;  // second C of pbg_multiply_into's overlapped rounds
     size_t zero_bytes = 0;
@@ -172,7 +172,7 @@ struct pbg_context {
         for (auto& b : wb) b.release();
         for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &gen_r, &gen_c, &gen_pos, &gen_stat, &va_colptr, &va_rowids, &va_vals,
                           &vcolflop, &bcuts, &vstat, &bd_zero, &bd_rowflop, &bd_rowoff, &bd_colflop,
-                          &bd_cuts, &sl_cnt, &sl_colptr, &sl_rowids, &sl_vals, &ck, &alt_rowptr,
+                          &bd_cuts, &sl_cnt, &sl_wpre, &sl_colptr, &sl_rowids, &sl_vals, &ck, &alt_rowptr,
                           &alt_ccol, &alt_cval})
             b->release();
         if (ev_ok)
@@ -1230,26 +1230,32 @@ int dev_cuts(pbg_context* ctx, uint32_t lo, uint32_t hi, uint32_t g, cudaStream_
 int dev_slab(pbg_context* ctx, const pbg_csx_view& A, uint32_t r0, uint32_t r1, cudaStream_t st,
              pbg_csx_view* out) {
     using namespace pbg;
-    const uint64_t k = A.ncols;
-    const uint64_t tiles = (k + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    const uint64_t k = A.ncols, nnz = A.nnz;
+    const uint64_t nwords = (nnz + 31) / 32;
+    const uint64_t tiles = (nwords + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
     int rc;
-    if ((rc = grow(ctx->sl_cnt, (k + 1 + 16 + tiles) * 8)) || (rc = grow(ctx->sl_colptr, (k + 2) * 8)))
+    // sl_cnt: word bits | word counts (u32 each) ; sl_wpre: word prefixes + scan status
+    if ((rc = grow(ctx->sl_cnt, (nwords + 1) * 8)) || (rc = grow(ctx->sl_wpre, (nwords + 2 + 16 + tiles) * 8)) ||
+        (rc = grow(ctx->sl_colptr, (k + 2) * 8)))
         return rc;
-    auto* cnt = static_cast<uint64_t*>(ctx->sl_cnt.p);
-    auto* zb = reinterpret_cast<unsigned long long*>(cnt + k + 1);  // ticket, total, status
+    auto* bits = static_cast<uint32_t*>(ctx->sl_cnt.p);
+    auto* wcnt = bits + nwords;
+    auto* wpre = static_cast<uint64_t*>(ctx->sl_wpre.p);
+    auto* zb = reinterpret_cast<unsigned long long*>(wpre + nwords + 2);  // ticket, total, status
     auto* colptr = static_cast<uint64_t*>(ctx->sl_colptr.p);
     CUDA_TRY(cudaMemsetAsync(zb, 0, (16 + tiles) * 8, st));
-    if (k) k_slab_count<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, k, r0, r1, cnt);
-    launch_scan(ArrayIn{cnt}, colptr, k, nullptr, k, zb + 16, reinterpret_cast<unsigned int*>(zb),
+    if (nnz) k_slab_bits<<<blocks_for(nnz, 256), 256, 0, st>>>(A.idx, nnz, r0, r1, bits, wcnt);
+    launch_scan(ArrayIn32{wcnt}, wpre, nwords, nullptr, nwords, zb + 16, reinterpret_cast<unsigned int*>(zb),
                 zb + 8, nullptr, st);
+    k_slab_colptr<<<blocks_for(k + 1, 256), 256, 0, st>>>(A.ptr, k, nnz, bits, wpre, colptr);
     uint64_t total = 0;
-    CUDA_TRY(cudaMemcpyAsync(&total, colptr + k, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&total, wpre + nwords, 8, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if ((rc = grow(ctx->sl_rowids, total * 4 + 16)) || (rc = grow(ctx->sl_vals, total * 8 + 16))) return rc;
-    if (k)
-        k_slab_copy<<<blocks_for(k, 256), 256, 0, st>>>(
-            A.ptr, A.idx, A.val, k, r0, r1, colptr, static_cast<uint32_t*>(ctx->sl_rowids.p),
-            static_cast<double*>(ctx->sl_vals.p));
+    if (nnz)
+        k_slab_gather<<<blocks_for(nnz, 256), 256, 0, st>>>(A.idx, A.val, nnz, r0, bits, wpre,
+                                                           static_cast<uint32_t*>(ctx->sl_rowids.p),
+                                                           static_cast<double*>(ctx->sl_vals.p));
     *out = pbg_csx_view{r1 - r0, A.ncols, total, colptr,
                         static_cast<const uint32_t*>(ctx->sl_rowids.p),
                         static_cast<const double*>(ctx->sl_vals.p)};
