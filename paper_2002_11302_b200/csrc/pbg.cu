@@ -126,7 +126,7 @@ struct pbg_context {
         child_pos, hstat, wcnt, wpos, wb_nnz, wb_out, hflop, hbound, hcolcnt, hzero, hdense;
     DevBuf items[2][8];
     DevBuf row_pack, tile_pos, tile_item, hv_hist, gen_r, gen_c, gen_pos, gen_stat;
-    DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat;
+    DevBuf va_colptr, va_rowids, va_vals, vcolflop, bcuts, vstat, vbits, vwpre;
     DevBuf wb[7];
     // row bands (pbg_bands.cuh): row-flop prefix / per-column flop of the
     // whole product, cuts, the current slab of A, checksum words
@@ -171,7 +171,7 @@ struct pbg_context {
             for (auto& b : set) b.release();
         for (auto& b : wb) b.release();
         for (DevBuf* b : {&row_pack, &tile_pos, &tile_item, &hv_hist, &gen_r, &gen_c, &gen_pos, &gen_stat, &va_colptr, &va_rowids, &va_vals,
-                          &vcolflop, &bcuts, &vstat, &bd_zero, &bd_rowflop, &bd_rowoff, &bd_colflop,
+                          &vcolflop, &bcuts, &vstat, &vbits, &vwpre, &bd_zero, &bd_rowflop, &bd_rowoff, &bd_colflop,
                           &bd_cuts, &sl_cnt, &sl_wpre, &sl_colptr, &sl_rowids, &sl_vals, &ck, &alt_rowptr,
                           &alt_ccol, &alt_cval})
             b->release();
@@ -498,15 +498,28 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
             auto* vst = static_cast<unsigned long long*>(ctx->vstat.p);
             CUDA_TRY(cudaMemsetAsync(vst, 0, (2 * vt + 16) * 8, st));
             k_band_cuts<<<1, 32, 0, st>>>(bin_rs, reinterpret_cast<const uint64_t*>(sc + S_NBINS), g, bc);
-            k_band_count<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, k, bc, g, vcp);
-            launch_scan(ArrayIn{vcp}, vcp, kv, nullptr, kv, vst + 16, reinterpret_cast<unsigned int*>(vst),
-                        nullptr, nullptr, st);
-            k_band_copy<<<blocks_for(k, 256), 256, 0, st>>>(A.ptr, A.idx, A.val, k, bc, g, vcp,
-                                                            static_cast<uint32_t*>(ctx->va_rowids.p),
-                                                            static_cast<double*>(ctx->va_vals.p));
+            {
+                const uint64_t nwords = (nnz_a + 31) / 32, gw = nwords * static_cast<uint64_t>(g);
+                const uint64_t wt = (gw + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+                if ((rc = grow(ctx->vbits, (gw + 1) * 8))) return rc;           // word bits | word counts
+                if ((rc = grow(ctx->vwpre, (gw + 2 + 16 + wt) * 8))) return rc;  // prefixes + scan status
+                auto* bits = static_cast<uint32_t*>(ctx->vbits.p);
+                auto* wcnt = bits + gw;
+                auto* wpre = static_cast<uint64_t*>(ctx->vwpre.p);
+                auto* wst = reinterpret_cast<unsigned long long*>(wpre + gw + 2);
+                CUDA_TRY(cudaMemsetAsync(wst, 0, (16 + wt) * 8, st));
+                k_band_bits<<<std::min<unsigned>(blocks_for(nnz_a, 256), 16u * ctx->num_sms), 256, 0, st>>>(
+                    A.idx, nnz_a, nwords, bc, g, bits, wcnt);
+                launch_scan(ArrayIn32{wcnt}, wpre, gw, nullptr, gw, wst + 16,
+                            reinterpret_cast<unsigned int*>(wst), nullptr, nullptr, st);
+                k_band_colptr<<<blocks_for(kv + 1, 256), 256, 0, st>>>(A.ptr, k, nnz_a, nwords, g, bits, wpre, vcp);
+                k_band_gather<<<blocks_for(nnz_a, 256), 256, 0, st>>>(
+                    A.idx, A.val, nnz_a, nwords, bc, g, bits, wpre, static_cast<uint32_t*>(ctx->va_rowids.p),
+                    static_cast<double*>(ctx->va_vals.p));
+            }
             launch_scan(VColFlopIn{vcp, B.ptr, k}, vcf, kv, nullptr, kv, vst + 16 + vt,
                         reinterpret_cast<unsigned int*>(vst) + 2, nullptr, nullptr, st);
-            L += 5;
+            L += 6;
             xa_colptr = vcp;
             xa_rowids = static_cast<const uint32_t*>(ctx->va_rowids.p);
             xa_vals = static_cast<const double*>(ctx->va_vals.p);
@@ -1244,7 +1257,9 @@ int dev_slab(pbg_context* ctx, const pbg_csx_view& A, uint32_t r0, uint32_t r1, 
     auto* zb = reinterpret_cast<unsigned long long*>(wpre + nwords + 2);  // ticket, total, status
     auto* colptr = static_cast<uint64_t*>(ctx->sl_colptr.p);
     CUDA_TRY(cudaMemsetAsync(zb, 0, (16 + tiles) * 8, st));
-    if (nnz) k_slab_bits<<<blocks_for(nnz, 256), 256, 0, st>>>(A.idx, nnz, r0, r1, bits, wcnt);
+    if (nnz)
+        k_slab_bits<<<std::min<unsigned>(blocks_for(nnz, 256), 16u * ctx->num_sms), 256, 0, st>>>(A.idx, nnz, r0, r1,
+                                                                                              bits, wcnt);
     launch_scan(ArrayIn32{wcnt}, wpre, nwords, nullptr, nwords, zb + 16, reinterpret_cast<unsigned int*>(zb),
                 zb + 8, nullptr, st);
     k_slab_colptr<<<blocks_for(k + 1, 256), 256, 0, st>>>(A.ptr, k, nnz, bits, wpre, colptr);

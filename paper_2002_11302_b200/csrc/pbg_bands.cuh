@@ -92,16 +92,28 @@ __global__ void k_ref_layout_uniform(const uint64_t* __restrict__ row_off, uint6
 // this one reads the row ids once.)
 __global__ void k_slab_bits(const uint32_t* __restrict__ a_rowids, uint64_t nnz, uint32_t r0,
                             uint32_t r1, uint32_t* bits, uint32_t* wcnt) {
-    const uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    bool in = false;
-    if (p < nnz) {
-        const uint32_t r = __ldcs(a_rowids + p);
-        in = r >= r0 && r < r1;
-    }
-    const uint32_t b = __ballot_sync(FULL, in);
-    if ((threadIdx.x & 31) == 0 && p < nnz) {
-        bits[p >> 5] = b;
-        wcnt[p >> 5] = __popc(b);
+    // a warp takes 32 words (1024 entries) per trip: lane i keeps the ballot of
+    // the trip's i-th word, so the words leave as coalesced 128-byte stores
+    const int lane = threadIdx.x & 31;
+    const uint64_t nwords = (nnz + 31) >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w0 = warp * 32; w0 < nwords; w0 += nwarps * 32) {
+        uint32_t mine = 0;
+        for (int i = 0; i < 32; ++i) {
+            const uint64_t p = (w0 + i) * 32 + lane;
+            bool in = false;
+            if (p < nnz) {
+                const uint32_t r = __ldcs(a_rowids + p);
+                in = r >= r0 && r < r1;
+            }
+            const uint32_t b = __ballot_sync(FULL, in);
+            if (lane == i) mine = b;
+        }
+        if (w0 + lane < nwords) {
+            bits[w0 + lane] = mine;
+            wcnt[w0 + lane] = __popc(mine);
+        }
     }
 }
 

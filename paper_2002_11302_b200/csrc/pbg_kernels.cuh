@@ -745,56 +745,88 @@ __device__ __forceinline__ int band_of(uint32_t r, const uint32_t* __restrict__ 
 
 constexpr int BAND_MAX = 16;
 
-// A(band s rows, j) counts, one pass over each column (per-band counters in
-// registers). Row ids inside a column need not be sorted.
-__global__ void k_band_count(const uint64_t* __restrict__ a_colptr,
-                             const uint32_t* __restrict__ a_rowids, uint64_t k,
-                             const uint32_t* __restrict__ cuts, int g, uint64_t* vcnt) {
+// Band-major re-ordering of A (virtual column v = band * k + j), entry-
+// parallel like the row slabs of pbg_bands.cuh: per band one selection bit per
+// entry (one word per 32 entries), ONE scan over the band-major sequence of
+// word popcounts (so a word's prefix is its place in the re-ordered arrays),
+// the virtual column pointers by lookup, a stable coalesced gather. (The
+// first version walked every column with one thread in a counting and a
+// copying kernel, with a scan over all G * k virtual columns between them:
+// 2.2 ms of C5a's expand phase.)
+__global__ void k_band_bits(const uint32_t* __restrict__ a_rowids, uint64_t nnz, uint64_t nwords,
+                            const uint32_t* __restrict__ cuts, int g, uint32_t* bits, uint32_t* wcnt) {
     __shared__ uint32_t s_cuts[BAND_MAX + 1];
     if (threadIdx.x <= g) s_cuts[threadIdx.x] = cuts[threadIdx.x];
     __syncthreads();
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= k) return;
-    const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
-    uint32_t c[BAND_MAX];
+    // a warp takes 32 words (1024 entries) per trip: lane i keeps the ballots
+    // of the trip's i-th word, so the words leave as coalesced 128-byte stores
+    // (one 4-byte store per word and band by lane 0 ran at 0.7 TB/s)
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w0 = warp * 32; w0 < nwords; w0 += nwarps * 32) {
+        uint32_t mine[BAND_MAX];
 #pragma unroll
-    for (int s = 0; s < BAND_MAX; ++s) c[s] = 0;
-    for (uint64_t p = p0; p < p1; ++p) {
-        const int bnd = band_of(a_rowids[p], s_cuts, g);
+        for (int s = 0; s < BAND_MAX; ++s) mine[s] = 0;
+        for (int i = 0; i < 32; ++i) {
+            const uint64_t p = (w0 + i) * 32 + lane;
+            const int bnd = p < nnz ? band_of(__ldcs(a_rowids + p), s_cuts, g) : -1;
 #pragma unroll
-        for (int s = 0; s < BAND_MAX; ++s) c[s] += bnd == s;
+            for (int s = 0; s < BAND_MAX; ++s) {
+                if (s < g) {
+                    const uint32_t b = __ballot_sync(FULL, bnd == s);
+                    if (lane == i) mine[s] = b;
+                }
+            }
+        }
+        if (w0 + lane < nwords) {
+#pragma unroll
+            for (int s = 0; s < BAND_MAX; ++s) {
+                if (s < g) {
+                    bits[static_cast<uint64_t>(s) * nwords + w0 + lane] = mine[s];
+                    wcnt[static_cast<uint64_t>(s) * nwords + w0 + lane] = __popc(mine[s]);
+                }
+            }
+        }
     }
-#pragma unroll
-    for (int s = 0; s < BAND_MAX; ++s)
-        if (s < g) vcnt[static_cast<uint64_t>(s) * k + j] = c[s];
 }
 
-// Band-major copy of A (stable inside each column), one pass per column.
-__global__ void k_band_copy(const uint64_t* __restrict__ a_colptr,
-                            const uint32_t* __restrict__ a_rowids,
-                            const double* __restrict__ a_vals, uint64_t k,
-                            const uint32_t* __restrict__ cuts, int g,
-                            const uint64_t* __restrict__ va_colptr, uint32_t* va_rowids,
-                            double* va_vals) {
+// va_colptr[v] for v = band * k + j (v = 0 .. g*k): entries of the bands before
+// `band` plus the band's entries before a_colptr[j]
+__global__ void k_band_colptr(const uint64_t* __restrict__ a_colptr, uint64_t k, uint64_t nnz,
+                              uint64_t nwords, int g, const uint32_t* __restrict__ bits,
+                              const uint64_t* __restrict__ wpre, uint64_t* va_colptr) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t kv = k * static_cast<uint64_t>(g);
+    if (v > kv) return;
+    if (v == kv) {
+        va_colptr[v] = wpre[static_cast<uint64_t>(g) * nwords];
+        return;
+    }
+    const uint64_t s = v / k, j = v - s * k;
+    const uint64_t p = a_colptr[j];
+    if (p >= nnz) {
+        va_colptr[v] = wpre[(s + 1) * nwords];  // the band's end
+        return;
+    }
+    const uint64_t w = s * nwords + (p >> 5);
+    va_colptr[v] = wpre[w] + __popc(bits[w] & ((1u << (p & 31u)) - 1u));
+}
+
+__global__ void k_band_gather(const uint32_t* __restrict__ a_rowids, const double* __restrict__ a_vals,
+                              uint64_t nnz, uint64_t nwords, const uint32_t* __restrict__ cuts, int g,
+                              const uint32_t* __restrict__ bits, const uint64_t* __restrict__ wpre,
+                              uint32_t* va_rowids, double* va_vals) {
     __shared__ uint32_t s_cuts[BAND_MAX + 1];
     if (threadIdx.x <= g) s_cuts[threadIdx.x] = cuts[threadIdx.x];
     __syncthreads();
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= k) return;
-    const uint64_t p0 = a_colptr[j], p1 = a_colptr[j + 1];
-    uint64_t d[BAND_MAX];
-#pragma unroll
-    for (int s = 0; s < BAND_MAX; ++s) d[s] = s < g ? va_colptr[static_cast<uint64_t>(s) * k + j] : 0;
-    for (uint64_t p = p0; p < p1; ++p) {
-        const uint32_t r = a_rowids[p];
-        const int bnd = band_of(r, s_cuts, g);
-        uint64_t q = 0;
-#pragma unroll
-        for (int s = 0; s < BAND_MAX; ++s)
-            if (bnd == s) q = d[s]++;
-        va_rowids[q] = r;
-        va_vals[q] = a_vals[p];
-    }
+    const uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (p >= nnz) return;
+    const uint32_t r = a_rowids[p];
+    const uint64_t w = static_cast<uint64_t>(band_of(r, s_cuts, g)) * nwords + (p >> 5);
+    const uint64_t at = wpre[w] + __popc(bits[w] & lanemask_lt());
+    va_rowids[at] = r;
+    va_vals[at] = a_vals[p];
 }
 
 __global__ void k_band_cuts(const uint32_t* __restrict__ bin_rs, const uint64_t* nb_dev, int g,
