@@ -753,9 +753,8 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
         // rows (the stencil, > 512 products per output row on average) and
         // heavy rows (RMAT) are duplicate-heavy and keep the 3-CTA shape
         const bool big_table = H == 0 && flop <= 512 * m;
-        static const bool cnt_v1 = getenv("PBG_CNT_V1") && atoi(getenv("PBG_CNT_V1")) != 0;  // A/B hook: round-1 kernel
         auto launch_count = [&](auto kern, int nt, size_t smem, int shape) -> int {
-            static std::atomic<bool> attr_set[4][64] = {};  // [kernel x shape][device]
+            static std::atomic<bool> attr_set[2][64] = {};  // [shape][device]
             if (!attr_set[shape][ctx->device & 63]) {
                 CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(smem)));
@@ -771,13 +770,7 @@ int run_pipeline_impl(pbg_context* ctx, const pbg_csx_view& A, const pbg_csx_vie
                    nt, smem, st>>>(keys, hc.skeys, w, nw_dev, cap, wb_nnz);
             return PBG_OK;
         };
-        if (cnt_v1) {
-            if (big_table) {
-                if ((rc = launch_count(k_bincount<1024, 27648>, 1024, 27648 * 4, 3))) return rc;
-            } else {
-                if ((rc = launch_count(k_bincount<512, 16384>, 512, 16384 * 4, 2))) return rc;
-            }
-        } else if (big_table) {
+        if (big_table) {
             if ((rc = launch_count(k_bincount2<1024, 27648>, 1024, (27648 + 32) * 4, 1))) return rc;
         } else {
             if ((rc = launch_count(k_bincount2<512, 16384>, 512, (16384 + 32) * 4, 0))) return rc;

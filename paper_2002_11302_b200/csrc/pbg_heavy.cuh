@@ -816,94 +816,7 @@ __global__ void k_work_fill_items(const uint64_t* __restrict__ wpos,
 // the host picks the shape from the bin statistics (CountShape below).
 constexpr uint32_t CNT_EMPTY = 0xffffffffu;
 
-template <int NT>
-__device__ __forceinline__ void cnt_load(const uint32_t* __restrict__ keys,
-                                         const uint32_t* __restrict__ skeys, const WorkBins& w,
-                                         uint64_t b, uint64_t nw, uint64_t cap,
-                                         uint32_t (&kk)[4096 / NT], uint32_t& n) {
-    constexpr int PER = 4096 / NT;  // keys per thread: bins of up to 4096 tuples
-    n = 0;
-    if (b >= nw) return;
-    const uint32_t fl = w.flags[b];
-    const uint64_t nn = w.n[b];
-    if ((fl & 2u) || nn > cap) return;
-    n = static_cast<uint32_t>(nn);
-    const uint32_t* kb = ((fl & 1u) ? skeys : keys) + w.off[b];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const uint32_t i = threadIdx.x + j * NT;
-        kk[j] = i < n ? __ldcs(kb + i) : CNT_EMPTY;
-    }
-}
-
-template <int NT, int SLOTS>
-__global__ void __launch_bounds__(NT) k_bincount(const uint32_t* __restrict__ keys,
-                                                 const uint32_t* __restrict__ skeys, WorkBins w,
-                                                 const uint64_t* nw_dev, uint64_t cap,
-                                                 uint64_t* wb_nnz) {
-    constexpr int PER = 4096 / NT;
-    static_assert(SLOTS % 4 == 0, "table cleared in uint4s");
-    extern __shared__ __align__(16) uint32_t table[];  // SLOTS
-    __shared__ uint32_t s_red[2][NT / 32];
-    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    const uint64_t nw = *nw_dev;
-    for (int i = tid; i < SLOTS / 4; i += NT)
-        reinterpret_cast<uint4*>(table)[i] = make_uint4(CNT_EMPTY, CNT_EMPTY, CNT_EMPTY, CNT_EMPTY);
-    __syncthreads();
-    int par = 0;
-    uint32_t kk[PER], n;
-    uint64_t b = blockIdx.x;
-    cnt_load<NT>(keys, skeys, w, b, nw, cap, kk, n);  // software pipeline: keys of bin b
-    for (; b < nw; b += gridDim.x) {
-        uint32_t cur[PER];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) cur[j] = kk[j];
-        const uint32_t ncur = n;
-        const uint32_t fl = w.flags[b];
-        cnt_load<NT>(keys, skeys, w, b + gridDim.x, nw, cap, kk, n);  // next bin's keys in flight
-        uint32_t slot[PER];
-        uint32_t fresh = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            slot[j] = SLOTS;  // none
-            if (tid + j * NT < ncur) {
-                const uint32_t key = cur[j];
-                // multiply-shift onto [0, SLOTS) (any table size)
-                uint32_t h = static_cast<uint32_t>(
-                    (static_cast<uint64_t>(key * 0x9E3779B1u) * SLOTS) >> 32);
-                while (true) {
-                    const uint32_t old = atomicCAS(&table[h], CNT_EMPTY, key);
-                    if (old == CNT_EMPTY) {
-                        ++fresh;
-                        slot[j] = h;
-                        break;
-                    }
-                    if (old == key) break;
-                    h = h + 1 == SLOTS ? 0u : h + 1;
-                }
-            }
-        }
-        fresh = warp_sum(fresh);
-        if (lane == 0) s_red[par][wp] = fresh;
-        __syncthreads();
-        // reset only the slots this thread claimed: the table is clean for the
-        // next bin without a full clear
-#pragma unroll
-        for (int j = 0; j < PER; ++j)
-            if (slot[j] < SLOTS) table[slot[j]] = CNT_EMPTY;
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int i = 0; i < NT / 32; ++i) t += s_red[par][i];
-            // merged items are already distinct; a valid list has no other
-            // bin above the capacity
-            wb_nnz[b] = (fl & 2u) ? w.n[b] : t;
-        }
-        par ^= 1;
-        __syncthreads();
-    }
-}
-
-// Pipelined count k_bincount2 (same result as k_bincount, C2 1.15 -> 1.01
+// Pipelined count k_bincount2 (same result as the round-1 kernel k_bincount, C2 1.15 -> 1.01
 // ms). The per-bin critical path of k_bincount held two dependent global
 // round trips (descriptor -> key address -> keys), every thread's probes ran
 // one after another behind a branch per key, and one thread summed the warp
