@@ -152,6 +152,28 @@ def test_device_band_cuts_follow_the_host_rule_and_bands_assemble():
             assert abs(ck[3] - full_ck[3]) <= 1e-9 * abs(full_ck[3])
 
 
+def test_device_row_slab_equals_host_row_band():
+    """pbg_row_slab_device (selection bits, word scan, lookups, stable gather)
+    against the host's row band, entry for entry: RMAT hub columns, an empty
+    band, single rows, the whole matrix, nnz not a multiple of 32."""
+    rng = np.random.default_rng(11)
+    for kind, scale, ef in (("rmat", 12, 9), ("er", 10, 5)):
+        csr = M.make_matrix(kind, scale, ef, seed=7)
+        a = M.csr_to_csc(csr)
+        A, _ = _upload(a, csr)
+        ctx = api.DeviceContext(0)
+        va = ctx.view(a.nrows, a.ncols, *A)
+        n = a.nrows
+        cuts = [(0, n), (0, 0), (n, n), (5, 6), (n - 1, n), (0, n // 3), (n // 3, n - 7)]
+        cuts += [tuple(sorted(int(x) for x in rng.integers(0, n + 1, 2))) for _ in range(6)]
+        for r0, r1 in cuts:
+            (cp, ri, vv), _view = ctx.row_slab(va, r0, r1)
+            ref = M.row_band(a, r0, r1)
+            assert np.array_equal(cp.cpu().numpy().astype(np.uint64), ref.colptr), (kind, r0, r1)
+            assert np.array_equal(ri.cpu().numpy().astype(np.uint32), ref.rowids), (kind, r0, r1)
+            assert np.array_equal(vv.cpu().numpy(), ref.values), (kind, r0, r1)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
