@@ -602,6 +602,9 @@ __global__ void __launch_bounds__(HV_PT) k_hv_children(HeavyCtx c, Items in, uin
 // parity-green, and measured slower: 20.2 vs 13.1 ms on a C3 round, eight
 // barriers per 4096-tuple batch against none here.)
 constexpr int HV_DENSE = 1 << HV_DENSE_BITS;
+#ifndef PBG_DENSE_DU
+#define PBG_DENSE_DU 4  // tuples a thread loads before their adds (8: +0.4 ms, 16: +2.6 ms per C3 round)
+#endif
 #ifndef PBG_DENSE_COPIES
 #define PBG_DENSE_COPIES 2
 #endif
@@ -631,9 +634,9 @@ __global__ void __launch_bounds__(HV_NT) k_hv_dense(HeavyCtx c, Items it, uint64
         for (int q = tid; q < HV_DC * HV_DENSE; q += HV_NT) acc_all[q] = -0.0;
         for (int q = tid; q < HV_DENSE; q += HV_NT) seen[q] = 0;
         __syncthreads();
-        // 8 tuples per thread in flight: the loads of a batch are issued
+        // DU tuples per thread in flight: the loads of a batch are issued
         // before its shared-memory adds
-        constexpr int DU = 8;
+        constexpr int DU = PBG_DENSE_DU;
         for (uint64_t q0 = 0; q0 < n; q0 += static_cast<uint64_t>(DU) * HV_NT) {
             uint32_t ks[DU];
             double vs[DU];
