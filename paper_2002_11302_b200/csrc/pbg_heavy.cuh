@@ -291,6 +291,7 @@ constexpr int HV_PB = (1 << HV_MAXD) / HV_PT;  // 4
 struct PlanSmem {
     uint32_t st[(1 << HV_MAXD) + 1];  // bucket starts (exclusive), st[nbk] = n
     uint32_t fl[1 << HV_MAXD];        // child index << 1 | starts-a-child
+    uint16_t nx[1 << HV_MAXD];        // greedy grouping: the bucket starting the next child
     uint32_t s_warp[HV_PT / 32 + 1];
 };
 __device__ uint32_t hv_plan_item(PlanSmem& sm, const uint32_t* cnt_g, uint32_t nbk, uint64_t cap) {
@@ -313,32 +314,66 @@ __device__ uint32_t hv_plan_item(PlanSmem& sm, const uint32_t* cnt_g, uint32_t n
     if (tid == 0) sm.st[nbk] = tot;
     __syncthreads();
 #if PBG_HV_GREEDY
-    // greedy grouping by one thread: a child takes consecutive buckets while
-    // their sum stays <= cap (children ~cap/2 on average under the window
-    // rule below; fuller children mean fewer work bins for the count and
-    // sort kernels). <= 1024 buckets per item: microseconds.
-    if (tid == 0) {
-        uint32_t run = 0, ci = 0;
-        bool open = false;
-        for (uint32_t q = 0; q < nbk; ++q) {
-            const uint32_t vq = sm.st[q + 1] - sm.st[q];
-            uint32_t f = 0;
-            if (vq) {
-                if (!open || run + static_cast<uint64_t>(vq) > cap) {
-                    f = 1;
-                    run = vq;
-                    open = true;
-                } else {
-                    run += vq;
-                }
-            }
-            sm.fl[q] = (ci << 1) | f;
-            ci += f;
+    // greedy grouping: a child takes consecutive buckets while their sum stays
+    // <= cap (children ~cap/2 on average under the window rule below; fuller
+    // children mean fewer work bins for the count and sort kernels). Every
+    // non-empty bucket finds by two binary searches over the prefix where a
+    // child starting at it would end and which non-empty bucket starts the
+    // next one; one thread then follows these links from the first non-empty
+    // bucket (one step per CHILD; walking all <= 1024 buckets serially cost
+    // 2.8 % of C3's late rounds in k_hv_plan + k_hv_children).
+    for (uint32_t q = tid; q < nbk; q += HV_PT) sm.fl[q] = 0;
+#pragma unroll
+    for (int j = 0; j < HV_PB; ++j) {
+        const uint32_t q = tid * HV_PB + j;
+        if (q >= nbk || !v[j]) continue;
+        const uint64_t limit = static_cast<uint64_t>(sm.st[q]) + cap;
+        // e = largest index in (q, nbk] with st[e] <= limit, at least q + 1
+        uint32_t lo = q + 1, hi = nbk;  // invariant: answer in [lo, hi]
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi + 1) >> 1;
+            if (sm.st[mid] <= limit) lo = mid;
+            else hi = mid - 1;
         }
-        sm.s_warp[0] = ci;
+        const uint32_t e = lo;
+        // next start: the first non-empty bucket >= e, i.e. one below the first
+        // prefix above st[e]; nbk if none
+        const uint32_t se = sm.st[e];
+        uint32_t a = e + 1, b = nbk + 1;  // first index in [e + 1, nbk] with st > se, else nbk + 1
+        while (a < b) {
+            const uint32_t mid = (a + b) >> 1;
+            if (sm.st[mid] > se) b = mid;
+            else a = mid + 1;
+        }
+        sm.nx[q] = static_cast<uint16_t>(a <= nbk ? a - 1 : nbk);
     }
     __syncthreads();
-    const uint32_t nchild = sm.s_warp[0];
+    if (tid == 0) {
+        // first non-empty bucket: one below the first prefix above 0
+        uint32_t a = 1, b = nbk + 1;
+        while (a < b) {
+            const uint32_t mid = (a + b) >> 1;
+            if (sm.st[mid] > 0) b = mid;
+            else a = mid + 1;
+        }
+        for (uint32_t q = a <= nbk ? a - 1 : nbk; q < nbk; q = sm.nx[q]) sm.fl[q] = 1;
+    }
+    __syncthreads();
+    uint32_t starts = 0, f[HV_PB];
+#pragma unroll
+    for (int j = 0; j < HV_PB; ++j) {
+        const uint32_t q = tid * HV_PB + j;
+        f[j] = q < nbk ? sm.fl[q] : 0u;
+        starts += f[j];
+    }
+    uint32_t nchild;
+    uint32_t ci = block_exclusive_scan<HV_PT>(starts, sm.s_warp, nchild);
+#pragma unroll
+    for (int j = 0; j < HV_PB; ++j) {
+        const uint32_t q = tid * HV_PB + j;
+        if (q < nbk) sm.fl[q] = (ci << 1) | f[j];
+        ci += f[j];
+    }
     __syncthreads();
     return nchild;
 #else
